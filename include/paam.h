@@ -1,0 +1,193 @@
+/* paam.h -- C ABI of the B200-native PAAM response-time analyser and arbitration simulator.
+ *
+ * What the library computes (PAPER.md = /root/reference/PAPER.md, "P:<line>"; SPEC.md "S:<line>"):
+ *   For every chain set ("SystemConfig") of a batch, the worst-case end-to-end response
+ *   time (WCRT) of every processing chain whose callbacks run on
+ *   single-threaded, non-preemptive, priority-driven executors (PiCAS) and send their
+ *   accelerator segments to a PAAM server (bucket downsampling P:279, rules R1-R4 P:366-373):
+ *     Eq.1  H*_c = H_c + sum eps
+ *     Eq.2  mu(t) = ceil(t/T) + 1                        (Lemma 1)
+ *     Eq.3  per-segment handling-time fixed point        (Lemma 2)
+ *     Eq.4  per-chain handling time, union of hps        (Lemma 3)
+ *     H_c = min(Eq.3 summed, Eq.4)
+ *     Eq.5  chain WCRT fixed point                       (Theorem 1)
+ *     R*   = sum of sub-chain R_c + comm per crossing
+ *   and the set's schedulability verdict (admission test).  The readings taken where the
+ *   paper is silent or garbled are listed in DESIGN.md ("Readings", A1-A16).
+ *   paam_simulate runs the discrete-event simulation of the PAAM arbitration (App. A
+ *   rules D1-D17) and checks observed response times against the bounds.
+ *
+ * Conventions.
+ *   - Every time is an unsigned 64-bit integer number of nanoseconds.  Each individual
+ *     period, deadline, WCET, eps, kappa and comm cost must be < 2^31 ns (about 2.1 s): the device
+ *     path computes in 32-bit integers with sums saturating just above the deadline, which is exact
+ *     because any value above the deadline is a miss.
+ *   - Indices inside a set are set-local (executor, accelerator, unit); CSR offset arrays are global.
+ *   - All calls are asynchronous on the given CUDA stream unless stated otherwise; none of them
+ *     synchronises the device except paam_pack with host-resident input (it must wait for the copy
+ *     before it may free its staging buffers) and the query paam_sets_info.
+ *   - The caller owns every input and output buffer.  The library owns the opaque paam_sets handle
+ *     (device memory) until paam_free.
+ *   - Return value: 0 = OK, negative = the whole call failed (PAAM_E*).  Per-set validation failures
+ *     do not fail the call; they are reported per set through out_status (PAAM_SET_*), and such a set
+ *     gets sched = 0 and every WCRT = PAAM_UNSCHED.
+ */
+#ifndef PAAM_H
+#define PAAM_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* paam_stream_t; /* a cudaStream_t (may be NULL = legacy default stream) */
+
+/* ---- call-level return codes -------------------------------------------------------------- */
+#define PAAM_OK 0
+#define PAAM_EINVAL -1 /* bad argument (NULL pointer, n == 0 where not allowed, bad flag, ...) */
+#define PAAM_ECUDA -2  /* a CUDA runtime call failed; paam_last_error() has the detail */
+#define PAAM_ENOMEM -3 /* device allocation failed */
+#define PAAM_ERANGE -4 /* batch-level size out of range (e.g. more than 2^32-1 chains) */
+
+/* ---- per-set validation status (out_status[i]) -------------------------------------------- */
+/* Checked in this order; the first failing rule is reported. */
+#define PAAM_SET_OK 0
+#define PAAM_SET_ERANGE 1    /* over the size caps below, T == 0, or a time >= 2^31 ns */
+#define PAAM_SET_EDANGLING 2 /* chain without callbacks, callback without segments, executor or
+                                unit index out of range */
+#define PAAM_SET_EACCEL 3    /* ACCEL segment on an undeclared accelerator */
+#define PAAM_SET_ESHAPE 4    /* segment WCET == 0, CPU/ACCEL segments do not alternate, or a
+                                chain revisits an executor non-contiguously (A13) */
+#define PAAM_SET_EDUPPRIO 5  /* duplicate chain priority or duplicate process priority of
+                                two executors on one core */
+#define PAAM_SET_EDEADLINE 6 /* CRITICAL chain with D > T or D == 0 (P:128 constrained deadlines) */
+#define PAAM_SET_ECORE 7     /* an accelerator's server core hosts a client executor (R1) */
+
+/* ---- per-set size caps (one set = one warp, record staged in shared memory) ---------------- */
+#define PAAM_MAX_CHAINS 32
+#define PAAM_MAX_SUBCHAINS 32
+#define PAAM_MAX_CALLBACKS 64
+#define PAAM_MAX_ACCEL_SEGS 64
+#define PAAM_MAX_SEGMENTS 192
+#define PAAM_MAX_EXECUTORS 32
+#define PAAM_MAX_ACCELS 4
+#define PAAM_MAX_UNITS 8   /* summed over the set's accelerators */
+#define PAAM_MAX_BUCKETS 32
+
+#define PAAM_UNSCHED UINT64_MAX /* WCRT of a chain whose fixed point exceeds its deadline */
+
+/* ---- flags (paam_batch.flags) --------------------------------------------------------------- */
+#define PAAM_MEM_HOST 0
+#define PAAM_MEM_DEVICE 1
+#define PAAM_FLAG_BLOCKING_SOUND 0x1u /* B_c charges an LP callback's accelerator handling time
+                                          (SURVEY.md §8(c) A10); default = the paper's B_c */
+
+/* Raw batch: the paper's system model as flat CSR arrays.  `mem` says whether the
+ * pointers are host or device memory.  Sizes n_chains..n_accels are the totals (= last entries
+ * of the offset arrays).  Layout per set i:
+ *   chains     [set_chain_off[i], set_chain_off[i+1])  : T, D, priority (unique, larger = higher),
+ *                                                        class (0 CRITICAL, 1 BEST_EFFORT)
+ *   callbacks of chain g [chain_cb_off[g], chain_cb_off[g+1]), in chain order
+ *   segments of callback j [cb_seg_off[j], cb_seg_off[j+1]): kind 0 CPU / 1 ACCEL, WCET, and for
+ *                                                        ACCEL the set-local accelerator and unit
+ *   executors  [set_exec_off[i], set_exec_off[i+1])    : core, process priority (unique per core,
+ *                                                        larger = higher), wait 0 SUSPEND / 1 SPIN
+ *   accelerators [set_accel_off[i], ...)                : buckets n (>1 = preemptive GPU-like,
+ *                                                        1 = TPU-like), units, server core, eps, kappa
+ */
+typedef struct {
+  uint32_t n_sets;
+  int32_t mem; /* PAAM_MEM_HOST | PAAM_MEM_DEVICE */
+  uint32_t n_chains, n_cbs, n_segs, n_execs, n_accels, n_bins;
+  const uint32_t *set_chain_off, *set_exec_off, *set_accel_off; /* [n_sets+1] */
+  const uint64_t *chain_T, *chain_D;
+  const uint32_t *chain_prio;
+  const uint8_t *chain_class;
+  const uint32_t *chain_cb_off; /* [n_chains+1] */
+  const uint16_t *cb_exec;      /* set-local executor of each callback */
+  const uint32_t *cb_seg_off;   /* [n_cbs+1] */
+  const uint8_t *seg_kind;
+  const uint64_t *seg_wcet;
+  const uint8_t *seg_accel, *seg_unit;
+  const uint8_t *exec_core;
+  const uint32_t *exec_prio;
+  const uint8_t *exec_wait;
+  const uint8_t *accel_buckets, *accel_units, *accel_server_core;
+  const uint64_t *accel_eps, *accel_kappa;
+  const uint32_t *set_bin; /* utilisation bin of each set, < n_bins (may be NULL: no bin counts) */
+  uint64_t comm_cost;      /* eps' per executor crossing (A9), default 100 us */
+  uint32_t flags;          /* PAAM_FLAG_* */
+  uint32_t _pad;
+} paam_batch;
+
+/* Generator knobs; integer only, reproduced bit-for-bit on host and device. */
+typedef struct {
+  uint32_t m_lo, m_hi, cbs_per_chain, n_bins;
+  uint32_t u_lo_q20, u_step_q20;
+  uint32_t ratio_acc, ratio_cpu;
+  uint32_t period_min_us, period_span_q12;
+  uint32_t exec_mode, n_cores, n_exec;
+  uint32_t n_accel;
+  uint32_t buckets[4], units[4];
+  uint64_t eps[4], kappa[4];
+  uint32_t be_frac_q16, spin_frac_q16, cpu_only_frac_q16, xexec_frac_q16, rm_priorities;
+  uint32_t _pad;
+} paam_gen_params;
+
+/* Device-resident raw batch produced by paam_generate (owned by the library). */
+typedef struct paam_raw paam_raw;
+/* Device-resident packed records (owned by the library). */
+typedef struct paam_sets paam_sets;
+
+/* paam_generate -- §8(a) step 1.  Generates sets [first_index, first_index + n) of the stream
+ * `seed` into a device raw batch.  Returns PAAM_EINVAL if the parameters exceed the generator's
+ * caps.  *out receives a handle; paam_raw_batch() exposes its arrays as a paam_batch (mem = DEVICE). */
+int paam_generate(const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
+                  uint64_t comm_cost, uint32_t flags, paam_raw** out, paam_stream_t stream);
+int paam_raw_batch(const paam_raw* raw, paam_batch* out);
+void paam_raw_free(paam_raw* raw);
+
+/* paam_pack -- §8(a) step 2.  Validates every set and derives the per-set record the analysis and
+ * the simulator read: sub-chains (maximal runs of callbacks on one executor), E_c, delta_c,
+ * A* = A + 2 kappa_eff, the bucket map, LP blocking per segment,
+ * interference sets hps/hp/hpp and the per-core analysis order.
+ * out_status: NULL or an array of n_sets int32 in the same memory space as the batch.
+ * Host input is copied to the device on `stream` (the call then synchronises that stream). */
+int paam_pack(const paam_batch* batch, paam_sets** out, int32_t* out_status, paam_stream_t stream);
+/* Re-pack into an existing handle of sufficient capacity (no allocation; for timed loops). */
+int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* out_status, paam_stream_t stream);
+
+/* paam_analyze -- §8(a) steps 3-6.  For each of the first n sets of the handle:
+ *   out_wcrt  [n_chains total, global chain order of the batch] R*_Gamma in ns or PAAM_UNSCHED;
+ *             may be NULL (verdict-only sweeps).
+ *   out_sched [n] 1 iff every CRITICAL chain has R* <= D (invalid sets: 0); may be NULL.
+ *   out_bins  [n_bins*2] int64, ACCUMULATED (+=): bins[2b] += sets of bin b, bins[2b+1] += schedulable
+ *             sets of bin b; may be NULL.  Integer sums, so the result is order-independent.
+ * Device pointers only. */
+int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcrt, uint8_t* out_sched,
+                 int64_t* out_bins, paam_stream_t stream);
+
+/* paam_simulate -- §8(a) steps 7-8.  Discrete-event simulation of every set over [0, horizon):
+ * chain release phases are 0 when seed == 0, else uniform in [0, T) from (seed, set, chain).
+ *   out_resp   [n_chains total] maximum observed end-to-end response time per chain (0 if none).
+ *   out_digest [n] FNV-1a-64 over the canonical event stream (may be NULL).
+ *   bound      [n_chains total] WCRTs from paam_analyze, or NULL.  With a bound, for every CRITICAL
+ *              chain with a finite bound, out_resp > bound increments *out_violations (int64, +=).
+ * Device pointers only. */
+int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed,
+                  uint64_t* out_resp, uint64_t* out_digest, const uint64_t* bound,
+                  int64_t* out_violations, paam_stream_t stream);
+
+/* Handle queries (synchronous, small). */
+int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins);
+void paam_free(paam_sets* sets);
+
+const char* paam_strerror(int code);
+const char* paam_last_error(void); /* thread-local detail of the last failure */
+uint64_t paam_kernel_launches(void); /* kernels launched by this library since load (process-wide) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif
