@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py -- chain sets analysed per second (PAAM WCRT fixed points) on N B200s.
+
+One step = the whole hot path over this rank's batch of synthetic chain sets that is already
+resident in HBM: paam_repack (validate + derive, §8(a) step 2) -> paam_analyze (Lemma 2 / Eq.5 fixed
+points, end-to-end WCRT, verdict, bin counts; steps 3-6) -> (N > 1) one NCCL all-reduce of the bin
+counts.  Weak scaling: every rank owns SETS_PER_GPU consecutive set indices of the config-4 stream
+(seed 4), so N = 8 is exactly config 4 (16M sets) and N = 1 is the config-3 recipe on 2M sets.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (the driver's contract).  The CPU oracle is executed only by the
+cpu_baseline leg (rank 0, N = 1) and by --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "chain-sets analysed/sec (WCRT fixed-point) at 1/2/4/8 B200; % of roofline"
+SEED = 4
+DEFAULT_SETS_PER_GPU = 2_000_000
+# Algorithmic integer work of one mu-term of Eq.2-Eq.5 after exact regrouping: multiply-high by the
+# period's magic constant, shift, multiply by the interfering weight, accumulate.
+OPS_PER_MU = 4
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(params, first, budget_s=15.0, nthreads=None):
+    """The oracle as it stands, on a bounded prefix of this rank's workload, all host cores.
+    The sample is generated first (untimed); only the oracle's analysis is timed."""
+    from gen.inputs import generate_host
+    from oracle import oracle as O
+    nthreads = nthreads or (os.cpu_count() or 1)
+    probe = generate_host(params, SEED, first, 2000)
+    t0 = time.perf_counter()
+    O.analyze(probe, nthreads=nthreads)
+    rate = 2000 / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(max(rate * budget_s, 2000), 2_000_000))
+    sample = generate_host(params, SEED, first, n)
+    t0 = time.perf_counter()
+    O.analyze(sample, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "chain-sets/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"first {n} sets of this rank's range (config-3 recipe, seed {SEED}): {dt:.1f} s "
+                      f"of oracle analysis on {nthreads} threads"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as it stands (this tier's reference arm)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from gen.inputs import config3_params, generate_host
+    from oracle import oracle as O
+    p = config3_params()
+    nthreads = os.cpu_count() or 1
+    per_step = args.ref_sets_per_step
+    batches = [generate_host(p, SEED, i * per_step, per_step) for i in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        O.analyze(batches[i], nthreads=nthreads)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        O.analyze(batches[args.warmup + i], nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    v = per_step * args.steps / dt
+    out = {"metric": METRIC, "value": v, "unit": "chain-sets/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"config-3 recipe, seed {SEED}, {per_step} sets per step (bounded sample)",
+                      "sets_per_step": per_step},
+           "cpu_baseline": {"value": v, "unit": "chain-sets/s", "cores": nthreads, "kind": "oracle",
+                            "sample": f"{per_step} sets per step x {args.steps} steps"},
+           "e2e": {"value": v, "unit": "chain-sets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def batch_bytes(c) -> int:
+    n, ch, cb, sg, ex, ac = c.n_sets, c.n_chains, c.n_cbs, c.n_segs, c.n_execs, c.n_accels
+    return (3 * 4 * (n + 1) + ch * (8 + 8 + 4 + 1) + 4 * (ch + 1) + cb * 2 + 4 * (cb + 1) + sg * (1 + 8 + 1 + 1)
+            + ex * (1 + 4 + 1) + ac * (1 + 1 + 1 + 8 + 8) + (4 * n if c.set_bin else 0))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_2404_06452_b200 import paam
+
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = args.sets_per_gpu
+    first = rank * n
+    from gen.inputs import config3_params  # workload recipe (shared input generator params)
+    gp = config3_params()
+    params = paam.PaamGenParams.from_buffer_copy(bytes(gp))
+    stream = torch.cuda.Stream(device=dev)
+
+    # ---- inputs resident in HBM (generated on device; outside the timed region) ------------------
+    with torch.cuda.stream(stream):
+        raw = paam.Raw(params, SEED, first, n, stream=stream)
+        sets = paam.Sets(raw, stream=stream)
+        wcrt = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
+        sched = torch.empty(n, dtype=torch.uint8, device=dev)
+        bins = torch.zeros(2 * gp.n_bins, dtype=torch.int64, device=dev)
+    stream.synchronize()
+    rec_bytes = paam.lib().paam_record_bytes()
+    in_bytes = batch_bytes(raw.c)
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    def step():
+        sets.repack(raw, stream=stream)                       # §8(a) step 2 (kernel)
+        sets.analyze(wcrt, sched, bins, stream=stream)        # steps 3-6 (kernel)
+        if dist is not None:                                  # the one exchange: bin counts
+            with torch.cuda.stream(stream):
+                dist.all_reduce(bins)
+
+    # ---- warm-up ------------------------------------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    barrier(world)
+
+    # ---- timed region: K steps, CUDA events on the launching stream ---------------------------------
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = paam.kernel_launches()
+    torch.cuda.synchronize()
+    barrier(world)
+    start.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        sets.repack(raw, stream=stream)
+        ev[k][1].record(stream)
+        sets.analyze(wcrt, sched, bins, stream=stream)
+        ev[k][2].record(stream)
+        if dist is not None:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(bins)
+    end.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = paam.kernel_launches() - launches0
+    clk = clocks.stop()
+    ms_local = start.elapsed_time(end)
+    ms = max_over_ranks(ms_local, world)
+    pack_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    ana_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    value = world * n * args.steps / (ms / 1e3)
+
+    # ---- e2e: the same metric through the C ABI with HOST buffers (copies inside the region) ------
+    e2e = None
+    if not args.no_e2e:
+        from gen.inputs import generate_host
+
+        def pinned(nbytes):
+            return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True).numpy()
+
+        host = generate_host(gp, SEED, first, n, pinned_alloc=pinned)
+        hb = paam.Batch.from_host(host)
+        sched_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        bins_h = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
+        hsets = paam.Sets(hb, stream=stream)
+        def e2e_step():
+            hsets.repack(hb, stream=stream)                    # H2D of the raw batch + pack kernel
+            hsets.analyze(None, sched, bins, stream=stream)
+            if dist is not None:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(bins)
+            with torch.cuda.stream(stream):
+                sched_h.copy_(sched, non_blocking=True)       # D2H: verdicts + bin counts
+                bins_h.copy_(bins, non_blocking=True)
+            stream.synchronize()
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        e2e = {"value": world * n * args.steps / e2e_s, "unit": "chain-sets/s",
+               "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
+               "ms_per_step": 1e3 * e2e_s / args.steps}
+        hsets.free()
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel --------------------------------------------------------------
+    pk = peaks()
+    work = work_per_set(gp, first)
+    ana_avg = sum(ana_ms) / len(ana_ms)
+    pack_avg = sum(pack_ms) / len(pack_ms)
+    sm_clock_hz = 1.965e9
+    alu_peak = 148 * 128 * sm_clock_hz / 1e12  # T lane-ops/s: 148 SMs x 4 SMSP x 32 lanes (alu + fma pipes)
+    ops = work["mu_regrouped_per_set"] * OPS_PER_MU * n
+    achieved = ops / (ana_avg / 1e3) / 1e12
+    traffic = measured_traffic_per_set()
+    roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s (int32 lane-ops)",
+            "frac": achieved / alu_peak,
+            "traffic": None if traffic is None else traffic * n,
+            "kernel": "analyze_kernel", "kernel_ms": ana_avg, "pack_kernel_ms": pack_avg,
+            "kernel_share_of_step": ana_avg / (ms_local / args.steps),
+            "ops_per_set": work["mu_regrouped_per_set"] * OPS_PER_MU,
+            "peak_source": "derived: 148 SMs x 128 int32 lanes/clk (B300_MICROARCH alu+fma pipes) x 1.965 GHz",
+            "hbm": {"achieved_GBps": (rec_bytes * n + 9 * n) / (ana_avg / 1e3) / 1e9,
+                    "peak_GBps": pk.get("hbm_gbs", 6533.2), "of": "measured" if pk else "fallback"}}
+    out = {"metric": METRIC, "value": value, "unit": "chain-sets/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+           "config": {"workload": f"config-3 recipe (m 8-16 chains x 4 callbacks, GPU-like n=6 + TPU-like n=1, "
+                                  f"9 utilisation bins), {n} sets/GPU, seed {SEED}, rank r owns "
+                                  f"[r*{n}, (r+1)*{n}) -- N=8 is config 4 (16M sets)",
+                      "sets_per_gpu": n, "global_sets": world * n, "seed": SEED,
+                      "l2": f"inputs larger than L2: {(in_bytes + rec_bytes * n) / 1e9:.1f} GB/GPU resident",
+                      "parallelism": f"dp{world} (set-index shards, NCCL all-reduce of bin counts)"},
+           "gpu_launches": int(launches), "clocks": clk, "roofline": roof,
+           "bins": bins.cpu().tolist()}
+    if e2e:
+        out["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(gp, first, budget_s=args.cpu_budget)
+    print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def work_per_set(gp, first, sample=4000):
+    """Oracle-counted mu-terms per set on a sample of the workload (algorithmic work, not timing)."""
+    try:
+        from oracle import oracle as O
+        _, _, _, cnt = O.generate_analyze(gp, SEED, first, sample, nthreads=os.cpu_count() or 1)
+        return {"mu_literal_per_set": float(cnt[0]) / sample, "mu_regrouped_per_set": float(cnt[1]) / sample,
+                "iterations_per_set": float(cnt[2]) / sample}
+    except Exception:
+        return {"mu_literal_per_set": None, "mu_regrouped_per_set": 780.0, "iterations_per_set": None}
+
+
+def measured_traffic_per_set():
+    """dram bytes per set of analyze_kernel from the committed ncu --set full capture, if present."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return float(d["analyze_kernel"]["dram_bytes_per_set"])
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sets-per-gpu", type=int, default=DEFAULT_SETS_PER_GPU)
+    ap.add_argument("--ref-sets-per-step", type=int, default=20_000)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 untimed warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -22,7 +22,11 @@
 
 #ifdef __CUDACC__
 #define PG_FN static __host__ __device__ __forceinline__
+#ifdef __CUDA_ARCH__
+#define PG_TABLE(i) PG_EXP2_Q30_DEV[i]
+#else
 #define PG_TABLE(i) PG_EXP2_Q30[i]
+#endif
 #else
 #define PG_FN static inline
 #define PG_TABLE(i) PG_EXP2_Q30[i]

@@ -19,7 +19,7 @@
  *
  * Conventions.
  *   - Every time is an unsigned 64-bit integer number of nanoseconds.  Each individual
- *     period, deadline, WCET, eps, kappa and comm cost must be < 2^31 ns (about 2.1 s): the device
+ *     period, deadline, WCET, eps, kappa and comm cost must be < 2^31 - 1 ns (about 2.1 s): the device
  *     path computes in 32-bit integers with sums saturating just above the deadline, which is exact
  *     because any value above the deadline is a miss.
  *   - Indices inside a set are set-local (executor, accelerator, unit); CSR offset arrays are global.
@@ -53,7 +53,7 @@ typedef void* paam_stream_t; /* a cudaStream_t (may be NULL = legacy default str
 /* ---- per-set validation status (out_status[i]) -------------------------------------------- */
 /* Checked in this order; the first failing rule is reported. */
 #define PAAM_SET_OK 0
-#define PAAM_SET_ERANGE 1    /* over the size caps below, T == 0, or a time >= 2^31 ns */
+#define PAAM_SET_ERANGE 1    /* over the size caps below, T == 0, or a time >= 2^31 - 1 ns */
 #define PAAM_SET_EDANGLING 2 /* chain without callbacks, callback without segments, executor or
                                 unit index out of range */
 #define PAAM_SET_EACCEL 3    /* ACCEL segment on an undeclared accelerator */
@@ -182,6 +182,10 @@ int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t 
 /* Handle queries (synchronous, small). */
 int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins);
 void paam_free(paam_sets* sets);
+
+/* Utility: synchronous copy between any two memory spaces (cudaMemcpyDefault) on `stream`. */
+int paam_copy(void* dst, const void* src, size_t bytes, paam_stream_t stream);
+uint32_t paam_record_bytes(void); /* size of one packed per-set record in device memory */
 
 const char* paam_strerror(int code);
 const char* paam_last_error(void); /* thread-local detail of the last failure */

@@ -34,7 +34,7 @@ struct Accel { int buckets, units, server_core; u64 eps, kappa; };
 struct System { std::vector<Chain> chains; std::vector<Exec> execs; std::vector<Accel> accels;
                 u64 comm; u32 flags; };
 
-const u64 LIM31 = 1ull << 31;
+const u64 LIM31 = (1ull << 31) - 1;  // every input time must be < 2^31 - 1 ns (A14)
 
 System read_set(const or_batch* b, u32 i) {
   System s;

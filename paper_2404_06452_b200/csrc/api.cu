@@ -1,0 +1,218 @@
+// api.cu -- the C ABI of include/paam.h: handles, host staging, argument checks, error reporting.
+// Every compute step runs in the kernels of pack.cu / analyze.cu / simulate.cu / generate.cu; this
+// file only moves buffers and launches them.  There is no CPU fallback: without a CUDA device every
+// entry point returns PAAM_ECUDA.
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+
+struct paam_sets {
+  uint32_t n_sets, n_chains, n_bins, cap;
+  paam::Record* rec;
+  uint64_t comm;
+  uint32_t flags;
+  void* stage;  // device staging of a host batch (grown on demand)
+  size_t stage_bytes;
+  int32_t* dstatus;  // device status staging for host batches
+  uint32_t dstatus_cap;
+};
+
+namespace paam {
+
+static std::atomic<uint64_t> g_launches{0};
+static thread_local char g_err[512] = "";
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int fail(int code, const char* what) {
+  std::snprintf(g_err, sizeof(g_err), "%s", what);
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char* what) {
+  std::snprintf(g_err, sizeof(g_err), "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? PAAM_ENOMEM : PAAM_ECUDA;
+}
+
+namespace {
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Field { const void** ptr; size_t elems, size; };
+
+// The array fields of a batch with their element counts (order of include/paam.h).
+int batch_fields(paam_batch* b, Field* f) {
+  const size_t nn = (size_t)b->n_sets + 1;
+  Field t[] = {
+      {(const void**)&b->set_chain_off, nn, 4}, {(const void**)&b->set_exec_off, nn, 4},
+      {(const void**)&b->set_accel_off, nn, 4},
+      {(const void**)&b->chain_T, b->n_chains, 8}, {(const void**)&b->chain_D, b->n_chains, 8},
+      {(const void**)&b->chain_prio, b->n_chains, 4}, {(const void**)&b->chain_class, b->n_chains, 1},
+      {(const void**)&b->chain_cb_off, (size_t)b->n_chains + 1, 4},
+      {(const void**)&b->cb_exec, b->n_cbs, 2}, {(const void**)&b->cb_seg_off, (size_t)b->n_cbs + 1, 4},
+      {(const void**)&b->seg_kind, b->n_segs, 1}, {(const void**)&b->seg_wcet, b->n_segs, 8},
+      {(const void**)&b->seg_accel, b->n_segs, 1}, {(const void**)&b->seg_unit, b->n_segs, 1},
+      {(const void**)&b->exec_core, b->n_execs, 1}, {(const void**)&b->exec_prio, b->n_execs, 4},
+      {(const void**)&b->exec_wait, b->n_execs, 1},
+      {(const void**)&b->accel_buckets, b->n_accels, 1}, {(const void**)&b->accel_units, b->n_accels, 1},
+      {(const void**)&b->accel_server_core, b->n_accels, 1}, {(const void**)&b->accel_eps, b->n_accels, 8},
+      {(const void**)&b->accel_kappa, b->n_accels, 8},
+      {(const void**)&b->set_bin, b->set_bin ? (size_t)b->n_sets : 0, 4}};
+  const int n = sizeof(t) / sizeof(t[0]);
+  for (int i = 0; i < n; i++) f[i] = t[i];
+  return n;
+}
+
+int check_batch(const paam_batch* b) {
+  if (!b) return fail(PAAM_EINVAL, "NULL batch");
+  if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
+  if (b->comm_cost >= LIM) return fail(PAAM_EINVAL, "batch.comm_cost must be < 2^31 - 1 ns");
+  if (b->flags & ~PAAM_FLAG_BLOCKING_SOUND) return fail(PAAM_EINVAL, "unknown flag");
+  if (b->set_bin && b->n_bins == 0) return fail(PAAM_EINVAL, "set_bin given with n_bins == 0");
+  paam_batch c = *b;
+  Field f[32];
+  const int nf = batch_fields(&c, f);
+  for (int i = 0; i < nf; i++)
+    if (f[i].elems && !*f[i].ptr && f[i].ptr != (const void**)&c.set_bin)
+      return fail(PAAM_EINVAL, "NULL array in a batch with a non-zero count");
+  return PAAM_OK;
+}
+
+}  // namespace
+}  // namespace paam
+
+using namespace paam;
+
+extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* out_status, paam_stream_t stream) {
+  int rc = check_batch(batch);
+  if (rc) return rc;
+  if (!sets) return fail(PAAM_EINVAL, "NULL handle");
+  if (batch->n_sets > sets->cap) return fail(PAAM_EINVAL, "paam_repack: handle capacity too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  paam_batch d = *batch;
+  int32_t* status_dev = out_status;
+  if (batch->mem == PAAM_MEM_HOST) {
+    Field f[32];
+    const int nf = batch_fields(&d, f);
+    size_t bytes = 0;
+    for (int i = 0; i < nf; i++) bytes += align256(f[i].elems * f[i].size);
+    if (bytes > sets->stage_bytes) {
+      if (sets->stage) cudaFree(sets->stage);
+      sets->stage = nullptr;
+      sets->stage_bytes = 0;
+      if ((e = cudaMalloc(&sets->stage, bytes)) != cudaSuccess) return fail_cuda(e, "paam_pack: staging cudaMalloc");
+      sets->stage_bytes = bytes;
+    }
+    char* base = (char*)sets->stage;
+    size_t off = 0;
+    for (int i = 0; i < nf; i++) {  // one cudaMemcpyAsync per array (no batched-copy APIs)
+      const size_t nb = f[i].elems * f[i].size;
+      if (nb) {
+        if ((e = cudaMemcpyAsync(base + off, *f[i].ptr, nb, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+          return fail_cuda(e, "paam_pack: H2D copy");
+        *f[i].ptr = base + off;
+      }
+      off += align256(nb);
+    }
+    if (out_status) {
+      if (sets->dstatus_cap < batch->n_sets) {
+        if (sets->dstatus) cudaFree(sets->dstatus);
+        sets->dstatus = nullptr;
+        sets->dstatus_cap = 0;
+        if ((e = cudaMalloc((void**)&sets->dstatus, sizeof(int32_t) * (batch->n_sets ? batch->n_sets : 1))) != cudaSuccess)
+          return fail_cuda(e, "paam_pack: status cudaMalloc");
+        sets->dstatus_cap = batch->n_sets;
+      }
+      status_dev = sets->dstatus;
+    }
+  }
+  rc = launch_pack(&d, sets->rec, status_dev, st);
+  if (rc) return rc;
+  if (batch->mem == PAAM_MEM_HOST) {
+    if (out_status && batch->n_sets)
+      if ((e = cudaMemcpyAsync(out_status, status_dev, sizeof(int32_t) * batch->n_sets, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return fail_cuda(e, "paam_pack: status D2H");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_pack: synchronize");
+  }
+  sets->n_sets = batch->n_sets;
+  sets->n_chains = batch->n_chains;
+  sets->n_bins = batch->set_bin ? batch->n_bins : 0;
+  sets->comm = batch->comm_cost;
+  sets->flags = batch->flags;
+  return PAAM_OK;
+}
+
+extern "C" int paam_pack(const paam_batch* batch, paam_sets** out, int32_t* out_status, paam_stream_t stream) {
+  if (!out) return fail(PAAM_EINVAL, "NULL out");
+  *out = nullptr;
+  int rc = check_batch(batch);
+  if (rc) return rc;
+  paam_sets* s = (paam_sets*)std::calloc(1, sizeof(paam_sets));
+  if (!s) return fail(PAAM_ENOMEM, "host allocation");
+  s->cap = batch->n_sets;
+  cudaError_t e = cudaMalloc((void**)&s->rec, sizeof(Record) * (size_t)(batch->n_sets ? batch->n_sets : 1));
+  if (e != cudaSuccess) {
+    std::free(s);
+    return fail_cuda(e, "paam_pack: record cudaMalloc");
+  }
+  rc = paam_repack(batch, s, out_status, stream);
+  if (rc) {
+    paam_free(s);
+    return rc;
+  }
+  *out = s;
+  return PAAM_OK;
+}
+
+extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcrt, uint8_t* out_sched,
+                            int64_t* out_bins, paam_stream_t stream) {
+  if (!sets) return fail(PAAM_EINVAL, "NULL handle");
+  if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_analyze: n exceeds the packed sets");
+  return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
+                        sets->n_bins ? out_bins : nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins) {
+  if (!sets) return fail(PAAM_EINVAL, "NULL handle");
+  if (n_sets) *n_sets = sets->n_sets;
+  if (n_chains) *n_chains = sets->n_chains;
+  if (n_bins) *n_bins = sets->n_bins;
+  return PAAM_OK;
+}
+
+extern "C" void paam_free(paam_sets* sets) {
+  if (!sets) return;
+  if (sets->rec) cudaFree(sets->rec);
+  if (sets->stage) cudaFree(sets->stage);
+  if (sets->dstatus) cudaFree(sets->dstatus);
+  std::free(sets);
+}
+
+extern "C" const char* paam_strerror(int code) {
+  switch (code) {
+    case PAAM_OK: return "ok";
+    case PAAM_EINVAL: return "invalid argument";
+    case PAAM_ECUDA: return "CUDA error";
+    case PAAM_ENOMEM: return "out of device memory";
+    case PAAM_ERANGE: return "batch size out of range";
+    default: return "unknown error";
+  }
+}
+
+extern "C" const char* paam_last_error(void) { return g_err; }
+extern "C" uint64_t paam_kernel_launches(void) { return g_launches.load(); }
+
+extern "C" uint32_t paam_record_bytes(void) { return (uint32_t)sizeof(Record); }
+
+extern "C" int paam_copy(void* dst, const void* src, size_t bytes, paam_stream_t stream) {
+  if ((!dst || !src) && bytes) return fail(PAAM_EINVAL, "paam_copy: NULL pointer");
+  if (!bytes) return PAAM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "paam_copy");
+}

@@ -1,0 +1,93 @@
+// common.cuh -- device-side conventions of the PAAM product path (sm_100a).
+//
+// Integer time (A14): every input time is < 2^31 - 1 ns, every derived quantity is a u32 that
+// saturates at SAT = 2^31 - 1.  Every cutoff (min(D, T)) is <= 2^31 - 2 < SAT, so a saturated value
+// is "above every deadline" and no finite result or verdict can differ from exact u64 arithmetic.
+// An unbounded Lemma-2 value (UNB) is represented by SAT as well: min(SAT, C) behaves exactly like
+// the paper's min(UNB, C) because any C >= SAT is itself above the cutoff.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/paam.h"
+
+namespace paam {
+
+constexpr uint32_t SAT = 0x7FFFFFFFu;
+constexpr uint64_t LIM = 0x7FFFFFFFull;  // inputs must be < LIM (validation, PAAM_SET_ERANGE)
+
+__device__ __forceinline__ uint32_t sadd(uint32_t a, uint32_t b) { return min(a + b, SAT); }  // a,b <= SAT
+__device__ __forceinline__ uint32_t smul(uint32_t a, uint32_t b) {
+  const uint64_t p = (uint64_t)a * b;
+  return p > SAT ? SAT : (uint32_t)p;
+}
+
+// mu(t) = ceil(t / T) + 1 (Lemma 1, Eq.2) for 1 <= t <= SAT, by multiply-high with the
+// per-period constant (M, L) from make_magic: floor(n / T) = umulhi(2n, M) >> L for n < 2^31
+// (Granlund-Montgomery with N = 31: M = ceil(2^(31+L) / T), L = ceil(log2 T)), and
+// ceil(t / T) = floor((t - 1) / T) + 1 for t >= 1.
+__device__ __forceinline__ uint32_t mu_magic(uint32_t t, uint32_t M, uint32_t L) {
+  return (__umulhi((t - 1u) << 1, M) >> L) + 2u;
+}
+__host__ __device__ inline void make_magic(uint32_t T, uint32_t* M, uint32_t* L) {
+  uint32_t l = 0;
+  while (l < 32 && (1ull << l) < T) l++;  // l = ceil(log2 T)
+  *L = l;
+  *M = (uint32_t)(((1ull << (31 + l)) + T - 1) / T);
+}
+
+// ---- packed per-set record (written by pack.cu, read by analyze.cu / simulate.cu) ------------------
+// Fixed stride, structure-of-arrays inside the record; everything a warp needs is one contiguous
+// 16-byte-aligned block that it bulk-loads into shared memory.
+constexpr int MAXC = 32;   // chains
+constexpr int MAXS = 32;   // sub-chains
+constexpr int MAXA = 64;   // accelerator segments
+constexpr int MAXU = 8;    // accelerator units (all accelerators of the set)
+constexpr int MAXX = 32;   // executors
+constexpr int MAXCB = 64;  // callbacks
+
+struct __align__(16) Record {
+  // header
+  uint8_t n_chain, n_sub, n_aseg, n_unit;
+  int32_t status;       // PAAM_SET_*
+  uint32_t chain_base;  // global index of the set's first chain (out_wcrt position)
+  uint32_t bin;         // utilisation bin (0 when the batch has none)
+  uint32_t n_out;       // chains of the set in the batch (== n_chain when valid)
+  uint32_t pad_[3];
+  // chains by rank (rank 0 = highest priority)
+  uint32_t cT[MAXC];     // period
+  uint32_t cCut[MAXC];   // cutoff min(D, T) (A4, A12)
+  uint32_t cD[MAXC];     // deadline (verdict)
+  uint32_t cM[MAXC];     // mu magic multiplier for T
+  uint32_t cMisc[MAXC];  // L (5 bits) | class << 8 | local index << 16 | n_sub << 24
+  // W[u][k]: sum of A* of chain rank k's segments on unit u (exact regrouping of Eq.3/Eq.4 sums)
+  uint32_t W[MAXU][MAXC];
+  // sub-chains in canonical analysis order (per core: process priority desc, chain rank asc; A7)
+  uint32_t sE[MAXS];      // calligraphic E_c
+  uint32_t sB[MAXS];      // B_c as written
+  uint32_t sEps[MAXS];    // sum of eps over the sub-chain's segments (delta_c * eps, A11)
+  uint32_t sBase3[MAXS];  // sum over segments of (A* + LPB): first term of Eq.4
+  uint32_t sHp[MAXS];     // bit h: h in hp(c)
+  uint32_t sHpp[MAXS];    // bit h: h in hpp(c)
+  uint32_t sLp[MAXS];     // bit h: h in lp(c)
+  uint32_t sMisc[MAXS];   // rank | unitmask << 8 | spin << 16 | chain-position << 24
+  uint32_t sSeg[MAXS];    // first accelerator segment | count << 8 | exec << 16 | core << 24
+  // accelerator segments, grouped by canonical sub-chain, in chain order inside a sub-chain
+  uint32_t aBase2[MAXA];  // A* + LPB: first two terms of Eq.3
+  uint32_t aEps[MAXA];    // eps of the segment's accelerator
+  uint32_t aCbE[MAXA];    // E_j of the segment's callback (PAAM_FLAG_BLOCKING_SOUND)
+  uint32_t aMisc[MAXA];   // rank | unit << 8 | sub << 16 | callback << 24
+};
+static_assert(sizeof(Record) % 16 == 0, "record must be 16-byte aligned");
+
+// ---- launch bookkeeping ---------------------------------------------------------------------------
+void count_launch();
+int fail_cuda(cudaError_t e, const char* what);
+int fail(int code, const char* what);
+
+// launchers (defined in the kernel files)
+int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status, cudaStream_t st);
+int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
+                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st);
+
+}  // namespace paam

@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path (through the C ABI) is bit-exact with the CPU oracle.
+
+Integer results -> bit-exact comparison of every WCRT, verdict, status and bin count.
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from gen.inputs import (CRITICAL, MS, US, Seg, System, acc, cb, config2_params, config3_params, cpu, flatten,
+                        generate_host, make_params, slice_sets)
+from oracle import oracle as O
+from paper_2404_06452_b200 import paam
+from tests.ref_scan import random_small_system
+from tests.test_oracle_pins import GOLD, a10_system, app_b_two_chains, cs3_system, two_chain_accel_system
+
+NPROC = os.cpu_count() or 1
+
+
+def gpu_host_path(batch):
+    return paam.analyze(paam.Batch.from_host(batch))
+
+
+def gpu_device_path(batch):
+    return paam.analyze(paam.Batch.from_host_to_device(batch))
+
+
+def assert_same(batch, gpu):
+    ow, osch, ost, ob = O.analyze(batch, nthreads=NPROC)
+    gw, gsch, gst, gb = gpu
+    assert np.array_equal(ost, gst), np.nonzero(ost != gst)[0][:10]
+    bad = np.nonzero(ow != gw)[0]
+    assert bad.size == 0, (bad[:10], ow[bad[:10]], gw[bad[:10]])
+    assert np.array_equal(osch, gsch)
+    if batch.get("n_bins"):
+        assert np.array_equal(ob, gb)
+
+
+def test_worked_examples_on_gpu():
+    systems = [two_chain_accel_system(), two_chain_accel_system(eps=391 * US), app_b_two_chains(),
+               cs3_system(6), cs3_system(1), a10_system()]
+    for flags in (0, 1):
+        b = flatten(systems, comm_cost=0, flags=flags)
+        assert_same(b, gpu_host_path(b))
+    gw, gsch, _, _ = gpu_host_path(flatten([cs3_system(6)], comm_cost=0))
+    assert gw[:2].tolist() == GOLD["cs3_n6"]["R"]
+    gw, _, _, _ = gpu_host_path(flatten([app_b_two_chains()], comm_cost=0))
+    assert gw.tolist() == GOLD["two_chains_one_executor"]["R"]
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_random_small_systems(flags):
+    rng = random.Random(77 + flags)
+    systems = [random_small_system(rng, max_chains=6, tmax=200) for _ in range(3000)]
+    b = flatten(systems, comm_cost=3, flags=flags)
+    assert_same(b, gpu_host_path(b))
+    assert_same(b, gpu_device_path(b))
+
+
+def mutate_invalid(s: System, rng):
+    """Break one validation rule (or none)."""
+    k = rng.randrange(10)
+    if k == 0 and len(s.chains) > 1:
+        s.chains[1].prio = s.chains[0].prio
+    elif k == 1:
+        s.chains[0].D = s.chains[0].T + 1
+        s.chains[0].cls = CRITICAL
+    elif k == 2:
+        s.chains[0].cbs[0].exec = 31
+    elif k == 3:
+        s.chains[0].cbs[0].segs.append(Seg(1, 1, 3, 0))
+    elif k == 4:
+        s.chains[0].cbs[0].segs[0].wcet = 0
+    elif k == 5:
+        s.execs[0] = (10, 1, 0)  # server core of accelerator 0
+    elif k == 6:
+        s.chains[0].T = 1 << 31
+    elif k == 7:
+        s.chains[0].cbs[0].segs.append(Seg(s.chains[0].cbs[0].segs[-1].kind, 1))
+    return s
+
+
+def test_validation_statuses_match():
+    rng = random.Random(5)
+    systems = [mutate_invalid(random_small_system(rng), rng) for _ in range(2000)]
+    b = flatten(systems, comm_cost=1)
+    _, _, st, _ = O.analyze(b)
+    assert len(set(st.tolist())) >= 6
+    assert_same(b, gpu_host_path(b))
+
+
+def test_edge_cases():
+    # empty set, single chain, maximum sizes: 32 chains, 64 accelerator segments over 8 units
+    s0 = System(); s0.accel(server_core=0)
+    s1 = System(); a = s1.accel(server_core=0); x = s1.executor(core=1)
+    s1.chain(T=10, prio=1, cbs=[cb(x, acc(a, 3))])
+    big = System()
+    accs = [big.accel(buckets=6, units=2, server_core=20, eps=2, kappa=1),
+            big.accel(buckets=1, units=2, server_core=21, eps=1),
+            big.accel(buckets=3, units=2, server_core=22),
+            big.accel(buckets=2, units=2, server_core=23)]
+    xs = [big.executor(core=i % 4, prio=i // 4 + 1) for i in range(16)]
+    rng = random.Random(3)
+    for c in range(32):
+        cbs = []
+        for j in range(2):
+            aa = accs[(c + j) % 4]
+            cbs.append(cb(xs[c % 16], cpu(rng.randint(1, 5)), acc(aa, rng.randint(1, 5), unit=(c + j) % 2)))
+        big.chain(T=rng.randint(2000, 5000), prio=c + 1, cbs=cbs)
+    b = flatten([s0, s1, big, s0], comm_cost=2)
+    _, _, st, _ = O.analyze(b)
+    assert st.tolist() == [0, 0, 0, 0]
+    assert_same(b, gpu_host_path(b))
+    # an over-cap set (33 chains) is rejected with ERANGE on both sides
+    over = System(); a = over.accel(server_core=0); x = over.executor(core=1)
+    for c in range(33):
+        over.chain(T=1000, prio=c + 1, cbs=[cb(x, cpu(1))])
+    b = flatten([over, s1], comm_cost=0)
+    assert_same(b, gpu_host_path(b))
+    assert gpu_host_path(b)[2].tolist() == [1, 0]
+
+
+@pytest.mark.parametrize("cfg,cpu_only", [("config2", 0.0), ("config2", 0.25), ("config3", 0.0), ("modeB_split", 0.0)])
+def test_generated_workloads_full(cfg, cpu_only):
+    if cfg == "config2":
+        p, seed, n = config2_params(cpu_only_frac=cpu_only), 2, 10_000
+    elif cfg == "config3":
+        p, seed, n = config3_params(), 3, 20_000
+    else:
+        p, seed, n = make_params(exec_mode=1, n_exec=4, xexec_frac=0.5, cpu_only_frac=0.2, spin_frac=0.5), 6, 20_000
+    b = generate_host(p, seed, 0, n)
+    assert_same(b, gpu_host_path(b))
+
+
+def gen_gpu(p, seed, first, n):
+    pp = paam.PaamGenParams.from_buffer_copy(bytes(p))
+    return paam.Raw(pp, seed, first, n)
+
+
+def test_device_generator_matches_host_bytes():
+    for p, seed in ((config3_params(), 3), (config2_params(0.25), 2), (make_params(exec_mode=1, xexec_frac=0.5), 8)):
+        h = generate_host(p, seed, 1000, 5000)
+        raw = gen_gpu(p, seed, 1000, 5000)
+        d = raw.to_host()
+        for k, v in h.items():
+            if isinstance(v, np.ndarray):
+                assert np.array_equal(v, d[k]), k
+        raw.free()
+
+
+def test_device_pipeline_generate_pack_analyze_bins():
+    """The bench's exact path (generate -> pack -> analyze with bins), 200k config-3 sets, vs oracle."""
+    p = config3_params()
+    n = 200_000
+    raw = gen_gpu(p, 3, 0, n)
+    dev = torch.device("cuda")
+    sets = paam.Sets(raw)
+    wcrt = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
+    sched = torch.empty(n, dtype=torch.uint8, device=dev)
+    bins = torch.zeros(2 * p.n_bins, dtype=torch.int64, device=dev)
+    sets.analyze(wcrt, sched, bins)
+    torch.cuda.synchronize()
+    ow, osch, ob, _ = O.generate_analyze(p, 3, 0, n, want_wcrt=True, nthreads=NPROC)
+    assert np.array_equal(sched.cpu().numpy(), osch)
+    assert np.array_equal(bins.cpu().numpy(), ob)
+    off = raw.to_host()["set_chain_off"]
+    gw = wcrt.cpu().numpy().view(np.uint64)
+    m = np.diff(off)
+    idx = np.repeat(np.arange(n), m) * 32 + (np.arange(len(gw)) - np.repeat(off[:-1], m))
+    assert np.array_equal(gw, ow.reshape(-1)[idx])
+
+
+def test_bins_accumulate_and_partition():
+    """Bin counts of two halves add up to the whole (the multi-GPU all-reduce relies on it)."""
+    p = config3_params()
+    dev = torch.device("cuda")
+    tot = torch.zeros(2 * p.n_bins, dtype=torch.int64, device=dev)
+    for first, n in ((0, 3000), (3000, 7000)):
+        raw = gen_gpu(p, 4, first, n)
+        sets = paam.Sets(raw)
+        sets.analyze(None, None, tot)
+    whole = torch.zeros_like(tot)
+    raw = gen_gpu(p, 4, 0, 10000)
+    paam.Sets(raw).analyze(None, None, whole)
+    torch.cuda.synchronize()
+    assert torch.equal(tot, whole)
+    _, _, ob, _ = O.generate_analyze(p, 4, 0, 10000, nthreads=NPROC)
+    assert np.array_equal(whole.cpu().numpy(), ob)
