@@ -83,17 +83,29 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
       const uint32_t nch = r.n_chain, nsub = r.n_sub, nas = r.n_aseg;
 
       // ---- step 3: Lemma 2, one lane per accelerator segment ----------------------------------------
+      // aBase2 already holds A* + LPB + 2 sum_{k<r} W[k][u] (the "+2" of every mu), so
+      // G(h) = aBase2 + sum_{k<r} floor((h-1)/T_k) * W[k][u]; starting at G's value for
+      // floor(.) = 0 is <= the least fixed point, so the lfp is unchanged (A3).  Products are
+      // 64-bit; a product >= 2^32 (high word != 0) is far above every cutoff, and without one the
+      // 64-bit sum of <= 31 products cannot overflow.
       for (uint32_t i = lane; i < nas; i += 32) {
         const uint32_t misc = r.aMisc[i];
         const uint32_t rk = misc & 0xffu, u = (misc >> 8) & 0xffu;
         const uint32_t base = r.aBase2[i], cut = r.cCut[rk];
         uint32_t h = base, H = SAT;
         while (h <= cut) {
-          uint32_t g = base;
+          const uint32_t h2 = (h - 1u) << 1;
+          uint64_t acc = base;
+          uint32_t hi = 0;
+#pragma unroll 2
           for (uint32_t k = 0; k < rk; k++) {
-            const uint32_t wk = r.W[u][k];
-            if (wk) g = sadd(g, smul(mu_magic(h, r.cM[k], r.cMisc[k] & 31u), wk));
+            const uint32_t q = __umulhi(h2, r.cM[k]) >> (r.cMisc[k] & 31u);
+            const uint64_t p = (uint64_t)q * r.W[k][u];
+            acc += p;
+            hi |= (uint32_t)(p >> 32);
           }
+          if (hi || acc > cut) break;
+          const uint32_t g = (uint32_t)acc;
           if (g == h) { H = h; break; }
           h = g;
         }
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
           while (um) {
             const uint32_t u = __ffs(um) - 1;
             um &= um - 1;
-            WU = sadd(WU, r.W[u][lane]);
+            WU = sadd(WU, r.W[lane][u]);
           }
         }
         uint32_t Rc = SAT, Hsc = SAT;

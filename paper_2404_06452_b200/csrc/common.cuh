@@ -60,8 +60,9 @@ struct __align__(16) Record {
   uint32_t cD[MAXC];     // deadline (verdict)
   uint32_t cM[MAXC];     // mu magic multiplier for T
   uint32_t cMisc[MAXC];  // L (5 bits) | class << 8 | local index << 16 | n_sub << 24
-  // W[u][k]: sum of A* of chain rank k's segments on unit u (exact regrouping of Eq.3/Eq.4 sums)
-  uint32_t W[MAXU][MAXC];
+  // W[k][u]: sum of A* of chain rank k's segments on unit u (exact regrouping of Eq.3/Eq.4 sums);
+  // rank-major so that lanes reading different units of one chain hit different banks
+  uint32_t W[MAXC][MAXU];
   // sub-chains in canonical analysis order (per core: process priority desc, chain rank asc; A7)
   uint32_t sE[MAXS];      // calligraphic E_c
   uint32_t sB[MAXS];      // B_c as written
@@ -72,8 +73,8 @@ struct __align__(16) Record {
   uint32_t sLp[MAXS];     // bit h: h in lp(c)
   uint32_t sMisc[MAXS];   // rank | unitmask << 8 | spin << 16 | chain-position << 24
   uint32_t sSeg[MAXS];    // first accelerator segment | count << 8 | exec << 16 | core << 24
-  // accelerator segments, grouped by canonical sub-chain, in chain order inside a sub-chain
-  uint32_t aBase2[MAXA];  // A* + LPB: first two terms of Eq.3
+  // accelerator segments in chain-rank order (a sub-chain's segments are contiguous)
+  uint32_t aBase2[MAXA];  // A* + LPB + 2 sum_{k<r} W[k][u]: Eq.3 with mu = floor((h-1)/T) + 2 split off
   uint32_t aEps[MAXA];    // eps of the segment's accelerator
   uint32_t aCbE[MAXA];    // E_j of the segment's callback (PAAM_FLAG_BLOCKING_SOUND)
   uint32_t aMisc[MAXA];   // rank | unit << 8 | sub << 16 | callback << 24

@@ -9,10 +9,12 @@
 //   * A* = A + 2 kappa_eff with kappa_eff = 0 on a one-bucket accelerator (A6);
 //   * the bucket of every (chain, accelerator): rank-based groups of ceil(m_a / n) (A5);
 //   * LP blocking per segment: max A* of lower-priority segments in the same bucket and unit;
-//   * W[u][k] = sum of A* of chain k on unit u (exact regrouping of the hps sums of Eq.3 / Eq.4);
+//   * W[k][u] = sum of A* of chain k on unit u (exact regrouping of the hps sums of Eq.3 / Eq.4);
 //   * B_c as written, hp / hpp / lp sets as bit masks;
 //   * the canonical analysis order: per core, process priority desc, then chain priority desc (A7).
-// Lanes run over chains / callbacks / segments / sub-chains; all staging is in shared memory.
+// Mapping: lane = chain (ranked), lane = callback (two passes of 32), lane = sub-chain; relations are
+// 32/64-bit masks built with ballot / match / warp reductions; the bucket LP-blocking maximum is a
+// segmented suffix-max scan over the users of each unit (buckets are aligned blocks in rank order).
 #include "common.cuh"
 
 namespace paam {
@@ -20,32 +22,68 @@ namespace paam {
 namespace {
 
 constexpr int WARPS = 4;
-constexpr int MAXG = 192;  // segments per set
+constexpr uint32_t FULL = 0xffffffffu;
 
 struct Scratch {
-  uint32_t cT[MAXC], cD[MAXC], cPrio[MAXC], cCb0[MAXC];
-  uint8_t cNcb[MAXC], cCls[MAXC], cRank[MAXC], cNsub[MAXC];
-  uint32_t cUse[MAXC];  // bit a: chain uses accelerator a
-  uint8_t cBucket[MAXC][4];
-  uint32_t bSeg0[MAXCB], bE[MAXCB];
-  uint8_t bNseg[MAXCB], bExec[MAXCB], bChain[MAXCB], bSub[MAXCB];
-  uint32_t gW[MAXG];
-  uint8_t gKind[MAXG], gAcc[MAXG], gUnit[MAXG], gCb[MAXG];
+  // chains by rank
+  uint32_t rT[MAXC], rD[MAXC], rCbo[MAXC], rA0[MAXC];  // rA0: first accelerator segment (rank order)
+  uint8_t rCls[MAXC], rIdx[MAXC], rNcb[MAXC], rNa[MAXC];
+  uint8_t rank_of[MAXC];  // chain index -> rank
+  uint32_t cA0[MAXC];     // chain index -> first accelerator segment in callback order
+  uint8_t bucket[MAXC][4];
+  // callbacks (set-local order)
+  uint32_t bE[MAXCB];
+  uint8_t bExec[MAXCB], bNa[MAXCB], bA0[MAXCB + 1], bSub[MAXCB];
+  // accelerator segments (callback order)
+  uint32_t qAstar[MAXA];
+  uint8_t qUnit[MAXA], qAcc[MAXA], qCb[MAXA], qRank[MAXA];
+  // executors
   uint32_t xPrio[MAXX];
-  uint8_t xCore[MAXX], xWait[MAXX];
+  uint8_t xCore[MAXX], xWait[MAXX], xPPrank[MAXX];
+  // accelerators
   uint32_t aN[4], aUnits[4], aUbase[4], aEps[4], aKeff[4], aServer[4];
-  uint32_t qAstar[MAXA], qLPB[MAXA];
-  uint8_t qChain[MAXA], qCb[MAXA], qSub[MAXA], qUnit[MAXA], qAcc[MAXA], qPos[MAXA];
-  uint8_t uChain[MAXS], uExec[MAXS], uCb0[MAXS], uNcb[MAXS], uCanon[MAXS], uNa[MAXS], uA0[MAXS];
-  unsigned long long W64[MAXU][MAXC];
+  uint8_t unitAcc[MAXU];
+  // per (rank, unit) / (unit, rank)
+  uint32_t W[MAXC][MAXU];
+  uint32_t maxA[MAXU][MAXC];
+  uint32_t lpb[MAXU][MAXC];
+  uint32_t pre2[MAXU][MAXC];
+  uint32_t cmp[MAXC];
+  // sub-chains (callback order of their first callback)
+  uint8_t sRank[MAXS], sCanon[MAXS], sExec[MAXS];
+  uint32_t sMaxE[MAXS];
 };
 
-__device__ __forceinline__ bool warp_any(bool p) { return __any_sync(0xffffffffu, p); }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// saturating inclusive prefix sum over lanes (Hillis-Steele; min(a+b, SAT) is associative on [0, SAT])
+__device__ __forceinline__ uint32_t scan_sat_incl(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v = sadd(v, y);
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t scan_excl(uint32_t v, int lane) {  // plain exclusive prefix sum
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x - v;
+}
 
 __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* __restrict__ recs,
                                                           int32_t* __restrict__ status_out) {
   __shared__ Scratch smem[WARPS];
   const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
   Scratch& s = smem[threadIdx.x >> 5];
   const uint32_t nwarps = gridDim.x * WARPS;
   for (uint32_t set = blockIdx.x * WARPS + (threadIdx.x >> 5); set < b.n_sets; set += nwarps) {
@@ -59,136 +97,145 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
     const uint32_t sg0 = b.cb_seg_off[cb0], sg1 = b.cb_seg_off[cb1];
     const uint32_t nseg = sg1 - sg0;
     int st = PAAM_SET_OK;
-    uint32_t n_aseg = 0, n_sub = 0, n_unit = 0;
 
-    // ---- 1. ERANGE: size caps, accelerator parameters, 31-bit times ------------------------------
-    if (nch > MAXC || ncb > MAXCB || nseg > MAXG || nex > MAXX || nac > 4) st = PAAM_SET_ERANGE;
+    if (nch > MAXC || ncb > MAXCB || nseg > 192 || nex > MAXX || nac > 4) st = PAAM_SET_ERANGE;
+    uint32_t n_aseg = 0, n_sub = 0, n_unit = 0;
+    uint64_t runstart = 0;  // bit j: callback j starts a sub-chain
+    uint64_t cstart = 0;    // bit j: callback j is the first of its chain
+    // per-lane chain data (lane = chain index)
+    uint32_t T = 0, D = 0, prio = 0, cls = 0, cbo = 0, cbn = 0, rank = 0;
     if (st == PAAM_SET_OK) {
-      bool bad = false;
-      for (uint32_t base = 0; base < nseg; base += 32) {  // warp-uniform trip count (ballot)
-        const uint32_t k = base + lane;
-        uint8_t kind = 0;
-        if (k < nseg) {
-          kind = b.seg_kind[sg0 + k];
-          const uint64_t w = b.seg_wcet[sg0 + k];
-          s.gKind[k] = kind;
-          s.gW[k] = (uint32_t)min(w, (uint64_t)SAT);
-          s.gAcc[k] = b.seg_accel[sg0 + k];
-          s.gUnit[k] = b.seg_unit[sg0 + k];
-          bad |= (w >= LIM);
-        }
-        n_aseg += __popc(__ballot_sync(0xffffffffu, k < nseg && kind == 1));
-      }
-      for (uint32_t k = lane; k < nch; k += 32) {
-        const uint64_t T = b.chain_T[c0 + k], D = b.chain_D[c0 + k];
-        bad |= (T == 0 || T >= LIM || D >= LIM);
-        s.cT[k] = (uint32_t)min(T, (uint64_t)SAT);
-        s.cD[k] = (uint32_t)min(D, (uint64_t)SAT);
-        s.cPrio[k] = b.chain_prio[c0 + k];
-        s.cCls[k] = b.chain_class[c0 + k];
-        s.cCb0[k] = b.chain_cb_off[c0 + k] - cb0;
-        s.cNcb[k] = (uint8_t)min(b.chain_cb_off[c0 + k + 1] - b.chain_cb_off[c0 + k], 255u);
+      // ---- load: chains (lane), accelerators (lane), executors (lane) ---------------------------
+      bool erange = false, edang = false, eaccel = false, eshape = false, edup = false, edl = false, ecore = false;
+      if (lane < nch) {
+        const uint64_t T64 = b.chain_T[c0 + lane], D64 = b.chain_D[c0 + lane];
+        erange |= (T64 == 0 || T64 >= LIM || D64 >= LIM);
+        T = (uint32_t)min(T64, (uint64_t)SAT);
+        D = (uint32_t)min(D64, (uint64_t)SAT);
+        prio = b.chain_prio[c0 + lane];
+        cls = b.chain_class[c0 + lane];
+        cbo = b.chain_cb_off[c0 + lane] - cb0;
+        cbn = b.chain_cb_off[c0 + lane + 1] - cb0 - cbo;
+        edang |= (cbn == 0);
+        eshape |= (cls > 1);
+        edl |= (D == 0 || (cls == 0 && D > T));
       }
       if (lane < nac) {
         const uint32_t n = b.accel_buckets[a0 + lane], u = b.accel_units[a0 + lane];
         const uint64_t e = b.accel_eps[a0 + lane], kp = b.accel_kappa[a0 + lane];
-        bad |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIM || kp >= LIM);
+        erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIM || kp >= LIM);
         s.aN[lane] = n;
         s.aUnits[lane] = u;
         s.aEps[lane] = (uint32_t)min(e, (uint64_t)SAT);
         s.aKeff[lane] = n > 1 ? (uint32_t)min(kp, (uint64_t)SAT) : 0u;  // A6
         s.aServer[lane] = b.accel_server_core[a0 + lane];
       }
-      __syncwarp();
-      if (lane == 0) {
-        uint32_t ub = 0;
-        for (uint32_t a = 0; a < nac; a++) { s.aUbase[a] = ub; ub += s.aUnits[a]; }
-        n_unit = ub;
-      }
-      n_unit = __shfl_sync(0xffffffffu, n_unit, 0);
-      if (warp_any(bad) || n_aseg > MAXA || n_unit > MAXU) st = PAAM_SET_ERANGE;
-    }
-    if (st == PAAM_SET_OK) {
-      for (uint32_t k = lane; k < ncb; k += 32) {
-        const uint32_t so = b.cb_seg_off[cb0 + k];
-        s.bSeg0[k] = so - sg0;
-        s.bNseg[k] = (uint8_t)min(b.cb_seg_off[cb0 + k + 1] - so, 255u);
-        s.bExec[k] = (uint8_t)min((uint32_t)b.cb_exec[cb0 + k], 255u);
-      }
-      for (uint32_t k = lane; k < nex; k += 32) {
-        s.xCore[k] = b.exec_core[x0 + k];
-        s.xPrio[k] = b.exec_prio[x0 + k];
-        s.xWait[k] = b.exec_wait[x0 + k];
+      uint32_t xcore = 0xffffffffu, xprio = 0;
+      if (lane < nex) {
+        xcore = b.exec_core[x0 + lane];
+        xprio = b.exec_prio[x0 + lane];
+        const uint32_t w = b.exec_wait[x0 + lane];
+        eshape |= (w > 1);
+        s.xCore[lane] = (uint8_t)xcore;
+        s.xPrio[lane] = xprio;
+        s.xWait[lane] = (uint8_t)w;
       }
       __syncwarp();
-      // callback -> chain, segment -> callback
-      for (uint32_t c = lane; c < nch; c += 32)
-        for (uint32_t j = 0; j < s.cNcb[c]; j++) s.bChain[s.cCb0[c] + j] = (uint8_t)c;
-      for (uint32_t j = lane; j < ncb; j += 32)
-        for (uint32_t k = 0; k < s.bNseg[j]; k++) s.gCb[s.bSeg0[j] + k] = (uint8_t)j;
+      // units: per-accelerator base and total
+      {
+        const uint32_t u = lane < nac ? s.aUnits[lane] : 0u;
+        const uint32_t ub = scan_excl(u, lane);
+        if (lane < nac) s.aUbase[lane] = ub;
+        n_unit = __reduce_add_sync(FULL, u);
+      }
+      // chain start callbacks as a 64-bit mask (bit cbo of every chain)
+      const uint64_t cstart_bit = (lane < nch && cbo < 64) ? (1ull << cbo) : 0ull;
+      cstart = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(cstart_bit >> 32)) << 32) |
+                              __reduce_or_sync(FULL, (uint32_t)cstart_bit);
       __syncwarp();
-      // ---- 2. EDANGLING ---------------------------------------------------------------------------
-      bool bad = false;
-      for (uint32_t c = lane; c < nch; c += 32) bad |= (s.cNcb[c] == 0);
-      for (uint32_t j = lane; j < ncb; j += 32) bad |= (s.bNseg[j] == 0 || s.bExec[j] >= nex);
-      for (uint32_t k = lane; k < nseg; k += 32)
-        bad |= (s.gKind[k] == 1 && s.gAcc[k] < nac && s.gUnit[k] >= s.aUnits[s.gAcc[k]]);
-      if (warp_any(bad)) st = PAAM_SET_EDANGLING;
-    }
-    if (st == PAAM_SET_OK) {  // ---- 3. EACCEL ---------------------------------------------------
-      bool bad = false;
-      for (uint32_t k = lane; k < nseg; k += 32) bad |= (s.gKind[k] == 1 && s.gAcc[k] >= nac);
-      if (warp_any(bad)) st = PAAM_SET_EACCEL;
-    }
-    if (st == PAAM_SET_OK) {  // ---- 4. ESHAPE ---------------------------------------------------
-      bool bad = false;
-      for (uint32_t x = lane; x < nex; x += 32) bad |= (s.xWait[x] > 1);
-      for (uint32_t c = lane; c < nch; c += 32) bad |= (s.cCls[c] > 1);
-      for (uint32_t k = lane; k < nseg; k += 32) {
-        bad |= (s.gKind[k] > 1 || s.gW[k] == 0);
-        if (k > 0 && s.gCb[k - 1] == s.gCb[k]) bad |= (s.gKind[k] == s.gKind[k - 1]);
+      // ---- callbacks: two passes of 32 lanes; each lane walks its segments ----------------------
+      uint32_t prev_exec = 0xffffffffu;
+      for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
+        const uint32_t j = pass * 32 + lane;
+        uint32_t exec = 0xffffffffu, E = 0, na = 0;
+        if (j < ncb) {
+          exec = b.cb_exec[cb0 + j];
+          const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
+          edang |= (se == so) || (exec >= nex);
+          uint32_t prev_kind = 0xffffffffu;
+          for (uint32_t k = so; k < se; k++) {
+            const uint32_t kind = b.seg_kind[k];
+            const uint64_t w = b.seg_wcet[k];
+            erange |= (w >= LIM);
+            eshape |= (kind > 1) || (w == 0) || (kind == prev_kind);
+            prev_kind = kind;
+            if (kind == 0) E = sadd(E, (uint32_t)min(w, (uint64_t)SAT));
+            if (kind == 1) {
+              const uint32_t a = b.seg_accel[k], u = b.seg_unit[k];
+              na++;
+              if (a >= nac) eaccel = true;
+              else edang |= (u >= s.aUnits[a]);
+            }
+          }
+          s.bExec[j] = (uint8_t)min(exec, 255u);
+          s.bE[j] = E;
+          s.bNa[j] = (uint8_t)min(na, 255u);
+        }
+        // previous callback's executor (shuffle; the pass boundary carries lane 31 over)
+        uint32_t pe = __shfl_up_sync(FULL, exec, 1);
+        if (lane == 0) pe = prev_exec;
+        prev_exec = __shfl_sync(FULL, exec, 31);
+        const bool first_of_chain = (j < ncb) && ((cstart >> j) & 1ull);
+        const bool start = (j < ncb) && (first_of_chain || exec != pe);
+        const uint32_t bal = __ballot_sync(FULL, start);
+        runstart |= (uint64_t)bal << (pass * 32);
+        n_aseg += __reduce_add_sync(FULL, na);
       }
-      for (uint32_t j = lane; j < ncb; j += 32) {  // a chain never re-enters an executor (A13)
-        const uint32_t c = s.bChain[j], f = s.cCb0[c];
-        if (j > f && s.bExec[j] != s.bExec[j - 1])
-          for (uint32_t i = f; i + 1 < j; i++) bad |= (s.bExec[i] == s.bExec[j]);
-      }
-      if (warp_any(bad)) st = PAAM_SET_ESHAPE;
-    }
-    if (st == PAAM_SET_OK) {  // ---- 4b. sub-chains and their count ---------------------------------
-      for (uint32_t base = 0; base < ncb; base += 32) {
-        const uint32_t j = base + lane;
-        bool start = false;
-        if (j < ncb) start = (j == s.cCb0[s.bChain[j]]) || (s.bExec[j] != s.bExec[j - 1]);
-        n_sub += __popc(__ballot_sync(0xffffffffu, start));
-      }
-      // sub-chain id of a callback = (number of run starts up to and including it) - 1
+      n_sub = __popcll(runstart);
+      __syncwarp();
+      // A13: a chain never re-enters an executor it left
       for (uint32_t j = lane; j < ncb; j += 32) {
-        uint32_t cnt = 0;
-        for (uint32_t i = 0; i <= j; i++)
-          cnt += (i == s.cCb0[s.bChain[i]]) || (s.bExec[i] != s.bExec[i - 1]);
-        s.bSub[j] = (uint8_t)min(cnt - 1, 255u);
+        if (((runstart >> j) & 1ull) && !((cstart >> j) & 1ull)) {
+          const uint32_t first = 63 - __clzll(cstart & ((2ull << j) - 1));  // chain's first callback
+          for (uint32_t i = first; i + 1 < j; i++) eshape |= (s.bExec[i] == s.bExec[j]);
+        }
       }
-      if (n_sub > MAXS) st = PAAM_SET_ERANGE;
-    }
-    if (st == PAAM_SET_OK) {  // ---- 5. EDUPPRIO --------------------------------------------------
-      bool bad = false;
-      for (uint32_t c = lane; c < nch; c += 32)
-        for (uint32_t d = 0; d < nch; d++) bad |= (d != c && s.cPrio[d] == s.cPrio[c]);
-      for (uint32_t x = lane; x < nex; x += 32)
-        for (uint32_t y = 0; y < nex; y++) bad |= (y != x && s.xCore[y] == s.xCore[x] && s.xPrio[y] == s.xPrio[x]);
-      if (warp_any(bad)) st = PAAM_SET_EDUPPRIO;
-    }
-    if (st == PAAM_SET_OK) {  // ---- 6. EDEADLINE -------------------------------------------------
-      bool bad = false;
-      for (uint32_t c = lane; c < nch; c += 32) bad |= (s.cD[c] == 0 || (s.cCls[c] == 0 && s.cD[c] > s.cT[c]));
-      if (warp_any(bad)) st = PAAM_SET_EDEADLINE;
-    }
-    if (st == PAAM_SET_OK) {  // ---- 7. ECORE (R1) ------------------------------------------------
-      bool bad = false;
-      for (uint32_t x = lane; x < nex; x += 32)
-        for (uint32_t a = 0; a < nac; a++) bad |= (s.xCore[x] == s.aServer[a]);
-      if (warp_any(bad)) st = PAAM_SET_ECORE;
+      // chain ranks and duplicate priorities
+      {
+        uint32_t rk = 0, eq = 0;
+        for (uint32_t d = 0; d < nch; d++) {
+          const uint32_t pd = __shfl_sync(FULL, prio, d);
+          rk += (pd > prio);
+          eq += (pd == prio);
+        }
+        rank = rk;
+        edup |= (lane < nch && eq > 1);
+      }
+      // executors: duplicate (core, priority) and process-priority rank on the core; R1 (ECORE)
+      {
+        uint32_t pr = 0;
+        for (uint32_t y = 0; y < nex; y++) {
+          const uint32_t cy = __shfl_sync(FULL, xcore, y), py = __shfl_sync(FULL, xprio, y);
+          if (y != (uint32_t)lane && cy == xcore) {
+            edup |= (py == xprio);
+            pr += (py > xprio);
+          }
+        }
+        if (lane < nex) {
+          s.xPPrank[lane] = (uint8_t)pr;
+          for (uint32_t a = 0; a < nac; a++) ecore |= (xcore == s.aServer[a]);
+        }
+      }
+      erange |= (n_aseg > MAXA) || (n_unit > MAXU);
+      // first failing class, in the documented order
+      if (__any_sync(FULL, erange)) st = PAAM_SET_ERANGE;
+      else if (__any_sync(FULL, edang)) st = PAAM_SET_EDANGLING;
+      else if (__any_sync(FULL, eaccel)) st = PAAM_SET_EACCEL;
+      else if (__any_sync(FULL, eshape)) st = PAAM_SET_ESHAPE;
+      else if (n_sub > MAXS) st = PAAM_SET_ERANGE;
+      else if (__any_sync(FULL, edup)) st = PAAM_SET_EDUPPRIO;
+      else if (__any_sync(FULL, edl)) st = PAAM_SET_EDEADLINE;
+      else if (__any_sync(FULL, ecore)) st = PAAM_SET_ECORE;
     }
 
     if (lane == 0) {
@@ -196,173 +243,202 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
       r->chain_base = c0;
       r->bin = b.set_bin ? b.set_bin[set] : 0u;
       r->n_out = nch;
+      if (status_out) status_out[set] = st;
+      if (st != PAAM_SET_OK) { r->n_chain = 0; r->n_sub = 0; r->n_aseg = 0; r->n_unit = 0; }
     }
-    if (status_out && lane == 0) status_out[set] = st;
     if (st != PAAM_SET_OK) {
-      if (lane == 0) { r->n_chain = 0; r->n_sub = 0; r->n_aseg = 0; r->n_unit = 0; }
       __syncwarp();
       continue;
     }
 
-    // ======================== derivation (valid set) ==================================================
-    // chain ranks: number of chains with a higher priority (priorities are unique)
-    for (uint32_t c = lane; c < nch; c += 32) {
-      uint32_t rk = 0;
-      for (uint32_t d = 0; d < nch; d++) rk += (s.cPrio[d] > s.cPrio[c]);
-      s.cRank[c] = (uint8_t)rk;
-      s.cUse[c] = 0;
-      s.cNsub[c] = 0;
+    // ======================== derivation (valid set) =================================================
+    const bool is_chain = lane < nch;
+    // chain data by rank; accelerator-segment offsets (callback order) per chain
+    if (is_chain) {
+      s.rank_of[lane] = (uint8_t)rank;
+      s.rT[rank] = T;
+      s.rD[rank] = D;
+      s.rCls[rank] = (uint8_t)cls;
+      s.rIdx[rank] = (uint8_t)lane;
+      s.rCbo[rank] = cbo;
+      s.rNcb[rank] = (uint8_t)cbn;
     }
-    // E_i of each callback: its CPU segments, saturating
-    for (uint32_t j = lane; j < ncb; j += 32) {
-      uint32_t e = 0;
-      for (uint32_t k = 0; k < s.bNseg[j]; k++)
-        if (s.gKind[s.bSeg0[j] + k] == 0) e = sadd(e, s.gW[s.bSeg0[j] + k]);
-      s.bE[j] = e;
-    }
-    for (uint32_t i = lane; i < MAXU * MAXC; i += 32) (&s.W64[0][0])[i] = 0ull;
-    __syncwarp();
-    // accelerator segments in original order: compaction by ballot
+    // per-callback first accelerator segment (exclusive scan over the callback order)
     {
-      uint32_t q0 = 0;
-      for (uint32_t base = 0; base < nseg; base += 32) {
-        const uint32_t k = base + lane;
-        const bool isA = (k < nseg) && s.gKind[k] == 1;
-        const uint32_t bal = __ballot_sync(0xffffffffu, isA);
-        if (isA) {
-          const uint32_t q = q0 + __popc(bal & ((1u << lane) - 1u));
-          const uint32_t j = s.gCb[k], c = s.bChain[j], a = s.gAcc[k];
-          s.qChain[q] = (uint8_t)c;
-          s.qCb[q] = (uint8_t)j;
-          s.qSub[q] = s.bSub[j];
-          s.qAcc[q] = (uint8_t)a;
-          s.qUnit[q] = (uint8_t)(s.aUbase[a] + s.gUnit[k]);
-          s.qAstar[q] = sadd(s.gW[k], sadd(s.aKeff[a], s.aKeff[a]));  // A* = A + 2 kappa_eff
-          atomicOr(&s.cUse[c], 1u << a);
-        }
-        q0 += __popc(bal);
+      uint32_t carry = 0;
+      for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
+        const uint32_t j = pass * 32 + lane;
+        const uint32_t na = j < ncb ? s.bNa[j] : 0u;
+        const uint32_t ex = scan_excl(na, lane);
+        if (j < ncb) s.bA0[j] = (uint8_t)(carry + ex);
+        carry += __reduce_add_sync(FULL, na);
       }
+      if (lane == 0) s.bA0[ncb] = (uint8_t)carry;
     }
     __syncwarp();
-    // buckets (A5): per accelerator, users ranked by priority, groups of ceil(m_a / n)
-    for (uint32_t a = 0; a < nac; a++) {
-      const bool use = (lane < nch) && ((s.cUse[lane] >> a) & 1u);
-      const uint32_t ma = __popc(__ballot_sync(0xffffffffu, use));
-      if (lane < nch) {
-        uint32_t ra = 0;
-        for (uint32_t d = 0; d < nch; d++) ra += ((s.cUse[d] >> a) & 1u) && s.cRank[d] < s.cRank[lane];
-        const uint32_t n = s.aN[a], g = (ma + n - 1) / n;
-        s.cBucket[lane][a] = use ? (uint8_t)(n - 1 - ra / g) : 0xFF;
-      }
-    }
-    __syncwarp();
-    // LP blocking and regrouped weights W
-    for (uint32_t q = lane; q < n_aseg; q += 32) {
-      const uint32_t c = s.qChain[q], u = s.qUnit[q], a = s.qAcc[q];
-      const uint32_t bk = s.cBucket[c][a];
-      uint32_t lpb = 0;
-      for (uint32_t p = 0; p < n_aseg; p++) {
-        const uint32_t d = s.qChain[p];
-        if (s.qUnit[p] == u && s.cRank[d] > s.cRank[c] && s.cBucket[d][a] == bk) lpb = max(lpb, s.qAstar[p]);
-      }
-      s.qLPB[q] = lpb;
-      atomicAdd(&s.W64[u][s.cRank[c]], (unsigned long long)s.qAstar[q]);
-    }
-    // sub-chain table in original order
-    for (uint32_t j = lane; j < ncb; j += 32) {
-      const bool start = (j == s.cCb0[s.bChain[j]]) || (s.bExec[j] != s.bExec[j - 1]);
-      if (start) {
-        const uint32_t u = s.bSub[j];
-        uint32_t n = 1;
-        while (j + n < ncb && s.bSub[j + n] == u) n++;
-        s.uChain[u] = s.bChain[j];
-        s.uExec[u] = s.bExec[j];
-        s.uCb0[u] = (uint8_t)j;
-        s.uNcb[u] = (uint8_t)n;
-      }
-    }
-    __syncwarp();
-    // canonical order (A7): per core, process priority desc, chain rank asc
-    for (uint32_t u = lane; u < n_sub; u += 32) {
-      const uint32_t xu = s.uExec[u], ru = s.cRank[s.uChain[u]];
-      const uint32_t cu = s.xCore[xu], pu = s.xPrio[xu];
-      uint32_t pos = 0;
-      for (uint32_t v = 0; v < n_sub; v++) {
-        const uint32_t xv = s.uExec[v], rv = s.cRank[s.uChain[v]];
-        const uint32_t cv = s.xCore[xv], pv = s.xPrio[xv];
-        pos += (cv < cu) || (cv == cu && (pv > pu || (pv == pu && rv < ru)));
-      }
-      s.uCanon[u] = (uint8_t)pos;
+    // per-chain accelerator-segment count, first index in callback order and in rank order
+    {
+      const uint32_t k = lane;  // rank
       uint32_t na = 0;
-      for (uint32_t q = 0; q < n_aseg; q++) na += (s.qSub[q] == u);
-      s.uNa[u] = (uint8_t)na;
+      if (k < nch) {
+        const uint32_t o = s.rCbo[k];
+        na = s.bA0[o + s.rNcb[k]] - s.bA0[o];
+        s.cA0[s.rIdx[k]] = s.bA0[o];
+      }
+      const uint32_t f = scan_excl(na, lane);
+      if (k < nch) { s.rA0[k] = f; s.rNa[k] = (uint8_t)na; }
+    }
+    // sub-chain id of every callback
+    for (uint32_t j = lane; j < ncb; j += 32) s.bSub[j] = (uint8_t)(__popcll(runstart & ((2ull << j) - 1)) - 1);
+    __syncwarp();
+    // ---- accelerator segments: A*, unit, rank; written in rank order --------------------------------
+    for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
+      const uint32_t j = pass * 32 + lane;
+      if (j < ncb && s.bNa[j]) {
+        const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1;  // chain index of callback j
+        const uint32_t rk = s.rank_of[c];
+        uint32_t q = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
+        const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
+        for (uint32_t k = so; k < se; k++) {
+          if (b.seg_kind[k] != 1) continue;
+          const uint32_t a = b.seg_accel[k];
+          const uint32_t w = (uint32_t)min(b.seg_wcet[k], (uint64_t)SAT);
+          s.qAstar[q] = sadd(w, sadd(s.aKeff[a], s.aKeff[a]));  // A* = A + 2 kappa_eff
+          s.qUnit[q] = (uint8_t)(s.aUbase[a] + b.seg_unit[k]);
+          s.qAcc[q] = (uint8_t)a;
+          s.qCb[q] = (uint8_t)j;
+          s.qRank[q] = (uint8_t)rk;
+          q++;
+        }
+      }
+    }
+    if (lane < (int)n_unit) {
+      uint32_t a = 0;
+      for (uint32_t x = 1; x < nac; x++) if (s.aUbase[x] <= (uint32_t)lane) a = x;
+      s.unitAcc[lane] = (uint8_t)a;
     }
     __syncwarp();
-    // first accelerator segment of each sub-chain in canonical grouping
-    for (uint32_t u = lane; u < n_sub; u += 32) {
-      uint32_t f = 0;
-      for (uint32_t v = 0; v < n_sub; v++) f += (s.uCanon[v] < s.uCanon[u]) ? s.uNa[v] : 0u;
-      s.uA0[u] = (uint8_t)f;
+    // ---- per chain (lane = rank): W[k][u], max A*[u][k], accelerator use mask ------------------------
+    uint32_t use = 0;
+    if (is_chain) {
+      const uint32_t k = lane;
+      for (uint32_t u = 0; u < n_unit; u++) { s.W[k][u] = 0; s.maxA[u][k] = 0; }
+      uint64_t w64[MAXU] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (uint32_t q = s.rA0[k]; q < s.rA0[k] + s.rNa[k]; q++) {
+        const uint32_t u = s.qUnit[q];
+        use |= 1u << s.qAcc[q];
+        s.maxA[u][k] = max(s.maxA[u][k], s.qAstar[q]);
+#pragma unroll
+        for (uint32_t x = 0; x < MAXU; x++) if (x == u) w64[x] += s.qAstar[q];
+      }
+#pragma unroll
+      for (uint32_t x = 0; x < MAXU; x++)
+        if (x < n_unit) s.W[k][x] = w64[x] > SAT ? SAT : (uint32_t)w64[x];
+    } else {
+      for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
     }
     __syncwarp();
-    for (uint32_t q = lane; q < n_aseg; q += 32) {
-      const uint32_t u = s.qSub[q];
-      uint32_t k = 0;
-      for (uint32_t p = 0; p < q; p++) k += (s.qSub[p] == u);
-      s.qPos[q] = (uint8_t)(s.uA0[u] + k);
+    // ---- buckets (A5) and LP blocking per (unit, rank) ---------------------------------
+    for (uint32_t a = 0; a < nac; a++) {
+      const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
+      const uint32_t ma = __popc(U), n = s.aN[a];
+      const uint32_t g = ma ? (ma + n - 1) / n : 1u;
+      const bool user = (U >> lane) & 1u;
+      const uint32_t p = __popc(U & lt);  // position among users in rank order
+      if (is_chain) s.bucket[lane][a] = user ? (uint8_t)(n - 1 - p / g) : (uint8_t)0xFF;
+      // users of a form aligned blocks of g consecutive positions, one block per bucket
+      const uint32_t blk_end = min(((uint32_t)lane / g + 1) * g, ma);
+      for (uint32_t u = s.aUbase[a]; u < s.aUbase[a] + s.aUnits[a]; u++) {
+        if (user) s.cmp[p] = s.maxA[u][lane];
+        __syncwarp();
+        uint32_t v = (uint32_t)lane < ma ? s.cmp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive suffix max
+          const uint32_t y = __shfl_down_sync(FULL, v, o);
+          if ((uint32_t)lane + o < blk_end) v = max(v, y);
+        }
+        const uint32_t nxt = __shfl_down_sync(FULL, v, 1);
+        const uint32_t ex = ((uint32_t)lane + 1 < blk_end) ? nxt : 0u;  // exclusive: lower priorities only
+        __syncwarp();
+        if ((uint32_t)lane < ma) s.cmp[lane] = ex;
+        __syncwarp();
+        s.lpb[u][lane] = user ? s.cmp[p] : 0u;
+        __syncwarp();
+      }
+    }
+    // 2 * sum_{k < r} W[k][u]: the "+1 +1" of mu summed over the HP chains (exact, saturating)
+    for (uint32_t u = 0; u < n_unit; u++) {
+      const uint32_t w = is_chain ? s.W[lane][u] : 0u;
+      const uint32_t incl = scan_sat_incl(w, lane);
+      const uint32_t prev = __shfl_up_sync(FULL, incl, 1);
+      const uint32_t ex = lane == 0 ? 0u : prev;
+      s.pre2[u][lane] = sadd(ex, ex);
     }
     __syncwarp();
 
-    // ---- write the record ---------------------------------------------------------------------------
-    if (lane == 0) { r->n_chain = (uint8_t)nch; r->n_sub = (uint8_t)n_sub; r->n_aseg = (uint8_t)n_aseg; r->n_unit = (uint8_t)n_unit; }
-    // chains by rank
-    for (uint32_t c = lane; c < nch; c += 32) {
-      const uint32_t k = s.cRank[c];
-      uint32_t M, L;
-      make_magic(s.cT[c], &M, &L);
-      uint32_t nsub = 0;
-      for (uint32_t u = 0; u < n_sub; u++) nsub += (s.uChain[u] == c);
-      r->cT[k] = s.cT[c];
-      r->cCut[k] = min(s.cD[c], s.cT[c]);
-      r->cD[k] = s.cD[c];
-      r->cM[k] = M;
-      r->cMisc[k] = L | ((uint32_t)s.cCls[c] << 8) | (c << 16) | (nsub << 24);
+    // ---- sub-chains (lane = sub-chain id, callback order) -------------------------------------------
+    uint32_t s_exec = 0, s_rank = 0, s_key = 0xffffffffu, s_j0 = 0, s_nj = 0;
+    if ((uint32_t)lane < n_sub) {
+      // position of the lane-th set bit of runstart
+      const uint32_t lo = (uint32_t)runstart, hi = (uint32_t)(runstart >> 32);
+      const uint32_t nlo = __popc(lo);
+      s_j0 = (uint32_t)lane < nlo ? __fns(lo, 0, lane + 1) : 32 + __fns(hi, 0, lane + 1 - nlo);
+      const uint64_t later = runstart & ~((2ull << s_j0) - 1);
+      const uint32_t c = __popcll(cstart & ((2ull << s_j0) - 1)) - 1;
+      const uint32_t chain_end = s.rCbo[s.rank_of[c]] + s.rNcb[s.rank_of[c]];
+      const uint32_t nxt = later ? (uint32_t)__ffsll(later) - 1 : ncb;
+      s_nj = min(nxt, chain_end) - s_j0;
+      s_exec = s.bExec[s_j0];
+      s_rank = s.rank_of[c];
+      s_key = ((uint32_t)s.xCore[s_exec] << 16) | ((uint32_t)s.xPPrank[s_exec] << 8) | s_rank;
+      uint32_t mE = 0;
+      for (uint32_t j = s_j0; j < s_j0 + s_nj; j++) mE = max(mE, s.bE[j]);
+      s.sMaxE[lane] = mE;
+      s.sRank[lane] = (uint8_t)s_rank;
+      s.sExec[lane] = (uint8_t)s_exec;
     }
-    for (uint32_t i = lane; i < n_unit * MAXC; i += 32) {
-      const uint32_t u = i / MAXC, k = i % MAXC;
-      const unsigned long long w = s.W64[u][k];
-      r->W[u][k] = w > SAT ? SAT : (uint32_t)w;
+    // canonical order (A7): per core, process priority desc, chain rank asc
+    {
+      uint32_t pos = 0;
+      for (uint32_t l = 0; l < n_sub; l++) pos += (__shfl_sync(FULL, s_key, l) < s_key);
+      if ((uint32_t)lane < n_sub) s.sCanon[lane] = (uint8_t)pos;
     }
-    // sub-chains in canonical order
-    for (uint32_t u = lane; u < n_sub; u += 32) {
-      const uint32_t c = s.uChain[u], x = s.uExec[u], rk = s.cRank[c];
+    __syncwarp();
+    const uint32_t same_exec = __match_any_sync(FULL, (uint32_t)lane < n_sub ? s_exec : 0x100u + lane);
+    const uint32_t my_core = (uint32_t)lane < n_sub ? s.xCore[s_exec] : 0x100u + lane;
+    const uint32_t same_core = __match_any_sync(FULL, my_core);
+    if ((uint32_t)lane < n_sub) {
+      const uint32_t k = s.sCanon[lane];
+      const uint32_t c = s.rIdx[s_rank];
+      // sub-chain's accelerator segments: contiguous in rank order
+      const uint32_t qa = s.rA0[s_rank] + (s.bA0[s_j0] - s.cA0[c]);
+      const uint32_t qn = s.bA0[s_j0 + s_nj] - s.bA0[s_j0];
       uint32_t E = 0;
-      for (uint32_t j = s.uCb0[u]; j < s.uCb0[u] + s.uNcb[u]; j++) E = sadd(E, s.bE[j]);
+      for (uint32_t j = s_j0; j < s_j0 + s_nj; j++) E = sadd(E, s.bE[j]);
       uint32_t eps = 0, base3 = 0, umask = 0;
-      for (uint32_t q = 0; q < n_aseg; q++)
-        if (s.qSub[q] == u) {
-          eps = sadd(eps, s.aEps[s.qAcc[q]]);
-          base3 = sadd(base3, sadd(s.qAstar[q], s.qLPB[q]));
-          umask |= 1u << s.qUnit[q];
-        }
-      uint32_t B = 0;  // B_c = max E_j over callbacks of lower-priority chains on the executor
-      for (uint32_t j = 0; j < ncb; j++)
-        if (s.bExec[j] == x && s.cRank[s.bChain[j]] > rk) B = max(B, s.bE[j]);
-      uint32_t hp = 0, hpp = 0, lp = 0;
-      for (uint32_t v = 0; v < n_sub; v++) {
-        const uint32_t xv = s.uExec[v], rv = s.cRank[s.uChain[v]];
-        const uint32_t bit = 1u << s.uCanon[v];
-        if (v == u) continue;
-        if (xv == x) {
-          if (rv < rk) hp |= bit;
-          else lp |= bit;
-        } else if (s.xCore[xv] == s.xCore[x] && s.xPrio[xv] > s.xPrio[x]) {
-          hpp |= bit;
-        }
+      for (uint32_t q = qa; q < qa + qn; q++) {
+        const uint32_t u = s.qUnit[q];
+        eps = sadd(eps, s.aEps[s.qAcc[q]]);
+        base3 = sadd(base3, sadd(s.qAstar[q], s.lpb[u][s_rank]));
+        umask |= 1u << u;
       }
-      uint32_t pos = 0;  // position of the sub-chain inside its chain
-      for (uint32_t v = 0; v < u; v++) pos += (s.uChain[v] == c);
-      const uint32_t k = s.uCanon[u];
+      uint32_t hp = 0, lp = 0, hpp = 0, B = 0;
+      uint32_t m = same_exec & ~(1u << lane);
+      while (m) {
+        const uint32_t l = __ffs(m) - 1;
+        m &= m - 1;
+        if (s.sRank[l] < s_rank) hp |= 1u << s.sCanon[l];
+        else { lp |= 1u << s.sCanon[l]; B = max(B, s.sMaxE[l]); }  // B_c
+      }
+      m = same_core & ~same_exec;
+      const uint32_t mypp = s.xPPrank[s_exec];
+      while (m) {
+        const uint32_t l = __ffs(m) - 1;
+        m &= m - 1;
+        if (s.xPPrank[s.sExec[l]] < mypp) hpp |= 1u << s.sCanon[l];
+      }
+      // position of this sub-chain inside its chain
+      const uint32_t pos = __popcll(runstart & ((1ull << s_j0) - 1) & ~((1ull << s.rCbo[s_rank]) - 1));
       r->sE[k] = E;
       r->sB[k] = B;
       r->sEps[k] = eps;
@@ -370,19 +446,33 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
       r->sHp[k] = hp;
       r->sHpp[k] = hpp;
       r->sLp[k] = lp;
-      r->sMisc[k] = rk | (umask << 8) | ((uint32_t)(s.xWait[x] == 1) << 16) | (pos << 24);
-      r->sSeg[k] = (uint32_t)s.uA0[u] | ((uint32_t)s.uNa[u] << 8) | (x << 16) | ((uint32_t)s.xCore[x] << 24);
+      r->sMisc[k] = s_rank | (umask << 8) | ((uint32_t)(s.xWait[s_exec] == 1) << 16) | (pos << 24);
+      r->sSeg[k] = qa | (qn << 8) | (s_exec << 16) | ((uint32_t)s.xCore[s_exec] << 24);
     }
-    // accelerator segments grouped by canonical sub-chain
+    // ---- chains by rank ---------------------------------------------------------------------------------
+    if (is_chain) {
+      const uint32_t k = lane;
+      uint32_t M, L;
+      make_magic(s.rT[k], &M, &L);
+      const uint32_t o = s.rCbo[k], nb = s.rNcb[k];
+      const uint64_t rng = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) << o;
+      const uint32_t nsub = __popcll(runstart & rng);
+      r->cT[k] = s.rT[k];
+      r->cCut[k] = min(s.rD[k], s.rT[k]);
+      r->cD[k] = s.rD[k];
+      r->cM[k] = M;
+      r->cMisc[k] = L | ((uint32_t)s.rCls[k] << 8) | ((uint32_t)s.rIdx[k] << 16) | (nsub << 24);
+      for (uint32_t u = 0; u < n_unit; u++) r->W[k][u] = s.W[k][u];
+    }
+    // ---- accelerator segments (rank order) ------------------------------------------------------------
     for (uint32_t q = lane; q < n_aseg; q += 32) {
-      const uint32_t p = s.qPos[q];
-      const uint32_t c = s.qChain[q];
-      r->aBase2[p] = sadd(s.qAstar[q], s.qLPB[q]);
-      r->aEps[p] = s.aEps[s.qAcc[q]];
-      r->aCbE[p] = s.bE[s.qCb[q]];
-      r->aMisc[p] = (uint32_t)s.cRank[c] | ((uint32_t)s.qUnit[q] << 8) | ((uint32_t)s.uCanon[s.qSub[q]] << 16) |
-                    ((uint32_t)s.qCb[q] << 24);
+      const uint32_t u = s.qUnit[q], rk = s.qRank[q];
+      r->aBase2[q] = sadd(sadd(s.qAstar[q], s.lpb[u][rk]), s.pre2[u][rk]);
+      r->aEps[q] = s.aEps[s.qAcc[q]];
+      r->aCbE[q] = s.bE[s.qCb[q]];
+      r->aMisc[q] = rk | (u << 8) | ((uint32_t)s.sCanon[s.bSub[s.qCb[q]]] << 16) | ((uint32_t)s.qCb[q] << 24);
     }
+    if (lane == 0) { r->n_chain = (uint8_t)nch; r->n_sub = (uint8_t)n_sub; r->n_aseg = (uint8_t)n_aseg; r->n_unit = (uint8_t)n_unit; }
     __syncwarp();
   }
 }
@@ -391,11 +481,14 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
 
 int launch_pack(const paam_batch* b, Record* rec, int32_t* status, cudaStream_t st) {
   if (b->n_sets == 0) return PAAM_OK;
-  int dev = 0, sms = 148;
+  int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_kernel, WARPS * 32, 0);
+  if (per_sm < 1) per_sm = 1;
   const uint32_t need = (b->n_sets + WARPS - 1) / WARPS;
-  const uint32_t grid = need < (uint32_t)sms * 16 ? need : (uint32_t)sms * 16;
+  const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
+  const uint32_t grid = need < cap ? need : cap;
   pack_kernel<<<grid, WARPS * 32, 0, st>>>(*b, rec, status);
   count_launch();
   const cudaError_t e = cudaGetLastError();
