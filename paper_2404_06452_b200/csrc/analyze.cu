@@ -32,19 +32,22 @@ struct __align__(16) WarpSmem {
   uint32_t R[MAXS];    // converged R_c (SAT = UNSCHED)
 };
 
-__device__ __forceinline__ void wsum2(uint32_t& a, uint32_t& b) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint32_t xa = __shfl_xor_sync(0xffffffffu, a, o);
-    const uint32_t xb = __shfl_xor_sync(0xffffffffu, b, o);
-    a = sadd(a, xa);
-    b = sadd(b, xb);
-  }
+// Exact saturating warp sums of values <= SAT via the integer reduction unit (REDUX): the 16-bit halves
+// are summed separately (32 * 2^16 < 2^32, no wrap) and recombined in 64 bits.
+__device__ __forceinline__ uint32_t wsum(uint32_t v) {
+  const uint32_t lo = __reduce_add_sync(0xffffffffu, v & 0xffffu);
+  const uint32_t hi = __reduce_add_sync(0xffffffffu, v >> 16);
+  const uint64_t t = ((uint64_t)hi << 16) + lo;
+  return t > SAT ? SAT : (uint32_t)t;
 }
-__device__ __forceinline__ uint32_t wsum(uint32_t a) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) a = sadd(a, __shfl_xor_sync(0xffffffffu, a, o));
-  return a;
+__device__ __forceinline__ void wsum2(uint32_t& a, uint32_t& b) {
+  const uint32_t alo = __reduce_add_sync(0xffffffffu, a & 0xffffu);
+  const uint32_t blo = __reduce_add_sync(0xffffffffu, b & 0xffffu);
+  const uint32_t ahi = __reduce_add_sync(0xffffffffu, a >> 16);
+  const uint32_t bhi = __reduce_add_sync(0xffffffffu, b >> 16);
+  const uint64_t ta = ((uint64_t)ahi << 16) + alo, tb = ((uint64_t)bhi << 16) + blo;
+  a = ta > SAT ? SAT : (uint32_t)ta;
+  b = tb > SAT ? SAT : (uint32_t)tb;
 }
 
 __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restrict__ recs, uint32_t n,

@@ -30,10 +30,21 @@ __device__ __forceinline__ uint32_t mu_magic(uint32_t t, uint32_t M, uint32_t L)
   return (__umulhi((t - 1u) << 1, M) >> L) + 2u;
 }
 __host__ __device__ inline void make_magic(uint32_t T, uint32_t* M, uint32_t* L) {
+#ifdef __CUDA_ARCH__
+  const uint32_t l = T > 1 ? 32u - __clz(T - 1u) : 0u;  // ceil(log2 T)
+  const uint64_t N = 1ull << (31 + l);
+  // M = ceil(N / T): double reciprocal estimate (< 2^33, off by at most a few), then exact fix-up
+  uint64_t m = (uint64_t)((double)N * __drcp_rn((double)T));
+  while (m * T < N) m++;
+  while (m > 0 && (m - 1) * T >= N) m--;
+  *L = l;
+  *M = (uint32_t)m;
+#else
   uint32_t l = 0;
   while (l < 32 && (1ull << l) < T) l++;  // l = ceil(log2 T)
   *L = l;
   *M = (uint32_t)(((1ull << (31 + l)) + T - 1) / T);
+#endif
 }
 
 // ---- packed per-set record (written by pack.cu, read by analyze.cu / simulate.cu) ------------------

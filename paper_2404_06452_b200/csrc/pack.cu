@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
           const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
           edang |= (se == so) || (exec >= nex);
           uint32_t prev_kind = 0xffffffffu;
+#pragma unroll 3
           for (uint32_t k = so; k < se; k++) {
             const uint32_t kind = b.seg_kind[k];
             const uint64_t w = b.seg_wcet[k];
@@ -323,17 +324,12 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
     if (is_chain) {
       const uint32_t k = lane;
       for (uint32_t u = 0; u < n_unit; u++) { s.W[k][u] = 0; s.maxA[u][k] = 0; }
-      uint64_t w64[MAXU] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (uint32_t q = s.rA0[k]; q < s.rA0[k] + s.rNa[k]; q++) {
-        const uint32_t u = s.qUnit[q];
+        const uint32_t u = s.qUnit[q], a = s.qAstar[q];
         use |= 1u << s.qAcc[q];
-        s.maxA[u][k] = max(s.maxA[u][k], s.qAstar[q]);
-#pragma unroll
-        for (uint32_t x = 0; x < MAXU; x++) if (x == u) w64[x] += s.qAstar[q];
+        s.maxA[u][k] = max(s.maxA[u][k], a);
+        s.W[k][u] = sadd(s.W[k][u], a);  // saturating sums are exact (associative on [0, SAT])
       }
-#pragma unroll
-      for (uint32_t x = 0; x < MAXU; x++)
-        if (x < n_unit) s.W[k][x] = w64[x] > SAT ? SAT : (uint32_t)w64[x];
     } else {
       for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
     }
