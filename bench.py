@@ -181,8 +181,8 @@ def run_ours(args):
 
     world, rank, local = dist_setup(args.gpus)
     dev = torch.device("cuda", torch.cuda.current_device())
-    n = args.sets_per_gpu
-    first = rank * n
+    from paper_2404_06452_b200.shard import allreduce_bins, shard_range
+    first, n = shard_range(rank, world, args.sets_per_gpu)
     from gen.inputs import config3_params  # workload recipe (shared input generator params)
     gp = config3_params()
     params = paam.PaamGenParams.from_buffer_copy(bytes(gp))
@@ -207,8 +207,7 @@ def run_ours(args):
         sets.repack(raw, stream=stream)                       # §8(a) step 2 (kernel)
         sets.analyze(wcrt, sched, bins, stream=stream)        # steps 3-6 (kernel)
         if dist is not None:                                  # the one exchange: bin counts
-            with torch.cuda.stream(stream):
-                dist.all_reduce(bins)
+            allreduce_bins(bins, stream=stream)
 
     # ---- warm-up ------------------------------------------------------------------------------------
     for _ in range(args.warmup):
@@ -232,8 +231,7 @@ def run_ours(args):
         sets.analyze(wcrt, sched, bins, stream=stream)
         ev[k][2].record(stream)
         if dist is not None:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(bins)
+            allreduce_bins(bins, stream=stream)
     end.record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
@@ -263,8 +261,7 @@ def run_ours(args):
             hsets.repack(hb, stream=stream)                    # H2D of the raw batch + pack kernel
             hsets.analyze(None, sched, bins, stream=stream)
             if dist is not None:
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(bins)
+                allreduce_bins(bins, stream=stream)
             with torch.cuda.stream(stream):
                 sched_h.copy_(sched, non_blocking=True)       # D2H: verdicts + bin counts
                 bins_h.copy_(bins, non_blocking=True)

@@ -70,7 +70,11 @@ typedef struct {
 } pg_set;
 
 enum { PG_D_M = 1, PG_D_CUT, PG_D_PERIOD, PG_D_CPUONLY, PG_D_ACC, PG_D_UNIT, PG_D_PERM,
-       PG_D_SPIN, PG_D_XEXEC };
+       PG_D_SPIN, PG_D_XEXEC, PG_D_PHASE };
+
+/* Release phase of chain c of set `index` for a simulation seeded with `seed` (DESIGN.md App. A D2):
+ * 0 when seed == 0 (synchronous critical instant), else uniform in [0, T).  Input generation: the
+ * simulator draws no random numbers itself; both sides take the phases from here. */
 
 PG_FN uint64_t pg_mix(uint64_t z) { /* SplitMix64 finaliser */
   z += 0x9E3779B97F4A7C15ull;
@@ -86,6 +90,16 @@ PG_FN uint64_t pg_draw(uint64_t key, uint32_t purpose, uint32_t idx) {
 PG_FN uint32_t pg_bounded(uint64_t r, uint32_t n) { return (uint32_t)(((r >> 32) * (uint64_t)n) >> 32); }
 /* Bernoulli with probability q16 / 65536 */
 PG_FN int pg_coin(uint64_t r, uint32_t q16) { return (uint32_t)(r >> 48) < q16; }
+
+PG_FN uint64_t pg_phase(uint64_t seed, uint64_t index, uint32_t c, uint64_t T) {
+  if (seed == 0 || T == 0) return 0;
+  const uint64_t r = pg_draw(pg_key(seed, index), PG_D_PHASE, c);
+#ifdef __CUDA_ARCH__
+  return __umul64hi(r, T);
+#else
+  return (uint64_t)(((unsigned __int128)r * T) >> 64);
+#endif
+}
 
 /* Returns 0 on success, nonzero if the parameters exceed the generator's caps. */
 PG_FN int pg_check_params(const pg_params* p) {

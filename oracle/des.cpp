@@ -1,2 +1,435 @@
-// des.cpp -- placeholder (DES oracle added later)
-#include "oracle.h"
+// des.cpp -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+//
+// Plain discrete-event simulation of the execution model and of PAAM's arbitration, written from the
+// paper's rules and DESIGN.md App. A (rules D1-D17):
+//   executors   single-threaded, non-preemptive, priority-driven (PiCAS): an idle
+//               executor holding its core picks the ready callback of highest chain priority (older
+//               release, lower callback index on ties) and runs it to completion, accelerator waits
+//               included ("the executor cannot execute any other callback");        D4
+//   cores       preemptive fixed priority among runnable executors by process priority;
+//               SPIN waits keep the core, SUSPEND waits release it;                  D5, D6
+//   PAAM server per request eps (client side, before enqueue), bucket by priority downsampling
+//               (R2), priority queue inside a bucket with FIFO on equal priority (R3, P:320,
+//               P:370), preemption of a lower bucket by a higher one costing kappa to switch out
+//               and kappa to switch back in (R4);                              D6-D11
+//   chains      periodic releases, successors released on completion, comm delay across
+//               executors, BE overrun drops (D14), response = last callback done -
+//               release (D16).
+// Same-timestamp order (D15): (A) every change due now -- unit phase ends / completions, eps and CPU
+// completions, comm arrivals, releases -- until stable, then (B) executor choice, core dispatch,
+// unit dispatch; repeat until nothing changes.  Time then jumps to the earliest next event.
+#include <cstring>
+#include <thread>
+
+#include "model.h"
+
+using namespace oracle_model;
+
+namespace {
+
+const int QCAP = 8;  // live instances per chain; a release beyond it is skipped and counted (A-D14b)
+
+enum EvKind {
+  EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_ENQUEUE, EV_ACC_START,
+  EV_ACC_PREEMPT, EV_ACC_RESUME, EV_ACC_DONE, EV_CB_DONE, EV_CHAIN_DONE
+};
+
+enum Phase { P_NONE = 0, P_CPU, P_EPS_SPIN, P_EPS_SUSP, P_WAIT };
+enum UState { U_IDLE = 0, U_RUN, U_SWOUT, U_SWIN };
+
+struct Instance {
+  bool live = false;
+  u64 release = 0, k = 0;
+  int cb = 0;
+  int state = 0;  // 0 READY at its callback's executor, 1 RUNNING, 2 TRANSIT until ready_at
+  u64 ready_at = 0;
+};
+
+struct ExecState {
+  int chain = -1, slot = -1, seg = 0;
+  int phase = P_NONE;
+  u64 rem = 0, timer = 0;
+};
+
+struct Req {
+  int chain, slot, cb, seg, exec, bucket;
+  u32 prio;
+  u64 k, seq, rem;
+  bool started;
+};
+
+struct UnitState {
+  int acc = 0;
+  std::vector<Req> q;
+  int state = U_IDLE, cur = -1;
+  u64 end = 0;
+};
+
+u64 fnv1a64(const unsigned char* p, int n) {
+  u64 h = 0xcbf29ce484222325ull;
+  for (int i = 0; i < n; i++) { h ^= p[i]; h *= 0x100000001b3ull; }
+  return h;
+}
+
+struct Sim {
+  const System& s;
+  std::vector<std::vector<int>> bucket;
+  std::vector<int> unit_base;
+  u64 horizon, t = 0;
+  std::vector<u64> phase, next_k;
+  std::vector<std::vector<Instance>> inst;  // [chain][QCAP]
+  std::vector<ExecState> ex;
+  std::vector<UnitState> units;
+  std::vector<int> core_owner;              // by core id (0..255), -1 none
+  u64 seq = 0, digest = 0;
+  // statistics per chain (D16)
+  std::vector<u64> max_resp, count, sum_resp, misses, drops, overflows;
+
+  Sim(const System& sys, u64 hz, const std::vector<u64>& ph) : s(sys), horizon(hz), phase(ph) {
+    bucket = bucket_map(s);
+    int ub = 0;
+    for (const Accel& a : s.accels) { unit_base.push_back(ub); ub += a.units; }
+    for (int a = 0; a < (int)s.accels.size(); a++)
+      for (int u = 0; u < s.accels[a].units; u++) { UnitState us; us.acc = a; units.push_back(us); }
+    const size_t m = s.chains.size();
+    next_k.assign(m, 0);
+    inst.assign(m, std::vector<Instance>(QCAP));
+    ex.assign(s.execs.size(), ExecState());
+    core_owner.assign(256, -1);
+    max_resp.assign(m, 0); count.assign(m, 0); sum_resp.assign(m, 0); misses.assign(m, 0);
+    drops.assign(m, 0); overflows.assign(m, 0);
+  }
+
+  void event(int kind, int chain, int cb, int seg, int unit, int bk) {
+    unsigned char rec[32];
+    const uint32_t f[6] = {(uint32_t)kind, (uint32_t)chain, (uint32_t)cb, (uint32_t)seg, (uint32_t)unit, (uint32_t)bk};
+    std::memcpy(rec, &t, 8);
+    std::memcpy(rec + 8, f, 24);
+    digest += fnv1a64(rec, 32);  // D17 (order-independent within the multiset of records)
+  }
+
+  const Cb& cbk(int c, int j) const { return s.chains[c].cbs[j]; }
+  int unit_of(const Seg& g) const { return unit_base[g.accel] + g.unit; }
+
+  // ---- executors --------------------------------------------------------------------------------
+  bool has_ready(int x) const {
+    for (int c = 0; c < (int)s.chains.size(); c++)
+      for (const Instance& I : inst[c])
+        if (I.live && I.state == 0 && cbk(c, I.cb).exec == x) return true;
+    return false;
+  }
+  bool runnable(int x) const {
+    const ExecState& e = ex[x];
+    if (e.phase == P_NONE) return has_ready(x);
+    if (e.phase == P_CPU || e.phase == P_EPS_SPIN) return true;
+    if (e.phase == P_WAIT) return s.execs[x].wait == 1;  // SPIN keeps the core busy
+    return false;                                        // SUSPEND during eps
+  }
+  bool on_core(int x) const { return core_owner[s.execs[x].core] == x; }
+
+  void begin_segment(int x) {
+    ExecState& e = ex[x];
+    const Seg& g = cbk(e.chain, inst[e.chain][e.slot].cb).segs[e.seg];
+    if (g.kind == 0) {
+      e.phase = P_CPU;
+      e.rem = g.wcet;
+    } else {
+      const u64 eps = s.accels[g.accel].eps;
+      if (s.execs[x].wait == 1) { e.phase = P_EPS_SPIN; e.rem = eps; }
+      else { e.phase = P_EPS_SUSP; e.timer = t + eps; }
+    }
+  }
+
+  void start_job(int x) {  // D4
+    int bc = -1, bs = -1;
+    for (int c = 0; c < (int)s.chains.size(); c++)
+      for (int k = 0; k < QCAP; k++) {
+        const Instance& I = inst[c][k];
+        if (!I.live || I.state != 0 || cbk(c, I.cb).exec != x) continue;
+        if (bc < 0) { bc = c; bs = k; continue; }
+        const Instance& B = inst[bc][bs];
+        const u32 pi = s.chains[c].prio, pb = s.chains[bc].prio;
+        if (pi > pb || (pi == pb && (I.release < B.release || (I.release == B.release && I.cb < B.cb)))) { bc = c; bs = k; }
+      }
+    Instance& I = inst[bc][bs];
+    I.state = 1;
+    ExecState& e = ex[x];
+    e.chain = bc; e.slot = bs; e.seg = 0;
+    event(EV_CB_START, bc, I.cb, 0, -1, -1);
+    begin_segment(x);
+  }
+
+  void advance_segment(int x) {
+    ExecState& e = ex[x];
+    Instance& I = inst[e.chain][e.slot];
+    const Cb& cb = cbk(e.chain, I.cb);
+    event(EV_SEG_DONE, e.chain, I.cb, e.seg, -1, -1);
+    e.seg++;
+    if (e.seg < (int)cb.segs.size()) { begin_segment(x); return; }
+    event(EV_CB_DONE, e.chain, I.cb, -1, -1, -1);
+    const int c = e.chain;
+    if (I.cb + 1 < (int)s.chains[c].cbs.size()) {
+      const int nx = cbk(c, I.cb + 1).exec;
+      I.cb++;
+      if (nx == x) I.state = 0;
+      else { I.state = 2; I.ready_at = t + s.comm; }  // D13
+    } else {
+      const u64 resp = t - I.release;  // D16
+      max_resp[c] = std::max(max_resp[c], resp);
+      count[c]++;
+      sum_resp[c] += resp;
+      if (resp > s.chains[c].D) misses[c]++;
+      event(EV_CHAIN_DONE, c, -1, -1, -1, -1);
+      I.live = false;
+    }
+    e.chain = -1; e.slot = -1; e.phase = P_NONE;
+  }
+
+  // ---- accelerator units ------------------------------------------------------------------------
+  int best_req(const UnitState& U) const {  // D8
+    int best = -1;
+    for (int i = 0; i < (int)U.q.size(); i++) {
+      if (i == U.cur) continue;
+      const Req& r = U.q[i];
+      if (best < 0) { best = i; continue; }
+      const Req& b = U.q[best];
+      if (r.bucket != b.bucket) { if (r.bucket > b.bucket) best = i; continue; }
+      if (r.started != b.started) { if (r.started) best = i; continue; }
+      if (r.prio != b.prio) { if (r.prio > b.prio) best = i; continue; }
+      if (r.seq < b.seq) best = i;
+    }
+    return best;
+  }
+  u64 kappa_eff(int a) const { return s.accels[a].buckets > 1 ? s.accels[a].kappa : 0; }
+
+  // ---- phase A: everything due at t, until stable -----------------------------------------------
+  bool phase_A() {
+    bool any = false;
+    for (;;) {
+      bool changed = false;
+      // (1) accelerator units, index order
+      for (int u = 0; u < (int)units.size(); u++) {
+        UnitState& U = units[u];
+        if ((U.state == U_SWOUT || U.state == U_SWIN) && U.end == t) {
+          if (U.state == U_SWOUT) { U.state = U_IDLE; U.cur = -1; }
+          else U.state = U_RUN;
+          changed = true;
+        }
+        if (U.state == U_RUN && U.q[U.cur].rem == 0) {
+          const Req r = U.q[U.cur];
+          event(EV_ACC_DONE, r.chain, r.cb, r.seg, u, r.bucket);
+          U.q.erase(U.q.begin() + U.cur);
+          U.state = U_IDLE; U.cur = -1;
+          advance_segment(r.exec);  // D12
+          changed = true;
+        }
+      }
+      // (2) executor CPU work / eps completions, index order; enqueues collected and sequenced (D7)
+      std::vector<int> enq;
+      for (int x = 0; x < (int)ex.size(); x++) {
+        ExecState& e = ex[x];
+        if (e.phase == P_CPU && e.rem == 0) { advance_segment(x); changed = true; }
+        else if ((e.phase == P_EPS_SPIN && e.rem == 0) || (e.phase == P_EPS_SUSP && e.timer == t)) {
+          e.phase = P_WAIT;
+          enq.push_back(x);
+          changed = true;
+        }
+      }
+      std::sort(enq.begin(), enq.end(), [&](int a, int b) {
+        const ExecState &ea = ex[a], &eb = ex[b];
+        if (ea.chain != eb.chain) return ea.chain < eb.chain;
+        return inst[ea.chain][ea.slot].k < inst[eb.chain][eb.slot].k;
+      });
+      for (int x : enq) {
+        const ExecState& e = ex[x];
+        const Instance& I = inst[e.chain][e.slot];
+        const Seg& g = cbk(e.chain, I.cb).segs[e.seg];
+        Req r;
+        r.chain = e.chain; r.slot = e.slot; r.cb = I.cb; r.seg = e.seg; r.exec = x;
+        r.bucket = bucket[e.chain][g.accel]; r.prio = s.chains[e.chain].prio;
+        r.k = I.k; r.seq = seq++; r.rem = g.wcet; r.started = false;
+        const int u = unit_of(g);
+        units[u].q.push_back(r);
+        event(EV_REQ_ENQUEUE, r.chain, r.cb, r.seg, u, r.bucket);
+      }
+      // (3) comm arrivals
+      for (int c = 0; c < (int)s.chains.size(); c++)
+        for (Instance& I : inst[c])
+          if (I.live && I.state == 2 && I.ready_at == t) { I.state = 0; changed = true; }
+      // (4) releases, chain index order (D2, D14)
+      for (int c = 0; c < (int)s.chains.size(); c++) {
+        const u64 r = phase[c] + next_k[c] * s.chains[c].T;
+        if (r != t || r >= horizon) continue;
+        if (s.chains[c].cls == 1)
+          for (Instance& I : inst[c])
+            if (I.live && I.state == 0 && I.cb == 0) {
+              I.live = false;
+              drops[c]++;
+              event(EV_DROP, c, -1, -1, -1, -1);
+            }
+        int slot = -1;
+        for (int k = 0; k < QCAP; k++) if (!inst[c][k].live) { slot = k; break; }
+        if (slot < 0) {
+          overflows[c]++;
+          event(EV_OVERFLOW, c, -1, -1, -1, -1);
+        } else {
+          Instance& I = inst[c][slot];
+          I.live = true; I.release = t; I.k = next_k[c]; I.cb = 0; I.state = 0;
+          event(EV_RELEASE, c, -1, -1, -1, -1);
+        }
+        next_k[c]++;
+        changed = true;
+      }
+      if (!changed) break;
+      any = true;
+    }
+    return any;
+  }
+
+  // ---- phase B: executor choice, core dispatch, unit dispatch -----------------------------------
+  bool phase_B() {
+    bool changed = false;
+    for (int x = 0; x < (int)ex.size(); x++)
+      if (ex[x].phase == P_NONE && on_core(x) && has_ready(x)) { start_job(x); changed = true; }
+    std::vector<int> cores;
+    for (const Exec& e : s.execs) if (std::find(cores.begin(), cores.end(), e.core) == cores.end()) cores.push_back(e.core);
+    for (int core : cores) {
+      int best = -1;
+      for (int x = 0; x < (int)ex.size(); x++)
+        if (s.execs[x].core == core && runnable(x) && (best < 0 || s.execs[x].prio > s.execs[best].prio)) best = x;
+      if (core_owner[core] != best) { core_owner[core] = best; changed = true; }
+    }
+    for (int u = 0; u < (int)units.size(); u++) {
+      UnitState& U = units[u];
+      const u64 kap = kappa_eff(U.acc);
+      if (U.state == U_IDLE) {
+        const int i = best_req(U);
+        if (i >= 0) {
+          Req& r = U.q[i];
+          U.cur = i;
+          if (r.started) {  // D10: switch back in
+            U.state = U_SWIN; U.end = t + kap;
+            event(EV_ACC_RESUME, r.chain, r.cb, r.seg, u, r.bucket);
+          } else {
+            r.started = true;
+            U.state = U_RUN;
+            event(EV_ACC_START, r.chain, r.cb, r.seg, u, r.bucket);
+          }
+          changed = true;
+        }
+      } else if (U.state == U_RUN && s.accels[U.acc].buckets > 1) {  // D9
+        const int i = best_req(U);
+        if (i >= 0 && U.q[i].bucket > U.q[U.cur].bucket) {
+          const Req& r = U.q[U.cur];
+          event(EV_ACC_PREEMPT, r.chain, r.cb, r.seg, u, r.bucket);
+          U.state = U_SWOUT; U.end = t + kap;
+          changed = true;
+        }
+      }
+    }
+    return changed;
+  }
+
+  u64 next_time() const {
+    u64 nt = UINT64_MAX;
+    for (int c = 0; c < (int)s.chains.size(); c++) {
+      const u64 r = phase[c] + next_k[c] * s.chains[c].T;
+      if (r < horizon) nt = std::min(nt, r);
+    }
+    for (int x = 0; x < (int)ex.size(); x++) {
+      const ExecState& e = ex[x];
+      if ((e.phase == P_CPU || e.phase == P_EPS_SPIN) && on_core(x)) nt = std::min(nt, t + e.rem);
+      if (e.phase == P_EPS_SUSP) nt = std::min(nt, e.timer);
+    }
+    for (int c = 0; c < (int)s.chains.size(); c++)
+      for (const Instance& I : inst[c])
+        if (I.live && I.state == 2) nt = std::min(nt, I.ready_at);
+    for (const UnitState& U : units) {
+      if (U.state == U_RUN) nt = std::min(nt, t + U.q[U.cur].rem);
+      if (U.state == U_SWOUT || U.state == U_SWIN) nt = std::min(nt, U.end);
+    }
+    return nt;
+  }
+
+  void advance(u64 dt) {
+    for (int x = 0; x < (int)ex.size(); x++)
+      if ((ex[x].phase == P_CPU || ex[x].phase == P_EPS_SPIN) && on_core(x)) ex[x].rem -= dt;
+    for (UnitState& U : units)
+      if (U.state == U_RUN) U.q[U.cur].rem -= dt;
+  }
+
+  void run() {
+    t = 0;
+    for (;;) {
+      for (;;) {  // D15
+        const bool a = phase_A();
+        const bool b = phase_B();
+        if (!a && !b) break;
+      }
+      const u64 nt = next_time();
+      if (nt == UINT64_MAX) break;
+      advance(nt - t);
+      t = nt;
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, uint64_t seed, uint64_t first_index,
+                                         const uint64_t* phases_or_null, uint64_t* out_resp, uint64_t* out_count,
+                                         uint64_t* out_misc, uint64_t* out_digest, const uint64_t* bound,
+                                         int64_t* out_violations, int nthreads) {
+  if (!b) return -1;
+  const uint32_t n = b->n_sets;
+  const int T = nthreads > 0 ? nthreads : 1;
+  std::vector<int64_t> viol(T, 0);
+  auto work = [&](uint32_t i, int th) {
+    System s = read_set(b, i);
+    const uint32_t c0 = b->set_chain_off[i];
+    const size_t m = s.chains.size();
+    if (validate(s) != OR_OK) {
+      for (size_t c = 0; c < m; c++) {
+        if (out_resp) out_resp[c0 + c] = 0;
+        if (out_count) out_count[c0 + c] = 0;
+        if (out_misc) for (int k = 0; k < 3; k++) out_misc[3 * (c0 + c) + k] = 0;
+      }
+      if (out_digest) out_digest[i] = 0;
+      return;
+    }
+    std::vector<u64> ph(m);
+    for (size_t c = 0; c < m; c++)
+      ph[c] = phases_or_null ? phases_or_null[c0 + c] : pg_phase(seed, first_index + i, (uint32_t)c, s.chains[c].T);
+    Sim sim(s, horizon, ph);
+    sim.run();
+    // sim <= bound is claimed only for sets the analysis declares schedulable: Lemma 1's
+    // arrival bound presumes schedulable interferers, so no bound is checked elsewhere.
+    bool set_sched = bound != nullptr;
+    for (size_t c = 0; c < m && bound; c++)
+      if (s.chains[c].cls == 0 && (bound[c0 + c] == OR_UNSCHED || bound[c0 + c] > s.chains[c].D)) set_sched = false;
+    for (size_t c = 0; c < m; c++) {
+      if (out_resp) out_resp[c0 + c] = sim.max_resp[c];
+      if (out_count) out_count[c0 + c] = sim.count[c];
+      if (out_misc) {
+        out_misc[3 * (c0 + c) + 0] = sim.misses[c];
+        out_misc[3 * (c0 + c) + 1] = sim.drops[c];
+        out_misc[3 * (c0 + c) + 2] = sim.overflows[c];
+      }
+      if (set_sched && s.chains[c].cls == 0 && sim.max_resp[c] > bound[c0 + c]) viol[th]++;
+    }
+    if (out_digest) out_digest[i] = sim.digest;
+  };
+  if (T <= 1 || n < 16) {
+    for (uint32_t i = 0; i < n; i++) work(i, 0);
+  } else {
+    std::vector<std::thread> th;
+    for (int k = 0; k < T; k++)
+      th.emplace_back([=, &work]() {
+        for (uint64_t i = (uint64_t)n * k / T; i < (uint64_t)n * (k + 1) / T; i++) work((uint32_t)i, k);
+      });
+    for (auto& x : th) x.join();
+  }
+  if (out_violations)
+    for (int k = 0; k < T; k++) *out_violations += viol[k];
+  return 0;
+}

@@ -77,6 +77,15 @@ int32_t oracle_generate_analyze(const void* params, uint64_t seed, uint64_t firs
                                 uint32_t wcrt_stride, uint8_t* out_sched, int64_t* out_bins,
                                 uint64_t* counters, int nthreads);
 
+/* Discrete-event simulation (des.cpp, DESIGN.md App. A): per chain max / count of observed end-to-end
+ * responses, misc[3] = {deadline misses, BE drops, overflowed releases}; per set an order-independent
+ * FNV-1a-64 digest of the event records; violations of `bound` counted for CRITICAL chains of sets
+ * whose every CRITICAL chain has bound <= D (the analysis' schedulable sets).  phases_or_null: explicit release phases per chain (brute force), else pg_phase(). */
+int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, uint64_t seed, uint64_t first_index,
+                              const uint64_t* phases_or_null, uint64_t* out_resp, uint64_t* out_count,
+                              uint64_t* out_misc, uint64_t* out_digest, const uint64_t* bound,
+                              int64_t* out_violations, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

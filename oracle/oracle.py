@@ -52,11 +52,10 @@ def lib():
                                                  ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32,
                                                  ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
                                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
-        if hasattr(_lib, "oracle_simulate_batch"):
-            _lib.oracle_simulate_batch.argtypes = [ctypes.POINTER(OrBatch), ctypes.c_uint64, ctypes.c_uint64,
-                                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                                   ctypes.c_int]
+        _lib.oracle_simulate_batch.argtypes = [ctypes.POINTER(OrBatch), ctypes.c_uint64, ctypes.c_uint64,
+                                               ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_int]
     return _lib
 
 
@@ -122,3 +121,25 @@ def generate_analyze(params: GenParams, seed: int, first: int, n: int, comm_cost
                                        _ptr(wcrt), stride, _ptr(sched), _ptr(bins), _ptr(cnt), nthreads)
     assert rc == 0, rc
     return wcrt, sched[:n], bins[:params.n_bins * 2], cnt
+
+
+def simulate(batch: dict, horizon: int, seed: int = 0, first_index: int = 0, phases=None, bound=None,
+             nthreads: int = 1) -> dict:
+    """Oracle DES.  Returns dict(resp, count, misses, drops, overflows per chain; digest per set;
+    violations)."""
+    b = make_batch(batch)
+    nch = int(batch["set_chain_off"][-1])
+    n = batch["n_sets"]
+    resp = np.zeros(max(nch, 1), np.uint64)
+    cnt = np.zeros(max(nch, 1), np.uint64)
+    misc = np.zeros(max(3 * nch, 3), np.uint64)
+    dig = np.zeros(max(n, 1), np.uint64)
+    viol = np.zeros(1, np.int64)
+    ph = None if phases is None else np.ascontiguousarray(phases, np.uint64)
+    bd = None if bound is None else np.ascontiguousarray(bound, np.uint64)
+    rc = lib().oracle_simulate_batch(ctypes.byref(b), horizon, seed, first_index, _ptr(ph), _ptr(resp), _ptr(cnt),
+                                     _ptr(misc), _ptr(dig), _ptr(bd), _ptr(viol), nthreads)
+    assert rc == 0
+    misc = misc[:3 * nch].reshape(-1, 3) if nch else np.zeros((0, 3), np.uint64)
+    return dict(resp=resp[:nch], count=cnt[:nch], misses=misc[:, 0], drops=misc[:, 1], overflows=misc[:, 2],
+                digest=dig[:n], violations=int(viol[0]))
