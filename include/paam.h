@@ -168,15 +168,21 @@ int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* out_status, p
 int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcrt, uint8_t* out_sched,
                  int64_t* out_bins, paam_stream_t stream);
 
-/* paam_simulate -- §8(a) steps 7-8.  Discrete-event simulation of every set over [0, horizon):
- * chain release phases are 0 when seed == 0, else uniform in [0, T) from (seed, set, chain).
+/* paam_simulate -- §8(a) steps 7-8.  Discrete-event simulation of every set (DESIGN.md App. A,
+ * rules D1-D17: PiCAS executors, fixed-priority cores, PAAM bucket queues with cross-bucket
+ * preemption, eps per request, kappa per switch) over releases in [0, horizon), run until every
+ * released instance completes.  Chain c of set i is released at phase + k*T with phase = 0 when
+ * seed == 0, else pg_phase(seed, first_index + i, c, T) (gen/paam_gen.h).
  *   out_resp   [n_chains total] maximum observed end-to-end response time per chain (0 if none).
- *   out_digest [n] FNV-1a-64 over the canonical event stream (may be NULL).
- *   bound      [n_chains total] WCRTs from paam_analyze, or NULL.  With a bound, for every CRITICAL
- *              chain with a finite bound, out_resp > bound increments *out_violations (int64, +=).
- * Device pointers only. */
-int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed,
-                  uint64_t* out_resp, uint64_t* out_digest, const uint64_t* bound,
+ *   out_count  [n_chains total] completed instances per chain (may be NULL).
+ *   out_digest [n] order-independent FNV-1a-64 digest of the event records (may be NULL).
+ *   bound      [n_chains total] WCRTs from paam_analyze, or NULL.  In every set whose CRITICAL
+ *              chains all have bound <= D (the analysis' schedulable sets, Lemma 1), each
+ *              CRITICAL chain with out_resp > bound adds 1 to *out_violations (int64, +=).
+ * Reads the raw batch the handle was packed from: a DEVICE batch must still be alive (a HOST batch
+ * was staged by paam_pack).  Device pointers only. */
+int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
+                  uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
                   int64_t* out_violations, paam_stream_t stream);
 
 /* Handle queries (synchronous, small). */

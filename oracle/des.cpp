@@ -27,7 +27,7 @@ using namespace oracle_model;
 
 namespace {
 
-const int QCAP = 8;  // live instances per chain; a release beyond it is skipped and counted (A-D14b)
+const int QCAP = 4;  // live instances per chain; a release beyond it is skipped and counted (D14b)
 
 enum EvKind {
   EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_ENQUEUE, EV_ACC_START,

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
 
 }  // namespace
 
+#ifndef PAAM_WARP_EMU
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st) {
   if (n == 0) return PAAM_OK;
@@ -260,5 +261,7 @@ int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags,
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "analyze_kernel launch");
 }
+
+#endif  // PAAM_WARP_EMU
 
 }  // namespace paam

@@ -18,6 +18,7 @@ struct paam_sets {
   size_t stage_bytes;
   int32_t* dstatus;  // device status staging for host batches
   uint32_t dstatus_cap;
+  paam_batch dev;    // the packed batch with device pointers (paam_simulate reads its structure)
 };
 
 namespace paam {
@@ -138,6 +139,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
         return fail_cuda(e, "paam_pack: status D2H");
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_pack: synchronize");
   }
+  sets->dev = d;
   sets->n_sets = batch->n_sets;
   sets->n_chains = batch->n_chains;
   sets->n_bins = batch->set_bin ? batch->n_bins : 0;
@@ -174,6 +176,15 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_analyze: n exceeds the packed sets");
   return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
                         sets->n_bins ? out_bins : nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
+                             uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
+                             int64_t* out_violations, paam_stream_t stream) {
+  if (!sets) return fail(PAAM_EINVAL, "NULL handle");
+  if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_simulate: n exceeds the packed sets");
+  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, out_resp, out_count, out_digest,
+                         bound, out_violations, (cudaStream_t)stream);
 }
 
 extern "C" int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins) {

@@ -7,11 +7,23 @@
 // the paper's min(UNB, C) because any C >= SAT is itself above the cutoff.
 #pragma once
 #include <cstdint>
+#ifdef PAAM_WARP_EMU
+#include "../../tools/warp_emu/emu.h"  // host-side debugging emulation of the warp intrinsics
+#else
 #include <cuda_runtime.h>
+#endif
 
 #include "../../include/paam.h"
 
 namespace paam {
+
+#ifndef PAAM_WARP_EMU
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+#endif
 
 constexpr uint32_t SAT = 0x7FFFFFFFu;
 constexpr uint64_t LIM = 0x7FFFFFFFull;  // inputs must be < LIM (validation, PAAM_SET_ERANGE)
@@ -93,6 +105,7 @@ struct __align__(16) Record {
 static_assert(sizeof(Record) % 16 == 0, "record must be 16-byte aligned");
 
 // ---- launch bookkeeping ---------------------------------------------------------------------------
+#ifndef PAAM_WARP_EMU
 void count_launch();
 int fail_cuda(cudaError_t e, const char* what);
 int fail(int code, const char* what);
@@ -101,5 +114,9 @@ int fail(int code, const char* what);
 int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status, cudaStream_t st);
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st);
+int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
+                    uint64_t first_index, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
+                    const uint64_t* bound, int64_t* out_viol, cudaStream_t st);
+#endif
 
 }  // namespace paam

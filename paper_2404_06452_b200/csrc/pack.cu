@@ -54,11 +54,6 @@ struct Scratch {
   uint32_t sMaxE[MAXS];
 };
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 
 // saturating inclusive prefix sum over lanes (Hillis-Steele; min(a+b, SAT) is associative on [0, SAT])
 __device__ __forceinline__ uint32_t scan_sat_incl(uint32_t v, int lane) {
@@ -475,6 +470,7 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
 
 }  // namespace
 
+#ifndef PAAM_WARP_EMU
 int launch_pack(const paam_batch* b, Record* rec, int32_t* status, cudaStream_t st) {
   if (b->n_sets == 0) return PAAM_OK;
   int dev = 0, sms = 148, per_sm = 1;
@@ -490,5 +486,7 @@ int launch_pack(const paam_batch* b, Record* rec, int32_t* status, cudaStream_t 
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "pack_kernel launch");
 }
+
+#endif  // PAAM_WARP_EMU
 
 }  // namespace paam

@@ -1,8 +1,597 @@
-// simulate.cu -- §8(a) steps 7-8 (placeholder until the DES kernel lands).
+// simulate.cu -- §8(a) steps 7-8: discrete-event simulation of PAAM arbitration, one warp per set.
+//
+// Semantics: DESIGN.md App. A (rules D1-D17), derived from the paper's execution model
+// (PiCAS executors P:135-136, fixed-priority cores P:136, PAAM server rules R1-R4 P:366-373,
+// eps / kappa overheads P:374, bucket FIFO on equal priority P:320).  Lane ownership:
+//   lane k  = chain of rank k (k = 0 highest priority): its <= QCAP live instances, release
+//             schedule, statistics;
+//   lane x  = executor x in canonical order (core asc, process priority desc): job, phase, work;
+//   lane u  = accelerator unit u: state (idle / run / switch-out / switch-in), current request.
+// Every timestamp is settled like this (D15): phase A = (1) unit phase ends and completions,
+// (2) executor CPU / eps completions with enqueues sequenced by (chain, instance) (D7),
+// (3) comm arrivals, (4) releases -- repeated until stable; phase B = (5) executor choice,
+// (6) core dispatch, (7) unit dispatch; A/B repeat until nothing changes.  Each sub-phase is
+// lane-parallel over the entities it touches (they touch disjoint state; shared statistics use
+// shared-memory atomics); "best" choices are warp reductions over rank-ordered lanes, so the
+// highest priority is the lowest set bit of a ballot.  Time then jumps to the warp-min next event.
+// The event digest is a sum of per-record FNV-1a-64 hashes (order independent), reduced at the end.
+#include "../../gen/paam_gen.h"
 #include "common.cuh"
-using namespace paam;
-extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t* out_resp,
-                             uint64_t* out_digest, const uint64_t* bound, int64_t* out_violations,
-                             paam_stream_t stream) {
-  return fail(PAAM_EINVAL, "paam_simulate: not implemented yet");
+
+struct paam_sets;  // defined in api.cu
+
+namespace paam {
+
+namespace {
+
+constexpr int SW = 4;      // warps per block
+constexpr int QCAP = 4;    // live instances per chain (D14b)
+constexpr int MAXG = 192;  // segments per set
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr uint64_t NONE64 = ~0ull;
+constexpr uint64_t STEP_CAP = 50000000ull;  // safety valve: a set exceeding it reports digest ~0
+
+enum { EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_ENQUEUE, EV_ACC_START,
+       EV_ACC_PREEMPT, EV_ACC_RESUME, EV_ACC_DONE, EV_CB_DONE, EV_CHAIN_DONE };
+enum { P_NONE = 0, P_CPU, P_EPS_SPIN, P_EPS_SUSP, P_WAIT };
+enum { U_IDLE = 0, U_RUN, U_SWOUT, U_SWIN };
+enum { I_FREE = 0, I_READY, I_RUN, I_TRANSIT };
+
+struct Inst {
+  uint64_t release, ready_at;
+  uint32_t k, seq, rem;  // rem: remaining accelerator work of a preempted request
+  uint8_t cb, state, waiting, started, unit, pad[3];
+};
+
+struct DesSmem {
+  // static (per set)
+  uint32_t cT[MAXC], cD[MAXC];
+  uint64_t cPhase[MAXC];
+  uint8_t cCls[MAXC], cLocal[MAXC], cCb0[MAXC], cNcb[MAXC];
+  uint8_t bExec[MAXCB], bNseg[MAXCB];
+  uint8_t bSeg0[MAXCB];
+  uint32_t gW[MAXG];
+  uint8_t gKind[MAXG], gUnit[MAXG], gBkt[MAXG];
+  uint32_t xSameCore[MAXX];
+  uint8_t xWait[MAXX];
+  uint32_t uEps[MAXU], uKap[MAXU], uN[MAXU];
+  // dynamic
+  Inst inst[MAXC][QCAP];
+  uint32_t exRem[MAXX];
+  uint64_t exTimer[MAXX];
+  uint8_t exChain[MAXX], exSlot[MAXX], exSeg[MAXX], exPhase[MAXX];
+  uint64_t unEnd[MAXU];
+  uint32_t unRem[MAXU];
+  uint8_t unState[MAXU], unChain[MAXU], unSlot[MAXU];
+  unsigned long long maxResp[MAXC];
+  uint32_t cnt[MAXC];
+};
+
+__device__ __forceinline__ uint64_t fnv_record(uint64_t t, uint32_t kind, uint32_t chain, uint32_t cb, uint32_t seg,
+                                               uint32_t unit, uint32_t bk) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  const uint32_t w[8] = {(uint32_t)t, (uint32_t)(t >> 32), kind, chain, cb, seg, unit, bk};
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      h ^= (w[i] >> (8 * b)) & 0xffu;
+      h *= 0x100000001b3ull;
+    }
+  return h;
 }
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+  const uint32_t hi = __reduce_min_sync(FULL, (uint32_t)(v >> 32));
+  const uint32_t lo = __reduce_min_sync(FULL, (uint32_t)(v >> 32) == hi ? (uint32_t)v : 0xffffffffu);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+struct Ctx {
+  DesSmem& S;
+  uint64_t t, horizon, comm;
+  uint64_t dig;  // this lane's partial digest
+  __device__ void ev(uint32_t kind, uint32_t c, uint32_t cb, uint32_t seg, uint32_t unit, uint32_t bk) {
+    dig += fnv_record(t, kind, S.cLocal[c], cb, seg, unit, bk);
+  }
+  // executor x starts segment exSeg[x] of its job's callback
+  __device__ void begin_segment(uint32_t x) {
+    const uint32_t c = S.exChain[x], sl = S.exSlot[x];
+    const uint32_t j = S.cCb0[c] + S.inst[c][sl].cb;
+    const uint32_t g = S.bSeg0[j] + S.exSeg[x];
+    if (S.gKind[g] == 0) {
+      S.exPhase[x] = P_CPU;
+      S.exRem[x] = S.gW[g];
+    } else {
+      const uint32_t eps = S.uEps[S.gUnit[g]];
+      if (S.xWait[x]) { S.exPhase[x] = P_EPS_SPIN; S.exRem[x] = eps; }
+      else { S.exPhase[x] = P_EPS_SUSP; S.exTimer[x] = t + eps; }
+    }
+  }
+  // executor x finished the current segment (D12, D13, D16)
+  __device__ void advance_segment(uint32_t x) {
+    const uint32_t c = S.exChain[x], sl = S.exSlot[x];
+    Inst& I = S.inst[c][sl];
+    const uint32_t j = S.cCb0[c] + I.cb;
+    ev(EV_SEG_DONE, c, I.cb, S.exSeg[x], FULL, FULL);
+    S.exSeg[x]++;
+    if (S.exSeg[x] < S.bNseg[j]) { begin_segment(x); return; }
+    ev(EV_CB_DONE, c, I.cb, FULL, FULL, FULL);
+    if (I.cb + 1u < S.cNcb[c]) {
+      const uint32_t nx = S.bExec[j + 1];
+      I.cb++;
+      if (nx == x) I.state = I_READY;
+      else { I.state = I_TRANSIT; I.ready_at = t + comm; }
+    } else {
+      const uint64_t resp = t - I.release;
+      atomicMax(&S.maxResp[c], (unsigned long long)resp);
+      atomicAdd(&S.cnt[c], 1u);
+      ev(EV_CHAIN_DONE, c, FULL, FULL, FULL, FULL);
+      I.state = I_FREE;
+    }
+    S.exPhase[x] = P_NONE;
+    S.exChain[x] = 0xff;
+  }
+};
+
+__global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
+                                                           uint64_t horizon, uint64_t seed, uint64_t first_index,
+                                                           uint64_t* __restrict__ out_resp, uint64_t* __restrict__ out_count,
+                                                           uint64_t* __restrict__ out_digest,
+                                                           const uint64_t* __restrict__ bound,
+                                                           int64_t* __restrict__ out_viol) {
+  __shared__ DesSmem smem[SW];
+  const uint32_t lane = threadIdx.x & 31;
+  DesSmem& S = smem[threadIdx.x >> 5];
+  const uint32_t nwarps = gridDim.x * SW;
+  for (uint32_t set = blockIdx.x * SW + (threadIdx.x >> 5); set < n; set += nwarps) {
+    const Record& rec = recs[set];
+    const uint32_t c0 = b.set_chain_off[set], c1 = b.set_chain_off[set + 1];
+    const uint32_t nch = c1 - c0;
+    if (rec.status != PAAM_SET_OK) {
+      for (uint32_t i = lane; i < nch; i += 32) {
+        if (out_resp) out_resp[c0 + i] = 0;
+        if (out_count) out_count[c0 + i] = 0;
+      }
+      if (lane == 0 && out_digest) out_digest[set] = 0;
+      continue;
+    }
+    const uint32_t x0 = b.set_exec_off[set], nex = b.set_exec_off[set + 1] - x0;
+    const uint32_t a0 = b.set_accel_off[set], nac = b.set_accel_off[set + 1] - a0;
+    const uint32_t cb0 = b.chain_cb_off[c0], ncb = b.chain_cb_off[c1] - cb0;
+    const uint32_t sg0 = b.cb_seg_off[cb0], nseg = b.cb_seg_off[cb0 + ncb] - sg0;
+
+    // ---- static staging ----------------------------------------------------------------------------
+    // chains: rank = number of higher priorities
+    uint32_t my_prio = lane < nch ? b.chain_prio[c0 + lane] : 0u, rank = 0;
+    for (uint32_t d = 0; d < nch; d++) rank += (__shfl_sync(FULL, my_prio, d) > my_prio);
+    uint32_t chain_of_rank_cb0 = 0;
+    if (lane < nch) {
+      const uint64_t T = b.chain_T[c0 + lane];
+      S.cT[rank] = (uint32_t)T;
+      S.cD[rank] = (uint32_t)b.chain_D[c0 + lane];
+      S.cCls[rank] = b.chain_class[c0 + lane];
+      S.cLocal[rank] = (uint8_t)lane;
+      chain_of_rank_cb0 = b.chain_cb_off[c0 + lane] - cb0;
+      S.cCb0[rank] = (uint8_t)chain_of_rank_cb0;
+      S.cNcb[rank] = (uint8_t)(b.chain_cb_off[c0 + lane + 1] - cb0 - chain_of_rank_cb0);
+      S.cPhase[rank] = pg_phase(seed, first_index + set, lane, T);  // D2
+    }
+    // executors: canonical order (core asc, process priority desc)
+    uint32_t xcore = lane < nex ? b.exec_core[x0 + lane] : 0x100u + lane;
+    uint32_t xprio = lane < nex ? b.exec_prio[x0 + lane] : 0u;
+    uint32_t xpos = 0;
+    for (uint32_t y = 0; y < nex; y++) {
+      const uint32_t cy = __shfl_sync(FULL, xcore, y), py = __shfl_sync(FULL, xprio, y);
+      xpos += (cy < xcore) || (cy == xcore && py > xprio);
+    }
+    __shared__ uint8_t xcanon_all[SW][MAXX];
+    uint8_t* xcanon = xcanon_all[threadIdx.x >> 5];
+    if (lane < nex) {
+      xcanon[lane] = (uint8_t)xpos;
+      S.xWait[xpos] = b.exec_wait[x0 + lane];
+    }
+    {
+      const uint32_t same = __match_any_sync(FULL, xcore);
+      // translate the same-core lane mask to canonical positions
+      uint32_t m = 0;
+      for (uint32_t y = 0; y < nex; y++) {
+        const uint32_t py = __shfl_sync(FULL, xpos, y);  // every lane shuffles (no divergent shuffle)
+        if ((same >> y) & 1u) m |= 1u << py;
+      }
+      if (lane < nex) S.xSameCore[xpos] = m;
+    }
+    __syncwarp();
+    // accelerators / units
+    __shared__ uint32_t ubase_all[SW][4];
+    uint32_t* ubase = ubase_all[threadIdx.x >> 5];
+    if (lane == 0) {
+      uint32_t u = 0;
+      for (uint32_t a = 0; a < nac; a++) {
+        ubase[a] = u;
+        const uint32_t nb = b.accel_buckets[a0 + a], nu = b.accel_units[a0 + a];
+        const uint32_t e = (uint32_t)b.accel_eps[a0 + a];
+        const uint32_t k = nb > 1 ? (uint32_t)b.accel_kappa[a0 + a] : 0u;  // A6
+        for (uint32_t v = 0; v < nu; v++, u++) { S.uEps[u] = e; S.uKap[u] = k; S.uN[u] = nb; }
+      }
+    }
+    __syncwarp();
+    const uint32_t n_unit = rec.n_unit;
+    // callbacks and segments
+    for (uint32_t j = lane; j < ncb; j += 32) {
+      const uint32_t so = b.cb_seg_off[cb0 + j] - sg0;
+      S.bExec[j] = xcanon[b.cb_exec[cb0 + j]];
+      S.bSeg0[j] = (uint8_t)so;
+      S.bNseg[j] = (uint8_t)(b.cb_seg_off[cb0 + j + 1] - sg0 - so);
+    }
+    for (uint32_t g = lane; g < nseg; g += 32) {
+      const uint32_t kind = b.seg_kind[sg0 + g];
+      S.gKind[g] = (uint8_t)kind;
+      S.gW[g] = (uint32_t)b.seg_wcet[sg0 + g];
+      S.gUnit[g] = kind == 1 ? (uint8_t)(ubase[b.seg_accel[sg0 + g]] + b.seg_unit[sg0 + g]) : (uint8_t)0;
+    }
+    __syncwarp();
+    // buckets (A5): per accelerator, chains using it ranked by priority, groups of ceil(m_a/n)
+    {
+      uint32_t use = 0;  // lane = rank
+      if (lane < nch) {
+        for (uint32_t j = S.cCb0[lane]; j < S.cCb0[lane] + S.cNcb[lane]; j++)
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1) {
+              uint32_t a = 0;
+              for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= S.gUnit[g]) a = q;
+              use |= 1u << a;
+            }
+      }
+      const uint32_t lt = lanemask_lt();
+      uint32_t bk[4] = {0, 0, 0, 0};
+      for (uint32_t a = 0; a < nac; a++) {
+        const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
+        const uint32_t ma = __popc(U), nb = b.accel_buckets[a0 + a];
+        const uint32_t gsz = ma ? (ma + nb - 1) / nb : 1u;
+        bk[a] = nb - 1 - __popc(U & lt) / gsz;
+      }
+      if (lane < nch)
+        for (uint32_t j = S.cCb0[lane]; j < S.cCb0[lane] + S.cNcb[lane]; j++)
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1) {
+              uint32_t a = 0;
+              for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= S.gUnit[g]) a = q;
+              S.gBkt[g] = (uint8_t)bk[a];
+            }
+    }
+    // dynamic state
+    if (lane < MAXC) {
+      for (int q = 0; q < QCAP; q++) { S.inst[lane][q].state = I_FREE; S.inst[lane][q].waiting = 0; }
+      S.maxResp[lane] = 0;
+      S.cnt[lane] = 0;
+      S.exPhase[lane] = P_NONE;
+      S.exChain[lane] = 0xff;
+    }
+    if (lane < MAXU) S.unState[lane] = U_IDLE;
+    __syncwarp();
+
+    Ctx C{S, 0, horizon, b.comm_cost, 0};
+    uint32_t next_k = 0;  // lane = rank
+    uint32_t seq = 0;     // warp-uniform
+    bool on_core = false; // lane = canonical executor
+    uint32_t drops = 0, ovf = 0;
+    uint64_t steps = 0;
+    bool aborted = false;
+    const bool is_chain = lane < nch, is_exec = lane < nex, is_unit = lane < n_unit;
+
+    for (;;) {
+      // ===================== settle time t (D15) =====================
+      for (;;) {
+        bool anyA = false;
+        for (;;) {
+          bool ch = false;
+          // (1) units
+          if (is_unit) {
+            const uint32_t u = lane;
+            if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
+              if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
+              else { S.unState[u] = U_RUN; S.unRem[u] = S.inst[S.unChain[u]][S.unSlot[u]].rem; }
+              ch = true;
+            }
+            if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
+              const uint32_t c = S.unChain[u], sl = S.unSlot[u];
+              Inst& I = S.inst[c][sl];
+              const uint32_t j = S.cCb0[c] + I.cb;
+              uint32_t x = S.bExec[j];
+              // the request's segment: the executor's current segment
+              const uint32_t g = S.bSeg0[j] + S.exSeg[x];
+              C.ev(EV_ACC_DONE, c, I.cb, S.exSeg[x], u, S.gBkt[g]);
+              I.waiting = 0;
+              S.unState[u] = U_IDLE;
+              C.advance_segment(x);
+              ch = true;
+            }
+          }
+          __syncwarp();
+          // (2) executors: CPU / eps completions; enqueues sequenced by (chain, instance) (D7)
+          bool enq = false;
+          uint32_t enq_key = 0xffffffffu;
+          if (is_exec) {
+            const uint32_t x = lane, ph = S.exPhase[x];
+            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); ch = true; }
+            else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
+              S.exPhase[x] = P_WAIT;
+              enq = true;
+              enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.inst[S.exChain[x]][S.exSlot[x]].k & 0xffffffu);
+              ch = true;
+            }
+          }
+          const uint32_t enq_mask = __ballot_sync(FULL, enq);
+          if (enq_mask) {
+            uint32_t pos = 0;
+            uint32_t mm = enq_mask;
+            while (mm) {
+              const uint32_t y = __ffs(mm) - 1;
+              mm &= mm - 1;
+              pos += (__shfl_sync(FULL, enq_key, y) < enq_key);
+            }
+            if (enq) {
+              const uint32_t x = lane, c = S.exChain[x], sl = S.exSlot[x];
+              Inst& I = S.inst[c][sl];
+              const uint32_t g = S.bSeg0[S.cCb0[c] + I.cb] + S.exSeg[x];
+              I.seq = seq + pos;
+              I.waiting = 1;
+              I.started = 0;
+              I.unit = S.gUnit[g];
+              C.ev(EV_REQ_ENQUEUE, c, I.cb, S.exSeg[x], S.gUnit[g], S.gBkt[g]);
+            }
+            seq += __popc(enq_mask);
+          }
+          __syncwarp();
+          // (3) comm arrivals, (4) releases (D2, D14)
+          if (is_chain) {
+            const uint32_t c = lane;
+            for (int q = 0; q < QCAP; q++) {
+              Inst& I = S.inst[c][q];
+              if (I.state == I_TRANSIT && I.ready_at == C.t) { I.state = I_READY; ch = true; }
+            }
+            const uint64_t r = S.cPhase[c] + (uint64_t)next_k * S.cT[c];
+            if (r == C.t && r < horizon) {
+              if (S.cCls[c] == 1)
+                for (int q = 0; q < QCAP; q++) {
+                  Inst& I = S.inst[c][q];
+                  if (I.state == I_READY && I.cb == 0) {
+                    I.state = I_FREE;
+                    drops++;
+                    C.ev(EV_DROP, c, FULL, FULL, FULL, FULL);
+                  }
+                }
+              int slot = -1;
+              for (int q = QCAP - 1; q >= 0; q--) if (S.inst[c][q].state == I_FREE) slot = q;
+              if (slot < 0) {
+                ovf++;
+                C.ev(EV_OVERFLOW, c, FULL, FULL, FULL, FULL);
+              } else {
+                Inst& I = S.inst[c][slot];
+                I.state = I_READY; I.release = C.t; I.k = next_k; I.cb = 0; I.waiting = 0;
+                C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
+              }
+              next_k++;
+              ch = true;
+            }
+          }
+          __syncwarp();
+          if (!__any_sync(FULL, ch)) break;
+          anyA = true;
+        }
+        // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
+        bool chB = false;
+        uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
+        if (is_chain)
+          for (int q = 0; q < QCAP; q++) {
+            const Inst& I = S.inst[lane][q];
+            if (I.state == I_READY) ready_x |= 1u << S.bExec[S.cCb0[lane] + I.cb];
+          }
+        const uint32_t has_ready = __reduce_or_sync(FULL, ready_x);
+        const uint32_t want = __ballot_sync(FULL, is_exec && on_core && S.exPhase[lane] == P_NONE && ((has_ready >> lane) & 1u));
+        uint32_t wm = want;
+        while (wm) {
+          const uint32_t x = __ffs(wm) - 1;
+          wm &= wm - 1;
+          const uint32_t cand = __ballot_sync(FULL, (ready_x >> x) & 1u);
+          const uint32_t c = __ffs(cand) - 1;
+          if (lane == c) {
+            int best = -1;
+            for (int q = 0; q < QCAP; q++) {
+              const Inst& I = S.inst[c][q];
+              if (I.state != I_READY || S.bExec[S.cCb0[c] + I.cb] != x) continue;
+              if (best < 0) { best = q; continue; }
+              const Inst& B = S.inst[c][best];
+              if (I.release < B.release || (I.release == B.release && I.cb < B.cb)) best = q;
+            }
+            Inst& I = S.inst[c][best];
+            I.state = I_RUN;
+            S.exChain[x] = (uint8_t)c;
+            S.exSlot[x] = (uint8_t)best;
+            S.exSeg[x] = 0;
+            C.ev(EV_CB_START, c, I.cb, 0, FULL, FULL);
+            C.begin_segment(x);
+            // this chain no longer offers that instance
+            ready_x = 0;
+            for (int q = 0; q < QCAP; q++) {
+              const Inst& J = S.inst[c][q];
+              if (J.state == I_READY) ready_x |= 1u << S.bExec[S.cCb0[c] + J.cb];
+            }
+          }
+          __syncwarp();
+          chB = true;
+        }
+        // (6) core dispatch (D5): highest process priority runnable executor per core
+        {
+          ready_x = 0;
+          if (is_chain)
+            for (int q = 0; q < QCAP; q++) {
+              const Inst& I = S.inst[lane][q];
+              if (I.state == I_READY) ready_x |= 1u << S.bExec[S.cCb0[lane] + I.cb];
+            }
+          const uint32_t hr = __reduce_or_sync(FULL, ready_x);
+          bool run = false;
+          if (is_exec) {
+            const uint32_t ph = S.exPhase[lane];
+            run = ph == P_NONE ? ((hr >> lane) & 1u) : (ph == P_CPU || ph == P_EPS_SPIN) ? true
+                : ph == P_WAIT ? (S.xWait[lane] != 0) : false;
+          }
+          const uint32_t R = __ballot_sync(FULL, run);
+          const uint32_t cand = is_exec ? (R & S.xSameCore[lane]) : 0u;
+          const bool oc = cand && (__ffs(cand) - 1 == lane);
+          if (__any_sync(FULL, oc != on_core)) chB = true;
+          on_core = oc;
+        }
+        // (7) unit dispatch (D8-D11)
+        for (uint32_t u = 0; u < n_unit; u++) {
+          const uint32_t ust = S.unState[u];
+          if (ust != U_IDLE && !(ust == U_RUN && S.uN[u] > 1)) continue;
+          // best waiting request on u, excluding the running one: key = bucket | started | priority
+          uint32_t key = 0;
+          int bslot = -1;
+          if (is_chain) {
+            for (int q = 0; q < QCAP; q++) {
+              const Inst& I = S.inst[lane][q];
+              if (!I.waiting || I.unit != u) continue;
+              if (ust == U_RUN && S.unChain[u] == lane && S.unSlot[u] == q) continue;
+              if (bslot < 0) { bslot = q; continue; }
+              const Inst& B = S.inst[lane][bslot];
+              if (I.started != B.started) { if (I.started) bslot = q; }
+              else if (I.seq < B.seq) bslot = q;
+            }
+            if (bslot >= 0) {
+              const Inst& I = S.inst[lane][bslot];
+              const uint32_t g = S.bSeg0[S.cCb0[lane] + I.cb];  // bucket is per (chain, accelerator)
+              uint32_t bkt = 0;
+              for (uint32_t gg = g; gg < g + S.bNseg[S.cCb0[lane] + I.cb]; gg++)
+                if (S.gKind[gg] == 1 && S.gUnit[gg] == u) bkt = S.gBkt[gg];
+              key = 1u + ((bkt << 6) | ((uint32_t)I.started << 5) | (31u - lane));
+            }
+          }
+          const uint32_t best = __reduce_max_sync(FULL, key);
+          if (best == 0) continue;
+          const uint32_t wc = 31u - ((best - 1u) & 31u);
+          const uint32_t wbkt = (best - 1u) >> 6;
+          if (lane == wc) {
+            Inst& I = S.inst[wc][bslot];
+            const uint32_t j = S.cCb0[wc] + I.cb;
+            const uint32_t x = S.bExec[j];
+            const uint32_t seg = S.exSeg[x];
+            if (ust == U_IDLE) {
+              S.unChain[u] = (uint8_t)wc;
+              S.unSlot[u] = (uint8_t)bslot;
+              if (I.started) {  // D10: switch back in
+                S.unState[u] = U_SWIN;
+                S.unEnd[u] = C.t + S.uKap[u];
+                C.ev(EV_ACC_RESUME, wc, I.cb, seg, u, wbkt);
+              } else {
+                I.started = 1;
+                S.unState[u] = U_RUN;
+                S.unRem[u] = S.gW[S.bSeg0[j] + seg];
+                C.ev(EV_ACC_START, wc, I.cb, seg, u, wbkt);
+              }
+            }
+          }
+          if (ust == U_RUN) {  // D9: preempt a lower bucket
+            const uint32_t rc = S.unChain[u];
+            Inst& R = S.inst[rc][S.unSlot[u]];
+            const uint32_t rj = S.cCb0[rc] + R.cb, rx = S.bExec[rj], rseg = S.exSeg[rx];
+            const uint32_t rbkt = S.gBkt[S.bSeg0[rj] + rseg];
+            if (wbkt > rbkt) {
+              if (lane == 0) {
+                C.ev(EV_ACC_PREEMPT, rc, R.cb, rseg, u, rbkt);
+                R.rem = S.unRem[u];
+                S.unState[u] = U_SWOUT;
+                S.unEnd[u] = C.t + S.uKap[u];
+              }
+              chB = true;
+            }
+          } else {
+            chB = true;
+          }
+          __syncwarp();
+        }
+        if (!anyA && !__any_sync(FULL, chB)) break;
+      }
+      // ===================== advance time =====================
+      uint64_t nt = NONE64;
+      if (is_chain) {
+        const uint64_t r = S.cPhase[lane] + (uint64_t)next_k * S.cT[lane];
+        if (r < horizon) nt = r;
+        for (int q = 0; q < QCAP; q++)
+          if (S.inst[lane][q].state == I_TRANSIT) nt = min(nt, S.inst[lane][q].ready_at);
+      }
+      if (is_exec) {
+        const uint32_t ph = S.exPhase[lane];
+        if ((ph == P_CPU || ph == P_EPS_SPIN) && on_core) nt = min(nt, C.t + S.exRem[lane]);
+        if (ph == P_EPS_SUSP) nt = min(nt, S.exTimer[lane]);
+      }
+      if (is_unit) {
+        if (S.unState[lane] == U_RUN) nt = min(nt, C.t + S.unRem[lane]);
+        if (S.unState[lane] == U_SWOUT || S.unState[lane] == U_SWIN) nt = min(nt, S.unEnd[lane]);
+      }
+      nt = warp_min_u64(nt);
+      if (nt == NONE64) break;
+      if (++steps > STEP_CAP) { aborted = true; break; }
+      const uint32_t dt = (uint32_t)min(nt - C.t, (uint64_t)0xffffffffu);
+      if (is_exec && on_core && (S.exPhase[lane] == P_CPU || S.exPhase[lane] == P_EPS_SPIN)) S.exRem[lane] -= dt;
+      if (is_unit && S.unState[lane] == U_RUN) S.unRem[lane] -= dt;
+      C.t = nt;
+      __syncwarp();
+    }
+
+    // ---- outputs ---------------------------------------------------------------------------------------
+    const uint64_t digest = warp_sum_u64(C.dig);
+    bool viol = false, set_sched = bound != nullptr;
+    if (is_chain) {
+      const uint32_t local = S.cLocal[lane];
+      if (out_resp) out_resp[c0 + local] = S.maxResp[lane];
+      if (out_count) out_count[c0 + local] = S.cnt[lane];
+      if (bound) {
+        const uint64_t bd = bound[c0 + local];
+        if (S.cCls[lane] == 0 && (bd == PAAM_UNSCHED || bd > S.cD[lane])) set_sched = false;
+        viol = S.cCls[lane] == 0 && S.maxResp[lane] > bd;
+      }
+    }
+    set_sched = __all_sync(FULL, set_sched || !is_chain);
+    const uint32_t nv = __popc(__ballot_sync(FULL, viol && set_sched));
+    if (lane == 0) {
+      if (out_digest) out_digest[set] = aborted ? ~0ull : digest;
+      if (out_viol && nv) atomicAdd((unsigned long long*)out_viol, (unsigned long long)nv);
+    }
+    (void)drops; (void)ovf;
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+#ifndef PAAM_WARP_EMU
+int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
+                    uint64_t first_index, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
+                    const uint64_t* bound, int64_t* out_viol, cudaStream_t st) {
+  if (n == 0) return PAAM_OK;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simulate_kernel, SW * 32, 0);
+  if (per_sm < 1) per_sm = 1;
+  const uint32_t need = (n + SW - 1) / SW;
+  const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
+  const uint32_t grid = need < cap ? need : cap;
+  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, out_resp, out_count, out_digest,
+                                           bound, out_viol);
+  count_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "simulate_kernel launch");
+}
+
+#endif  // PAAM_WARP_EMU
+
+}  // namespace paam

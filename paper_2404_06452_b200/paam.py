@@ -79,7 +79,8 @@ def lib():
         L.paam_pack.argtypes = [ctypes.POINTER(PaamBatch), ctypes.POINTER(_vp), _vp, _vp]
         L.paam_repack.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp]
         L.paam_analyze.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp]
-        L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _vp, _vp, _vp, _vp, _vp]
+        L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                    _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_sets_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_uint32)]
         L.paam_free.argtypes = [_vp]
@@ -241,11 +242,12 @@ class Sets:
         check(lib().paam_analyze(self.h, self.n_sets if n is None else n, ptr(out_wcrt), ptr(out_sched),
                                  ptr(out_bins), _stream_ptr(stream)), "paam_analyze")
 
-    def simulate(self, horizon, seed, out_resp, out_digest=None, bound=None, out_violations=None, n=None, stream=None):
+    def simulate(self, horizon, seed, out_resp, out_count=None, out_digest=None, bound=None, out_violations=None,
+                 first_index=0, n=None, stream=None):
         ptr = lambda t: None if t is None else t.data_ptr()
-        check(lib().paam_simulate(self.h, self.n_sets if n is None else n, horizon, seed, ptr(out_resp),
-                                  ptr(out_digest), ptr(bound), ptr(out_violations), _stream_ptr(stream)),
-              "paam_simulate")
+        check(lib().paam_simulate(self.h, self.n_sets if n is None else n, horizon, seed, first_index, ptr(out_resp),
+                                  ptr(out_count), ptr(out_digest), ptr(bound), ptr(out_violations),
+                                  _stream_ptr(stream)), "paam_simulate")
 
     def free(self):
         if self.h:

@@ -7,7 +7,7 @@ sets pins the oracle's time-advance, timers, preemption and tie-breaking code.
 """
 import math
 
-QCAP = 8
+QCAP = 4
 
 
 def buckets_of(s):

@@ -1,7 +1,7 @@
 # quick GPU check: parity tests + smoke + short bench
 set -o pipefail
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest=$?"
+timeout 1200 python -m pytest tests -m gpu -x -q --timeout=400 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest=$?"
 tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke=$?"
 timeout 600 python bench.py --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench=$?"

@@ -1,0 +1,83 @@
+"""Run the product kernels under the host warp emulator (libpaam_emu.so) and compare with the oracle.
+DEBUGGING AID: python tools/warp_emu/check.py [analyze|des] ..."""
+import ctypes
+import os
+import random
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from gen.inputs import MS, config2_params, config3_params, flatten, generate_host, make_params  # noqa
+from oracle import oracle as O  # noqa
+from paper_2404_06452_b200.paam import Batch  # noqa  (only for the batch struct marshalling)
+
+L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaam_emu.so"))
+vp = ctypes.c_void_p
+L.emu_pack.argtypes = [vp, vp, vp]
+L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
+L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, vp, vp, vp, vp, vp]
+L.emu_record_bytes.restype = ctypes.c_uint32
+
+
+def emu_run(batch, horizon=None, seed=0, first=0):
+    hb = Batch.from_host(batch)
+    n = hb.n_sets
+    rec = np.zeros((max(n, 1), L.emu_record_bytes()), np.uint8)
+    st = np.zeros(max(n, 1), np.int32)
+    L.emu_pack(ctypes.addressof(hb.c), rec.ctypes.data, st.ctypes.data)
+    nch = max(hb.c.n_chains, 1)
+    w = np.zeros(nch, np.uint64)
+    sc = np.zeros(max(n, 1), np.uint8)
+    bins = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
+    L.emu_analyze(rec.ctypes.data, n, hb.c.comm_cost, hb.c.flags, hb.c.n_bins if hb.c.set_bin else 0,
+                  w.ctypes.data, sc.ctypes.data, bins.ctypes.data if hb.c.set_bin else None)
+    out = dict(status=st[:n], wcrt=w[:hb.c.n_chains], sched=sc[:n], bins=bins[:2 * hb.c.n_bins])
+    if horizon is not None:
+        resp = np.zeros(nch, np.uint64)
+        cnt = np.zeros(nch, np.uint64)
+        dig = np.zeros(max(n, 1), np.uint64)
+        viol = np.zeros(1, np.int64)
+        L.emu_simulate(ctypes.addressof(hb.c), rec.ctypes.data, n, horizon, seed, first, resp.ctypes.data,
+                       cnt.ctypes.data, dig.ctypes.data, w.ctypes.data, viol.ctypes.data)
+        out.update(resp=resp[:hb.c.n_chains], count=cnt[:hb.c.n_chains], digest=dig[:n], violations=int(viol[0]))
+    return out
+
+
+def compare(batch, horizon=None, seed=0, first=0, label=""):
+    e = emu_run(batch, horizon, seed, first)
+    ow, osch, ost, ob = O.analyze(batch)
+    ok = np.array_equal(ost, e["status"]) and np.array_equal(ow, e["wcrt"]) and np.array_equal(osch, e["sched"])
+    msg = [f"{label}: analyze {'OK' if ok else 'MISMATCH'}"]
+    if not ok:
+        bad = np.nonzero(ow != e["wcrt"])[0][:5]
+        msg.append(f"  status o={ost[:8]} e={e['status'][:8]} wcrt bad idx {bad} o={ow[bad]} e={e['wcrt'][bad]}")
+    if horizon is not None:
+        o = O.simulate(batch, horizon, seed=seed, first_index=first, bound=e["wcrt"], nthreads=8)
+        ok2 = (np.array_equal(o["resp"], e["resp"]) and np.array_equal(o["count"], e["count"])
+               and np.array_equal(o["digest"], e["digest"]) and o["violations"] == e["violations"])
+        msg.append(f"  des {'OK' if ok2 else 'MISMATCH'}")
+        if not ok2:
+            msg.append(f"  resp o={o['resp'][:8]} e={e['resp'][:8]}\n  count o={o['count'][:8]} e={e['count'][:8]}"
+                       f"\n  dig o={o['digest'][:4]} e={e['digest'][:4]} viol o={o['violations']} e={e['violations']}")
+        ok = ok and ok2
+    print("\n".join(msg), flush=True)
+    return ok
+
+
+if __name__ == "__main__":
+    from tests.ref_scan import random_small_system
+    import tests.test_oracle_pins as P
+    what = sys.argv[1] if len(sys.argv) > 1 else "des"
+    systems = {"two": P.two_chain_accel_system(kappa=100_000, buckets=2), "appb": P.app_b_two_chains(),
+               "a10": P.a10_system(), "cs3": P.cs3_system(6), "cs3n1": P.cs3_system(1)}
+    for nm, s in systems.items():
+        compare(flatten([s], comm_cost=0), horizon=500 * MS if what == "des" else None, seed=1, label=nm)
+    rng = random.Random(1)
+    for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 20):
+        s = random_small_system(rng, max_chains=5, tmax=50)
+        if not compare(flatten([s], comm_cost=1), horizon=300 if what == "des" else None, seed=i % 3, label=f"rand{i}"):
+            print(s)
+            break
