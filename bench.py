@@ -278,6 +278,30 @@ def run_ours(args):
                "ms_per_step": 1e3 * e2e_s / args.steps}
         hsets.free()
 
+    # ---- config 5 leg: the paired DES (paam_simulate) with the sim <= bound census -------------------
+    des = None
+    if args.des_sets > 0:
+        nd = min(args.des_sets, n)
+        resp = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
+        dig = torch.empty(n, dtype=torch.int64, device=dev)
+        viol = torch.zeros(1, dtype=torch.int64, device=dev)
+        hz = int(args.des_horizon_s * 1e9)
+        sets.simulate(hz, 3, resp, None, dig, None, None, first_index=first, n=min(nd, 1024), stream=stream)  # warm-up
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = paam.kernel_launches()
+        e0.record(stream)
+        sets.simulate(hz, 3, resp, None, dig, wcrt, viol, first_index=first, n=nd, stream=stream)
+        e1.record(stream)
+        stream.synchronize()
+        des_ms = max_over_ranks(e0.elapsed_time(e1), world)
+        v = viol.clone()
+        if dist is not None:
+            dist.all_reduce(v)
+        des = {"metric": "chain-sets simulated/sec (PAAM DES, config-5 leg)", "value": world * nd / (des_ms / 1e3),
+               "unit": "chain-sets/s", "sets_per_gpu": nd, "horizon_s": args.des_horizon_s, "seed": 3,
+               "ms": des_ms, "sim_le_bound_violations": int(v.item()), "gpu_launches": paam.kernel_launches() - l0,
+               "scope": "violations counted in sets the analysis declares schedulable (every CRITICAL chain R* <= D)"}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -315,6 +339,8 @@ def run_ours(args):
            "bins": bins.cpu().tolist()}
     if e2e:
         out["e2e"] = e2e
+    if des:
+        out["des"] = des
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(gp, first, budget_s=args.cpu_budget)
     print(json.dumps(out), flush=True)
@@ -353,6 +379,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--des-sets", type=int, default=100_000, help="sets per GPU for the DES leg (0 = skip)")
+    ap.add_argument("--des-horizon-s", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 untimed warm-up steps
