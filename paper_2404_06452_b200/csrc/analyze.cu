@@ -30,24 +30,32 @@ struct __align__(16) WarpSmem {
   uint32_t S[MAXS];    // per-segment bound summed over the sub-chain
   uint32_t Bc[MAXS];   // blocking term in use (as written, or the sound variant)
   uint32_t R[MAXS];    // converged R_c (SAT = UNSCHED)
+  uint32_t Hs[MAXS];   // H*_c(R_c) of every solved sub-chain
+  unsigned long long sum[MAXC];  // end-to-end accumulation per chain
+  uint32_t uns[MAXC];
 };
 
-// Exact saturating warp sums of values <= SAT via the integer reduction unit (REDUX): the 16-bit halves
-// are summed separately (32 * 2^16 < 2^32, no wrap) and recombined in 64 bits.
-__device__ __forceinline__ uint32_t wsum(uint32_t v) {
-  const uint32_t lo = __reduce_add_sync(0xffffffffu, v & 0xffffu);
-  const uint32_t hi = __reduce_add_sync(0xffffffffu, v >> 16);
-  const uint64_t t = ((uint64_t)hi << 16) + lo;
-  return t > SAT ? SAT : (uint32_t)t;
+constexpr uint32_t FULL = 0xffffffffu;
+// 8-lane group reductions (xor within aligned groups of 8)
+__device__ __forceinline__ uint32_t gsum8(uint32_t v) {
+  v = sadd(v, __shfl_xor_sync(FULL, v, 4));
+  v = sadd(v, __shfl_xor_sync(FULL, v, 2));
+  return sadd(v, __shfl_xor_sync(FULL, v, 1));
 }
-__device__ __forceinline__ void wsum2(uint32_t& a, uint32_t& b) {
-  const uint32_t alo = __reduce_add_sync(0xffffffffu, a & 0xffffu);
-  const uint32_t blo = __reduce_add_sync(0xffffffffu, b & 0xffffu);
-  const uint32_t ahi = __reduce_add_sync(0xffffffffu, a >> 16);
-  const uint32_t bhi = __reduce_add_sync(0xffffffffu, b >> 16);
-  const uint64_t ta = ((uint64_t)ahi << 16) + alo, tb = ((uint64_t)bhi << 16) + blo;
-  a = ta > SAT ? SAT : (uint32_t)ta;
-  b = tb > SAT ? SAT : (uint32_t)tb;
+__device__ __forceinline__ void gsum8x2(uint32_t& a, uint32_t& b) {
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    const uint32_t xa = __shfl_xor_sync(FULL, a, o), xb = __shfl_xor_sync(FULL, b, o);
+    a = sadd(a, xa);
+    b = sadd(b, xb);
+  }
+}
+__device__ __forceinline__ bool gor8(bool p) {
+  uint32_t v = p;
+  v |= __shfl_xor_sync(FULL, v, 4);
+  v |= __shfl_xor_sync(FULL, v, 2);
+  v |= __shfl_xor_sync(FULL, v, 1);
+  return v != 0;
 }
 
 __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restrict__ recs, uint32_t n,
@@ -145,81 +153,131 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
       }
       __syncwarp();
 
-      // ---- step 4: Eq.5 per sub-chain, canonical order ----------------------------------------------
-      const bool is_chain = lane < nch;
-      const uint32_t Mk = is_chain ? r.cM[lane] : 1u;
-      const uint32_t Lk = is_chain ? (r.cMisc[lane] & 31u) : 0u;
+      // ---- step 4: Eq.5, one core at a time per 8-lane group, four cores in parallel -------------------
+      // Dependencies (hp, hpp) only point to earlier sub-chains of the same core (A7), and the canonical
+      // order groups sub-chains by core, so lane group g (lanes 8g..8g+7) walks core group g's
+      // sub-chains in order while the other groups walk theirs.  Within a group, lane l handles the
+      // Lemma-3 chains k = l, l+8, ... (< rank) and the hp/hpp sub-chains h = l, l+8, ...; the two
+      // interference sums are reduced over the group with three xor-shuffles each.
+      const uint32_t gi = lane >> 3, gl = lane & 7;
       const bool is_sub = lane < nsub;
-      const uint32_t hmisc = is_sub ? r.sMisc[lane] : 0u;
-      const uint32_t h_rank = hmisc & 31u;
-      const bool h_spin = (hmisc >> 16) & 1u;
-      const uint32_t h_E = is_sub ? r.sE[lane] : 0u, h_eps = is_sub ? r.sEps[lane] : 0u;
-      uint32_t h_R = 0, h_Hs = 0;  // this lane's sub-chain once solved
-      for (uint32_t c = 0; c < nsub; c++) {
-        const uint32_t cmisc = r.sMisc[c];
-        const uint32_t rk = cmisc & 0xffu, umask = (cmisc >> 8) & 0xffu;
-        const uint32_t in_hp = (r.sHp[c] >> lane) & 1u, in_hpp = (r.sHpp[c] >> lane) & 1u;
-        const bool dep_unsched = (in_hp || (in_hpp && h_spin)) && h_R == SAT;
-        uint32_t X = 0;
-        if (in_hp) X = sadd(h_E, h_Hs);
-        else if (in_hpp) X = sadd(h_E, h_spin ? h_Hs : h_eps);  // spin(Gamma_h)
-        uint32_t WU = 0;  // Lemma-3 weight of chain `lane` over the units of c (union of hps, A1)
-        if (lane < rk) {
-          uint32_t um = umask;
-          while (um) {
-            const uint32_t u = __ffs(um) - 1;
-            um &= um - 1;
-            WU = sadd(WU, r.W[lane][u]);
-          }
+      const uint32_t my_core = is_sub ? (r.sSeg[lane] >> 24) : 0x100u + lane;
+      const uint32_t prev_core = __shfl_up_sync(FULL, my_core, 1);
+      const uint32_t gstart = __ballot_sync(FULL, is_sub && (lane == 0 || my_core != prev_core));
+      const uint32_t ngroups = __popc(gstart);
+      const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
+      for (uint32_t gb = 0; gb < ngroups; gb += 4) {
+        const uint32_t grp = gb + gi;
+        uint32_t g0 = 0, glen = 0;
+        if (grp < ngroups) {
+          g0 = __fns(gstart, 0, grp + 1);
+          const uint32_t rest = gstart & ~((2u << g0) - 1u);
+          glen = (rest ? (uint32_t)__ffs(rest) - 1u : nsub) - g0;
         }
-        uint32_t Rc = SAT, Hsc = SAT;
-        if (!__any_sync(0xffffffffu, dep_unsched)) {  // A8: an unschedulable dependency poisons c
-          const uint32_t BE = sadd(w.Bc[c], r.sE[c]);
-          const uint32_t S = w.S[c], base3 = r.sBase3[c], eps = r.sEps[c], cut = r.cCut[rk];
-          // start: the first three terms B + E + H*(0), with mu(0) = 1
-          const uint32_t A0 = wsum(WU);
-          uint32_t R = sadd(BE, sadd(min(S, sadd(base3, A0)), eps));
-          uint32_t Hst = 0;
-          for (;;) {
-            if (R > cut) { R = SAT; break; }
-            const uint32_t mk = is_chain ? mu_magic(R, Mk, Lk) : 0u;
-            uint32_t a = smul(mk, WU);
-            const uint32_t mh = __shfl_sync(0xffffffffu, mk, h_rank);
-            uint32_t bsum = smul(mh, X);
-            wsum2(a, bsum);
-            Hst = sadd(min(S, sadd(base3, a)), eps);
-            const uint32_t F = sadd(sadd(BE, Hst), bsum);
-            if (F == R) break;
-            R = F;
+        const uint32_t maxlen = __reduce_max_sync(FULL, glen);
+        for (uint32_t pos = 0; pos < maxlen; pos++) {
+          const bool act = pos < glen;
+          const uint32_t c = act ? g0 + pos : 0u;
+          const uint32_t cmisc = act ? r.sMisc[c] : 0u;
+          const uint32_t rk = cmisc & 0xffu, umask = (cmisc >> 8) & 0xffu;
+          const uint32_t hpm = act ? r.sHp[c] : 0u, hppm = act ? r.sHpp[c] : 0u;
+          const uint32_t cpu_m = hpm | hppm, dep = hpm | (hppm & spin_mask);
+          const uint32_t hibit = cpu_m ? 32u - __clz(cpu_m) : 0u;
+          const uint32_t jmax = (__reduce_max_sync(FULL, max(rk, hibit)) + 7u) >> 3;
+          // per-lane interferers: Lemma-3 chains and hp/hpp sub-chains (A8 poison on dependencies)
+          uint32_t WU[4], XM[4], XL[4], KM[4], KL[4], X[4];
+          bool pois = false;
+#pragma unroll
+          for (uint32_t j = 0; j < 4; j++) {
+            WU[j] = 0; X[j] = 0; KM[j] = 1; KL[j] = 0; XM[j] = 1; XL[j] = 0;
+            if (j < jmax) {
+              const uint32_t k = gl + 8 * j;
+              if (k < rk) {
+                uint32_t um = umask, wu = 0;
+                while (um) {
+                  const uint32_t u = __ffs(um) - 1;
+                  um &= um - 1;
+                  wu = sadd(wu, r.W[k][u]);  // union of hps over the sub-chain's units (A1)
+                }
+                WU[j] = wu;
+                KM[j] = r.cM[k];
+                KL[j] = r.cMisc[k] & 31u;
+              }
+              if ((cpu_m >> k) & 1u) {
+                const uint32_t hE = r.sE[k], hHs = w.Hs[k];
+                const uint32_t hm = r.sMisc[k] & 0xffu;
+                X[j] = ((hpm >> k) & 1u) ? sadd(hE, hHs)
+                                         : sadd(hE, ((spin_mask >> k) & 1u) ? hHs : r.sEps[k]);  // spin() P:1132
+                XM[j] = r.cM[hm];
+                XL[j] = r.cMisc[hm] & 31u;
+                if ((dep >> k) & 1u) pois |= (w.R[k] == SAT);
+              }
+            }
           }
-          Rc = R;
-          Hsc = (R == SAT) ? SAT : Hst;
+          uint32_t wu_sum = 0;
+#pragma unroll
+          for (uint32_t j = 0; j < 4; j++) wu_sum = sadd(wu_sum, WU[j]);
+          pois = gor8(pois);
+          const uint32_t A0 = gsum8(wu_sum);  // mu(0) = 1: the paper's start B + E + H*(0)
+          const uint32_t BE = act ? sadd(w.Bc[c], r.sE[c]) : 0u;
+          const uint32_t S = act ? w.S[c] : 0u, base3 = act ? r.sBase3[c] : 0u, eps = act ? r.sEps[c] : 0u;
+          const uint32_t cut = act ? r.cCut[rk] : 0u;
+          uint32_t R = sadd(BE, sadd(min(S, sadd(base3, A0)), eps)), Hst = 0;
+          bool done = !act || pois;
+          if (pois) R = SAT;
+          while (__any_sync(FULL, !done)) {
+            if (!done && R > cut) { R = SAT; done = true; }
+            const uint32_t h2 = (R - 1u) << 1;
+            uint64_t aa = 0, bb = 0;
+            uint32_t hi = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 4; j++) {
+              if (j < jmax) {
+                const uint64_t pa = (uint64_t)((__umulhi(h2, KM[j]) >> KL[j]) + 2u) * WU[j];
+                const uint64_t pb = (uint64_t)((__umulhi(h2, XM[j]) >> XL[j]) + 2u) * X[j];
+                aa += pa;
+                bb += pb;
+                hi |= (uint32_t)(pa >> 32) | (uint32_t)(pb >> 32);
+              }
+            }
+            uint32_t a = (hi || aa > SAT) ? SAT : (uint32_t)aa;
+            uint32_t bs = (hi || bb > SAT) ? SAT : (uint32_t)bb;
+            gsum8x2(a, bs);
+            if (!done) {
+              Hst = sadd(min(S, sadd(base3, a)), eps);
+              const uint32_t F = sadd(sadd(BE, Hst), bs);
+              if (F == R) done = true;
+              else R = F;
+            }
+          }
+          if (act && gl == 0) {
+            w.R[c] = R;
+            w.Hs[c] = (R == SAT) ? SAT : Hst;
+          }
+          __syncwarp();
         }
-        if (lane == c) { h_R = Rc; h_Hs = Hsc; }
       }
-      if (is_sub) w.R[lane] = h_R;
       __syncwarp();
 
       // ---- step 5: end to end and verdict ---------------------------------------------------------
+      if (lane < nch) { w.sum[lane] = 0; w.uns[lane] = 0; }
+      __syncwarp();
+      if (is_sub) {
+        const uint32_t rk = r.sMisc[lane] & 0xffu, Rh = w.R[lane];
+        if (Rh == SAT) w.uns[rk] = 1;
+        else atomicAdd(&w.sum[rk], (unsigned long long)Rh);
+      }
+      __syncwarp();
       bool ok = true;
-      if (is_chain) {
-        uint64_t sum = 0;
-        uint32_t cnt = 0;
-        bool uns = false;
-        for (uint32_t h = 0; h < nsub; h++)
-          if ((r.sMisc[h] & 0xffu) == (uint32_t)lane) {
-            const uint32_t Rh = w.R[h];
-            uns |= (Rh == SAT);
-            sum += Rh;
-            cnt++;
-          }
-        const uint64_t Rstar = uns ? UNS : sum + comm * (uint64_t)(cnt - 1);
+      if (lane < nch) {
         const uint32_t cm = r.cMisc[lane];
+        const uint32_t nsc = cm >> 24;  // sub-chains of this chain
+        const uint64_t Rstar = w.uns[lane] ? UNS : w.sum[lane] + comm * (uint64_t)(nsc - 1);
         if (out_wcrt) out_wcrt[r.chain_base + ((cm >> 16) & 0xffu)] = Rstar;
         const bool critical = ((cm >> 8) & 0xffu) == 0;
         ok = !critical || (Rstar != UNS && Rstar <= (uint64_t)r.cD[lane]);
       }
-      sched = __all_sync(0xffffffffu, ok) ? 1u : 0u;
+      sched = __all_sync(FULL, ok) ? 1u : 0u;
     }
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
