@@ -168,6 +168,14 @@ int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* out_status, p
 int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcrt, uint8_t* out_sched,
                  int64_t* out_bins, paam_stream_t stream);
 
+/* paam_pack_analyze -- steps 2-6 in one call, pipelined: the batch is cut into chunks whose
+ * pack_kernel and analyze_kernel launches overlap on two internal streams (chunk i's analysis
+ * runs while chunk i+1 is packed), joined back into `stream`.  Same results as paam_repack followed
+ * by paam_analyze; `sets` must have capacity for batch->n_sets (from paam_pack).  Host batches are
+ * staged first (synchronising, as paam_repack). */
+int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
+                      uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream);
+
 /* paam_simulate -- §8(a) steps 7-8.  Discrete-event simulation of every set (DESIGN.md App. A,
  * rules D1-D17: PiCAS executors, fixed-priority cores, PAAM bucket queues with cross-bucket
  * preemption, eps per request, kappa per switch) over releases in [0, horizon), run until every

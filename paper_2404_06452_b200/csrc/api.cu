@@ -19,6 +19,8 @@ struct paam_sets {
   int32_t* dstatus;  // device status staging for host batches
   uint32_t dstatus_cap;
   paam_batch dev;    // the packed batch with device pointers (paam_simulate reads its structure)
+  cudaStream_t side[2];  // internal streams of paam_pack_analyze (created on first use)
+  cudaEvent_t ev[17];
 };
 
 namespace paam {
@@ -187,6 +189,63 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
                          bound, out_violations, (cudaStream_t)stream);
 }
 
+extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
+                                 uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream) {
+  int rc = check_batch(batch);
+  if (rc) return rc;
+  if (!sets) return fail(PAAM_EINVAL, "NULL handle");
+  if (batch->n_sets > sets->cap) return fail(PAAM_EINVAL, "paam_pack_analyze: handle capacity too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (batch->mem == PAAM_MEM_HOST || batch->n_sets < 4096) {  // small or host batch: sequential
+    rc = paam_repack(batch, sets, out_status, stream);
+    if (rc) return rc;
+    return paam_analyze(sets, batch->n_sets, out_wcrt, out_sched, out_bins, stream);
+  }
+  cudaError_t e;
+  if (!sets->side[0]) {
+    for (int i = 0; i < 2; i++)
+      if ((e = cudaStreamCreateWithFlags(&sets->side[i], cudaStreamNonBlocking)) != cudaSuccess)
+        return fail_cuda(e, "paam_pack_analyze: stream");
+    for (int i = 0; i < 17; i++)
+      if ((e = cudaEventCreateWithFlags(&sets->ev[i], cudaEventDisableTiming)) != cudaSuccess)
+        return fail_cuda(e, "paam_pack_analyze: event");
+  }
+  const int K = 8;  // chunks
+  const uint32_t n = batch->n_sets;
+  cudaEventRecord(sets->ev[16], st);
+  cudaStreamWaitEvent(sets->side[0], sets->ev[16], 0);
+  cudaStreamWaitEvent(sets->side[1], sets->ev[16], 0);
+  for (int i = 0; i < K; i++) {
+    const uint32_t lo = (uint32_t)((uint64_t)n * i / K), hi = (uint32_t)((uint64_t)n * (i + 1) / K);
+    paam_batch view = *batch;  // CSR offsets stay global: a chunk is a shifted window of set offsets
+    view.n_sets = hi - lo;
+    view.set_chain_off += lo;
+    view.set_exec_off += lo;
+    view.set_accel_off += lo;
+    if (view.set_bin) view.set_bin += lo;
+    rc = launch_pack(&view, sets->rec + lo, out_status ? out_status + lo : nullptr, sets->side[0]);
+    if (rc) return rc;
+    cudaEventRecord(sets->ev[i], sets->side[0]);
+    cudaStreamWaitEvent(sets->side[1], sets->ev[i], 0);
+    rc = launch_analyze(sets->rec + lo, hi - lo, batch->comm_cost, batch->flags, batch->set_bin ? batch->n_bins : 0,
+                        out_wcrt, out_sched ? out_sched + lo : nullptr, batch->set_bin ? out_bins : nullptr,
+                        sets->side[1]);
+    if (rc) return rc;
+  }
+  cudaEventRecord(sets->ev[8], sets->side[1]);
+  cudaEventRecord(sets->ev[9], sets->side[0]);
+  cudaStreamWaitEvent(st, sets->ev[8], 0);
+  cudaStreamWaitEvent(st, sets->ev[9], 0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "paam_pack_analyze");
+  sets->dev = *batch;
+  sets->n_sets = n;
+  sets->n_chains = batch->n_chains;
+  sets->n_bins = batch->set_bin ? batch->n_bins : 0;
+  sets->comm = batch->comm_cost;
+  sets->flags = batch->flags;
+  return PAAM_OK;
+}
+
 extern "C" int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins) {
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n_sets) *n_sets = sets->n_sets;
@@ -200,6 +259,10 @@ extern "C" void paam_free(paam_sets* sets) {
   if (sets->rec) cudaFree(sets->rec);
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
+  if (sets->side[0]) {
+    for (int i = 0; i < 2; i++) cudaStreamDestroy(sets->side[i]);
+    for (int i = 0; i < 17; i++) cudaEventDestroy(sets->ev[i]);
+  }
   std::free(sets);
 }
 

@@ -79,6 +79,7 @@ def lib():
         L.paam_pack.argtypes = [ctypes.POINTER(PaamBatch), ctypes.POINTER(_vp), _vp, _vp]
         L.paam_repack.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp]
         L.paam_analyze.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp]
+        L.paam_pack_analyze.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                     _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_sets_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
@@ -235,6 +236,12 @@ class Sets:
         st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
                                              else out_status.data_ptr())
         check(lib().paam_repack(ctypes.byref(batch.c), self.h, st, _stream_ptr(stream)), "paam_repack")
+
+    def pack_analyze(self, batch, out_wcrt=None, out_sched=None, out_bins=None, out_status=None, stream=None):
+        """Pipelined repack + analyze (paam_pack_analyze); device tensors or None."""
+        ptr = lambda t: None if t is None else t.data_ptr()
+        check(lib().paam_pack_analyze(ctypes.byref(batch.c), self.h, ptr(out_status), ptr(out_wcrt), ptr(out_sched),
+                                      ptr(out_bins), _stream_ptr(stream)), "paam_pack_analyze")
 
     def analyze(self, out_wcrt=None, out_sched=None, out_bins=None, n=None, stream=None):
         """Device tensors (torch) or None; returns nothing (asynchronous on `stream`)."""

@@ -191,3 +191,27 @@ def test_bins_accumulate_and_partition():
     assert torch.equal(tot, whole)
     _, _, ob, _ = O.generate_analyze(p, 4, 0, 10000, nthreads=NPROC)
     assert np.array_equal(whole.cpu().numpy(), ob)
+
+
+def test_pipelined_pack_analyze_matches_oracle():
+    """paam_pack_analyze (chunks of pack and analyze overlapped on two streams) == oracle."""
+    p = config3_params()
+    n = 100_003
+    raw = gen_gpu(p, 4, 7, n)
+    dev = torch.device("cuda")
+    sets = paam.Sets(raw)
+    wcrt = torch.full((raw.c.n_chains,), -7, dtype=torch.int64, device=dev)
+    sched = torch.full((n,), 9, dtype=torch.uint8, device=dev)
+    bins = torch.zeros(2 * p.n_bins, dtype=torch.int64, device=dev)
+    status = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    sets.pack_analyze(raw, wcrt, sched, bins, out_status=status)
+    torch.cuda.synchronize()
+    assert (status.cpu().numpy() == 0).all()
+    ow, osch, ob, _ = O.generate_analyze(p, 4, 7, n, want_wcrt=True, nthreads=NPROC)
+    assert np.array_equal(sched.cpu().numpy(), osch)
+    assert np.array_equal(bins.cpu().numpy(), ob)
+    off = raw.to_host()["set_chain_off"]
+    gw = wcrt.cpu().numpy().view(np.uint64)
+    m = np.diff(off)
+    idx = np.repeat(np.arange(n), m) * 32 + (np.arange(len(gw)) - np.repeat(off[:-1], m))
+    assert np.array_equal(gw, ow.reshape(-1)[idx])
