@@ -180,7 +180,8 @@ int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_sta
  * rules D1-D17: PiCAS executors, fixed-priority cores, PAAM bucket queues with cross-bucket
  * preemption, eps per request, kappa per switch) over releases in [0, horizon), run until every
  * released instance completes.  Chain c of set i is released at phase + k*T with phase = 0 when
- * seed == 0, else pg_phase(seed, first_index + i, c, T) (gen/paam_gen.h).
+ * seed == 0, else pg_phase(seed, first_index + i, c, T) (gen/paam_gen.h).  sim_flags: 0 = PAAM, or
+ * PAAM_SIM_FIFO_DIRECT (the direct-invocation baseline the paper compares against).
  *   out_resp   [n_chains total] maximum observed end-to-end response time per chain (0 if none).
  *   out_count  [n_chains total] completed instances per chain (may be NULL).
  *   out_digest [n] order-independent FNV-1a-64 digest of the event records (may be NULL).
@@ -189,8 +190,10 @@ int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_sta
  *              CRITICAL chain with out_resp > bound adds 1 to *out_violations (int64, +=).
  * Reads the raw batch the handle was packed from: a DEVICE batch must still be alive (a HOST batch
  * was staged by paam_pack).  Device pointers only. */
+#define PAAM_SIM_FIFO_DIRECT 0x1u /* baseline arbitration: one FIFO per unit in arrival
+                                     order, non-preemptive, no eps, no kappa, buckets ignored */
 int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
-                  uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
+                  uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
                   int64_t* out_violations, paam_stream_t stream);
 
 /* Handle queries (synchronous, small). */

@@ -73,6 +73,7 @@ u64 fnv1a64(const unsigned char* p, int n) {
 
 struct Sim {
   const System& s;
+  bool fifo = false;  // FIFO_DIRECT: one FIFO per unit, no eps, no kappa, no preemption
   std::vector<std::vector<int>> bucket;
   std::vector<int> unit_base;
   u64 horizon, t = 0;
@@ -134,7 +135,7 @@ struct Sim {
       e.phase = P_CPU;
       e.rem = g.wcet;
     } else {
-      const u64 eps = s.accels[g.accel].eps;
+      const u64 eps = fifo ? 0 : s.accels[g.accel].eps;
       if (s.execs[x].wait == 1) { e.phase = P_EPS_SPIN; e.rem = eps; }
       else { e.phase = P_EPS_SUSP; e.timer = t + eps; }
     }
@@ -193,6 +194,7 @@ struct Sim {
       const Req& r = U.q[i];
       if (best < 0) { best = i; continue; }
       const Req& b = U.q[best];
+      if (fifo) { if (r.seq < b.seq) best = i; continue; }  // arrival order only
       if (r.bucket != b.bucket) { if (r.bucket > b.bucket) best = i; continue; }
       if (r.started != b.started) { if (r.started) best = i; continue; }
       if (r.prio != b.prio) { if (r.prio > b.prio) best = i; continue; }
@@ -200,7 +202,7 @@ struct Sim {
     }
     return best;
   }
-  u64 kappa_eff(int a) const { return s.accels[a].buckets > 1 ? s.accels[a].kappa : 0; }
+  u64 kappa_eff(int a) const { return (!fifo && s.accels[a].buckets > 1) ? s.accels[a].kappa : 0; }
 
   // ---- phase A: everything due at t, until stable -----------------------------------------------
   bool phase_A() {
@@ -246,7 +248,7 @@ struct Sim {
         const Seg& g = cbk(e.chain, I.cb).segs[e.seg];
         Req r;
         r.chain = e.chain; r.slot = e.slot; r.cb = I.cb; r.seg = e.seg; r.exec = x;
-        r.bucket = bucket[e.chain][g.accel]; r.prio = s.chains[e.chain].prio;
+        r.bucket = fifo ? 0 : bucket[e.chain][g.accel]; r.prio = s.chains[e.chain].prio;
         r.k = I.k; r.seq = seq++; r.rem = g.wcet; r.started = false;
         const int u = unit_of(g);
         units[u].q.push_back(r);
@@ -317,7 +319,7 @@ struct Sim {
           }
           changed = true;
         }
-      } else if (U.state == U_RUN && s.accels[U.acc].buckets > 1) {  // D9
+      } else if (U.state == U_RUN && !fifo && s.accels[U.acc].buckets > 1) {  // D9
         const int i = best_req(U);
         if (i >= 0 && U.q[i].bucket > U.q[U.cur].bucket) {
           const Req& r = U.q[U.cur];
@@ -377,7 +379,7 @@ struct Sim {
 }  // namespace
 
 extern "C" int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, uint64_t seed, uint64_t first_index,
-                                         const uint64_t* phases_or_null, uint64_t* out_resp, uint64_t* out_count,
+                                         uint32_t sim_flags, const uint64_t* phases_or_null, uint64_t* out_resp, uint64_t* out_count,
                                          uint64_t* out_misc, uint64_t* out_digest, const uint64_t* bound,
                                          int64_t* out_violations, int nthreads) {
   if (!b) return -1;
@@ -401,6 +403,7 @@ extern "C" int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, ui
     for (size_t c = 0; c < m; c++)
       ph[c] = phases_or_null ? phases_or_null[c0 + c] : pg_phase(seed, first_index + i, (uint32_t)c, s.chains[c].T);
     Sim sim(s, horizon, ph);
+    sim.fifo = (sim_flags & 1u) != 0;
     sim.run();
     // sim <= bound is claimed only for sets the analysis declares schedulable: Lemma 1's
     // arrival bound presumes schedulable interferers, so no bound is checked elsewhere.

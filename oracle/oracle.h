@@ -82,7 +82,7 @@ int32_t oracle_generate_analyze(const void* params, uint64_t seed, uint64_t firs
  * FNV-1a-64 digest of the event records; violations of `bound` counted for CRITICAL chains of sets
  * whose every CRITICAL chain has bound <= D (the analysis' schedulable sets).  phases_or_null: explicit release phases per chain (brute force), else pg_phase(). */
 int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, uint64_t seed, uint64_t first_index,
-                              const uint64_t* phases_or_null, uint64_t* out_resp, uint64_t* out_count,
+                              uint32_t sim_flags /* 1 = FIFO_DIRECT */, const uint64_t* phases_or_null, uint64_t* out_resp, uint64_t* out_count,
                               uint64_t* out_misc, uint64_t* out_digest, const uint64_t* bound,
                               int64_t* out_violations, int nthreads);
 

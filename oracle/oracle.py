@@ -53,7 +53,7 @@ def lib():
                                                  ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
                                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         _lib.oracle_simulate_batch.argtypes = [ctypes.POINTER(OrBatch), ctypes.c_uint64, ctypes.c_uint64,
-                                               ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_int]
     return _lib
@@ -124,7 +124,7 @@ def generate_analyze(params: GenParams, seed: int, first: int, n: int, comm_cost
 
 
 def simulate(batch: dict, horizon: int, seed: int = 0, first_index: int = 0, phases=None, bound=None,
-             nthreads: int = 1) -> dict:
+             nthreads: int = 1, fifo: bool = False) -> dict:
     """Oracle DES.  Returns dict(resp, count, misses, drops, overflows per chain; digest per set;
     violations)."""
     b = make_batch(batch)
@@ -137,7 +137,7 @@ def simulate(batch: dict, horizon: int, seed: int = 0, first_index: int = 0, pha
     viol = np.zeros(1, np.int64)
     ph = None if phases is None else np.ascontiguousarray(phases, np.uint64)
     bd = None if bound is None else np.ascontiguousarray(bound, np.uint64)
-    rc = lib().oracle_simulate_batch(ctypes.byref(b), horizon, seed, first_index, _ptr(ph), _ptr(resp), _ptr(cnt),
+    rc = lib().oracle_simulate_batch(ctypes.byref(b), horizon, seed, first_index, 1 if fifo else 0, _ptr(ph), _ptr(resp), _ptr(cnt),
                                      _ptr(misc), _ptr(dig), _ptr(bd), _ptr(viol), nthreads)
     assert rc == 0
     misc = misc[:3 * nch].reshape(-1, 3) if nch else np.zeros((0, 3), np.uint64)

@@ -181,11 +181,12 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
 }
 
 extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
-                             uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
+                             uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
                              int64_t* out_violations, paam_stream_t stream) {
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_simulate: n exceeds the packed sets");
-  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, out_resp, out_count, out_digest,
+  if (sim_flags & ~(uint32_t)PAAM_SIM_FIFO_DIRECT) return fail(PAAM_EINVAL, "paam_simulate: unknown sim flag");
+  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
                          bound, out_violations, (cudaStream_t)stream);
 }
 

@@ -96,6 +96,7 @@ struct Ctx {
   DesSmem& S;
   uint64_t t, horizon, comm;
   uint64_t dig;  // this lane's partial digest
+  bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
   __device__ void ev(uint32_t kind, uint32_t c, uint32_t cb, uint32_t seg, uint32_t unit, uint32_t bk) {
     dig += fnv_record(t, kind, S.cLocal[c], cb, seg, unit, bk);
   }
@@ -108,7 +109,7 @@ struct Ctx {
       S.exPhase[x] = P_CPU;
       S.exRem[x] = S.gW[g];
     } else {
-      const uint32_t eps = S.uEps[S.gUnit[g]];
+      const uint32_t eps = fifo ? 0u : S.uEps[S.gUnit[g]];
       if (S.xWait[x]) { S.exPhase[x] = P_EPS_SPIN; S.exRem[x] = eps; }
       else { S.exPhase[x] = P_EPS_SUSP; S.exTimer[x] = t + eps; }
     }
@@ -141,7 +142,7 @@ struct Ctx {
 
 __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
                                                            uint64_t horizon, uint64_t seed, uint64_t first_index,
-                                                           uint64_t* __restrict__ out_resp, uint64_t* __restrict__ out_count,
+                                                           uint32_t sim_flags, uint64_t* __restrict__ out_resp, uint64_t* __restrict__ out_count,
                                                            uint64_t* __restrict__ out_digest,
                                                            const uint64_t* __restrict__ bound,
                                                            int64_t* __restrict__ out_viol) {
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
         ubase[a] = u;
         const uint32_t nb = b.accel_buckets[a0 + a], nu = b.accel_units[a0 + a];
         const uint32_t e = (uint32_t)b.accel_eps[a0 + a];
-        const uint32_t k = nb > 1 ? (uint32_t)b.accel_kappa[a0 + a] : 0u;  // A6
+        const uint32_t k = (nb > 1 && !(sim_flags & PAAM_SIM_FIFO_DIRECT)) ? (uint32_t)b.accel_kappa[a0 + a] : 0u;  // A6
         for (uint32_t v = 0; v < nu; v++, u++) { S.uEps[u] = e; S.uKap[u] = k; S.uN[u] = nb; }
       }
     }
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             if (S.gKind[g] == 1) {
               uint32_t a = 0;
               for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= S.gUnit[g]) a = q;
-              S.gBkt[g] = (uint8_t)bk[a];
+              S.gBkt[g] = (sim_flags & PAAM_SIM_FIFO_DIRECT) ? (uint8_t)0 : (uint8_t)bk[a];
             }
     }
     // dynamic state
@@ -276,7 +277,8 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
     if (lane < MAXU) S.unState[lane] = U_IDLE;
     __syncwarp();
 
-    Ctx C{S, 0, horizon, b.comm_cost, 0};
+    const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
+    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo};
     uint32_t next_k = 0;  // lane = rank
     uint32_t seq = 0;     // warp-uniform
     bool on_core = false; // lane = canonical executor
@@ -451,6 +453,31 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
         // (7) unit dispatch (D8-D11)
         for (uint32_t u = 0; u < n_unit; u++) {
           const uint32_t ust = S.unState[u];
+          if (fifo) {  // FIFO_DIRECT: an idle unit starts the oldest request; never preempts
+            if (ust != U_IDLE) continue;
+            uint32_t myseq = 0xffffffffu;
+            int fslot = -1;
+            if (is_chain)
+              for (int q = 0; q < QCAP; q++) {
+                const Inst& I = S.inst[lane][q];
+                if (I.waiting && I.unit == u && I.seq < myseq) { myseq = I.seq; fslot = q; }
+              }
+            const uint32_t oldest = __reduce_min_sync(FULL, myseq);
+            if (oldest == 0xffffffffu) continue;
+            if (myseq == oldest) {
+              Inst& I = S.inst[lane][fslot];
+              const uint32_t j = S.cCb0[lane] + I.cb, x = S.bExec[j], seg = S.exSeg[x];
+              S.unChain[u] = (uint8_t)lane;
+              S.unSlot[u] = (uint8_t)fslot;
+              I.started = 1;
+              S.unState[u] = U_RUN;
+              S.unRem[u] = S.gW[S.bSeg0[j] + seg];
+              C.ev(EV_ACC_START, lane, I.cb, seg, u, 0u);
+            }
+            chB = true;
+            __syncwarp();
+            continue;
+          }
           if (ust != U_IDLE && !(ust == U_RUN && S.uN[u] > 1)) continue;
           // best waiting request on u, excluding the running one: key = bucket | started | priority
           uint32_t key = 0;
@@ -574,7 +601,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
 
 #ifndef PAAM_WARP_EMU
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
+                    uint64_t first_index, uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
                     const uint64_t* bound, int64_t* out_viol, cudaStream_t st) {
   if (n == 0) return PAAM_OK;
   int dev = 0, sms = 148, per_sm = 1;
@@ -585,7 +612,7 @@ int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t
   const uint32_t need = (n + SW - 1) / SW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, out_resp, out_count, out_digest,
+  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
                                            bound, out_viol);
   count_launch();
   const cudaError_t e = cudaGetLastError();

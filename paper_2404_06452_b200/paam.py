@@ -17,6 +17,7 @@ UNSCHED = (1 << 64) - 1
 
 PAAM_MEM_HOST, PAAM_MEM_DEVICE = 0, 1
 PAAM_FLAG_BLOCKING_SOUND = 0x1
+PAAM_SIM_FIFO_DIRECT = 0x1
 SET_STATUS = {0: "OK", 1: "ERANGE", 2: "EDANGLING", 3: "EACCEL", 4: "ESHAPE", 5: "EDUPPRIO",
               6: "EDEADLINE", 7: "ECORE"}
 
@@ -81,7 +82,7 @@ def lib():
         L.paam_analyze.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp]
         L.paam_pack_analyze.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
-                                    _vp, _vp, _vp, _vp, _vp, _vp]
+                                    ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_sets_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_uint32)]
         L.paam_free.argtypes = [_vp]
@@ -250,9 +251,10 @@ class Sets:
                                  ptr(out_bins), _stream_ptr(stream)), "paam_analyze")
 
     def simulate(self, horizon, seed, out_resp, out_count=None, out_digest=None, bound=None, out_violations=None,
-                 first_index=0, n=None, stream=None):
+                 first_index=0, n=None, stream=None, fifo=False):
         ptr = lambda t: None if t is None else t.data_ptr()
-        check(lib().paam_simulate(self.h, self.n_sets if n is None else n, horizon, seed, first_index, ptr(out_resp),
+        check(lib().paam_simulate(self.h, self.n_sets if n is None else n, horizon, seed, first_index,
+                                  PAAM_SIM_FIFO_DIRECT if fifo else 0, ptr(out_resp),
                                   ptr(out_count), ptr(out_digest), ptr(bound), ptr(out_violations),
                                   _stream_ptr(stream)), "paam_simulate")
 

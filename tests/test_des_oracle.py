@@ -148,3 +148,31 @@ def test_deterministic_and_seeded():
         assert np.array_equal(r1[k], r2[k])
     r3 = O.simulate(b, 2_000 * MS, seed=8)
     assert not np.array_equal(r1["digest"], r3["digest"])
+
+
+def test_fifo_direct_baseline_case_study_3():
+    """PAAM vs the direct-invocation FIFO baseline on Case Study 3:
+    chain 1's maximum under PAAM stays within its bound and is >= 20% below FIFO's maximum (the paper
+    measured -60% on hardware; the simulation asserts direction and margin only)."""
+    for buckets in (6, 1):
+        b = flatten([cs3_system(buckets)], comm_cost=0)
+        w, _, _, _ = O.analyze(b)
+        paam_max, fifo_max = 0, 0
+        for seed in range(12):
+            rp = O.simulate(b, 3_000 * MS, seed=seed, bound=w)
+            rf = O.simulate(b, 3_000 * MS, seed=seed, fifo=True)
+            assert rp["violations"] == 0
+            paam_max = max(paam_max, int(rp["resp"][0]))
+            fifo_max = max(fifo_max, int(rf["resp"][0]))
+        assert paam_max <= w[0]
+        assert paam_max <= 0.8 * fifo_max
+
+
+def test_fifo_has_no_overheads_or_priorities():
+    """FIFO_DIRECT: no eps / kappa, arrival order regardless of priority."""
+    s = System(); a = s.accel(buckets=6, server_core=0, eps=391 * US, kappa=130 * US)
+    x1 = s.executor(core=1); x2 = s.executor(core=2)
+    s.chain(T=1000 * MS, prio=1, cbs=[cb(x1, acc(a, 10 * MS))])
+    s.chain(T=1000 * MS, prio=2, cbs=[cb(x2, acc(a, 3 * MS))])
+    r = O.simulate(flatten([s], comm_cost=0), 5 * MS, phases=np.array([0, 4 * MS], np.uint64), fifo=True)
+    assert r["resp"].tolist() == [10 * MS, 6 * MS + 3 * MS]  # HP waits behind the earlier LP request

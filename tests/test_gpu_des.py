@@ -91,3 +91,31 @@ def test_des_first_index_shards_compose():
     a = gpu_sim(generate_host(p, 5, 0, 32), 3_000 * MS, 7, first_index=0, with_bound=False)
     b2 = gpu_sim(generate_host(p, 5, 32, 32), 3_000 * MS, 7, first_index=32, with_bound=False)
     assert np.array_equal(np.concatenate([a["digest"], b2["digest"]]), g["digest"])
+
+
+def gpu_sim_fifo(batch, horizon, seed):
+    dev = torch.device("cuda")
+    hb = paam.Batch.from_host(batch)
+    sets = paam.Sets(hb)
+    nch = max(hb.c.n_chains, 1)
+    resp = torch.zeros(nch, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(nch, dtype=torch.int64, device=dev)
+    dig = torch.zeros(max(hb.n_sets, 1), dtype=torch.int64, device=dev)
+    sets.simulate(horizon, seed, resp, cnt, dig, fifo=True)
+    torch.cuda.synchronize()
+    return (resp.cpu().numpy().view(np.uint64)[:hb.c.n_chains], cnt.cpu().numpy().view(np.uint64)[:hb.c.n_chains],
+            dig.cpu().numpy().view(np.uint64)[:hb.n_sets])
+
+
+def test_fifo_direct_parity_and_comparison():
+    rng = random.Random(31)
+    systems = [random_small_system(rng, max_chains=6, tmax=60) for _ in range(400)] + [cs3_system(6), cs3_system(1)]
+    b = flatten(systems, comm_cost=1)
+    for seed in (0, 4):
+        g = gpu_sim_fifo(b, 500, seed)
+        o = O.simulate(b, 500, seed=seed, nthreads=NPROC, fifo=True)
+        assert np.array_equal(g[0], o["resp"]) and np.array_equal(g[1], o["count"]) and np.array_equal(g[2], o["digest"])
+    cs = flatten([cs3_system(6)], comm_cost=0)
+    paam_r = gpu_sim(cs, 3_000 * MS, 1)
+    fifo_r = gpu_sim_fifo(cs, 3_000 * MS, 1)
+    assert paam_r["resp"][0] <= paam_r["bound"][0] and paam_r["resp"][0] <= 0.8 * fifo_r[0][0]

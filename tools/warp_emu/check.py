@@ -18,11 +18,11 @@ L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaa
 vp = ctypes.c_void_p
 L.emu_pack.argtypes = [vp, vp, vp]
 L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
-L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, vp, vp, vp, vp, vp]
+L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp, vp, vp, vp, vp]
 L.emu_record_bytes.restype = ctypes.c_uint32
 
 
-def emu_run(batch, horizon=None, seed=0, first=0):
+def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     hb = Batch.from_host(batch)
     n = hb.n_sets
     rec = np.zeros((max(n, 1), L.emu_record_bytes()), np.uint8)
@@ -40,14 +40,14 @@ def emu_run(batch, horizon=None, seed=0, first=0):
         cnt = np.zeros(nch, np.uint64)
         dig = np.zeros(max(n, 1), np.uint64)
         viol = np.zeros(1, np.int64)
-        L.emu_simulate(ctypes.addressof(hb.c), rec.ctypes.data, n, horizon, seed, first, resp.ctypes.data,
-                       cnt.ctypes.data, dig.ctypes.data, w.ctypes.data, viol.ctypes.data)
+        L.emu_simulate(ctypes.addressof(hb.c), rec.ctypes.data, n, horizon, seed, first, 1 if fifo else 0, resp.ctypes.data,
+                       cnt.ctypes.data, dig.ctypes.data, None if fifo else w.ctypes.data, viol.ctypes.data)
         out.update(resp=resp[:hb.c.n_chains], count=cnt[:hb.c.n_chains], digest=dig[:n], violations=int(viol[0]))
     return out
 
 
-def compare(batch, horizon=None, seed=0, first=0, label=""):
-    e = emu_run(batch, horizon, seed, first)
+def compare(batch, horizon=None, seed=0, first=0, label="", fifo=False):
+    e = emu_run(batch, horizon, seed, first, fifo)
     ow, osch, ost, ob = O.analyze(batch)
     ok = np.array_equal(ost, e["status"]) and np.array_equal(ow, e["wcrt"]) and np.array_equal(osch, e["sched"])
     msg = [f"{label}: analyze {'OK' if ok else 'MISMATCH'}"]
@@ -55,7 +55,7 @@ def compare(batch, horizon=None, seed=0, first=0, label=""):
         bad = np.nonzero(ow != e["wcrt"])[0][:5]
         msg.append(f"  status o={ost[:8]} e={e['status'][:8]} wcrt bad idx {bad} o={ow[bad]} e={e['wcrt'][bad]}")
     if horizon is not None:
-        o = O.simulate(batch, horizon, seed=seed, first_index=first, bound=e["wcrt"], nthreads=8)
+        o = O.simulate(batch, horizon, seed=seed, first_index=first, bound=None if fifo else e["wcrt"], nthreads=8, fifo=fifo)
         ok2 = (np.array_equal(o["resp"], e["resp"]) and np.array_equal(o["count"], e["count"])
                and np.array_equal(o["digest"], e["digest"]) and o["violations"] == e["violations"])
         msg.append(f"  des {'OK' if ok2 else 'MISMATCH'}")
