@@ -293,3 +293,11 @@ def generate_host(params: GenParams, seed: int, first: int, n: int, comm_cost=10
     if rc:
         raise RuntimeError("pg_batch_fill failed")
     return out
+
+
+def with_candidate(s: System, T, prio, cbs, D=None, cls=CRITICAL) -> System:
+    """What-if copy of a hand-built system with one more chain (admission control)."""
+    import copy
+    t = copy.deepcopy(s)
+    t.chain(T=T, D=D, prio=prio, cls=cls, cbs=cbs)
+    return t

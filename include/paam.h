@@ -168,6 +168,15 @@ int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* out_status, p
 int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcrt, uint8_t* out_sched,
                  int64_t* out_bins, paam_stream_t stream);
 
+/* paam_admit -- batched admission test.  Each packed set is a what-if
+ * "system plus candidate chain(s)"; the decision is computed by the same analysis as paam_analyze:
+ *   out_decision[i] = -1            ACCEPT: every CRITICAL chain has R* <= D;
+ *                   = c >= 0        REJECT: c is the set-local index of the highest-priority CRITICAL
+ *                                   chain with R* > D (old chain or candidate);
+ *                   = -2 - status   REJECT by validation (status = PAAM_SET_*, e.g. duplicate priority).
+ *   out_wcrt as in paam_analyze (may be NULL).  Device pointers only. */
+int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_t* out_wcrt, paam_stream_t stream);
+
 /* paam_pack_analyze -- steps 2-6 in one call, pipelined: the batch is cut into chunks whose
  * pack_kernel and analyze_kernel launches overlap on two internal streams (chunk i's analysis
  * runs while chunk i+1 is packed), joined back into `stream`.  Same results as paam_repack followed

@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
                                                           uint64_t comm, uint32_t flags, uint32_t n_bins,
                                                           uint64_t* __restrict__ out_wcrt,
                                                           uint8_t* __restrict__ out_sched,
-                                                          int64_t* __restrict__ out_bins) {
+                                                          int64_t* __restrict__ out_bins,
+                                                          int32_t* __restrict__ out_fail) {
   __shared__ WarpSmem smem[AW];
   __shared__ unsigned int sbins[2 * MAX_BINS];
   const bool smem_bins = out_bins && n_bins <= MAX_BINS;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
     if (status != PAAM_SET_OK) {
       if (out_wcrt)
         for (uint32_t i = lane; i < r.n_out; i += 32) out_wcrt[r.chain_base + i] = UNS;
+      if (out_fail && lane == 0) out_fail[set] = -2 - status;  // admission: rejected by validation
     } else {
       const uint32_t nch = r.n_chain, nsub = r.n_sub, nas = r.n_aseg;
 
@@ -278,6 +280,10 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
         ok = !critical || (Rstar != UNS && Rstar <= (uint64_t)r.cD[lane]);
       }
       sched = __all_sync(FULL, ok) ? 1u : 0u;
+      if (out_fail) {  // admission: the first failing chain in priority order (lane = rank)
+        const uint32_t bad = __ballot_sync(FULL, !ok);
+        if (lane == 0) out_fail[set] = bad ? (int32_t)((r.cMisc[__ffs(bad) - 1] >> 16) & 0xffu) : -1;
+      }
     }
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
 
 #ifndef PAAM_WARP_EMU
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
-                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st) {
+                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st, int32_t* out_fail) {
   if (n == 0) return PAAM_OK;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -314,7 +320,7 @@ int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags,
   const uint32_t need = (n + AW - 1) / AW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  analyze_kernel<<<grid, AW * 32, 0, st>>>(rec, n, comm, flags, n_bins, out_wcrt, out_sched, out_bins);
+  analyze_kernel<<<grid, AW * 32, 0, st>>>(rec, n, comm, flags, n_bins, out_wcrt, out_sched, out_bins, out_fail);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "analyze_kernel launch");

@@ -180,6 +180,14 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
                         sets->n_bins ? out_bins : nullptr, (cudaStream_t)stream);
 }
 
+extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_t* out_wcrt,
+                          paam_stream_t stream) {
+  if (!sets || !out_decision) return fail(PAAM_EINVAL, "paam_admit: NULL argument");
+  if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_admit: n exceeds the packed sets");
+  return launch_analyze(sets->rec, n, sets->comm, sets->flags, 0, out_wcrt, nullptr, nullptr, (cudaStream_t)stream,
+                        out_decision);
+}
+
 extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
                              uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
                              int64_t* out_violations, paam_stream_t stream) {

@@ -80,6 +80,7 @@ def lib():
         L.paam_pack.argtypes = [ctypes.POINTER(PaamBatch), ctypes.POINTER(_vp), _vp, _vp]
         L.paam_repack.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp]
         L.paam_analyze.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp]
+        L.paam_admit.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp]
         L.paam_pack_analyze.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                     ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp]
@@ -237,6 +238,12 @@ class Sets:
         st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
                                              else out_status.data_ptr())
         check(lib().paam_repack(ctypes.byref(batch.c), self.h, st, _stream_ptr(stream)), "paam_repack")
+
+    def admit(self, out_decision, out_wcrt=None, n=None, stream=None):
+        """Batched admission decisions (paam_admit): -1 accept, >= 0 first failing chain, <= -2 invalid."""
+        ptr = lambda t: None if t is None else t.data_ptr()
+        check(lib().paam_admit(self.h, self.n_sets if n is None else n, ptr(out_decision), ptr(out_wcrt),
+                               _stream_ptr(stream)), "paam_admit")
 
     def pack_analyze(self, batch, out_wcrt=None, out_sched=None, out_bins=None, out_status=None, stream=None):
         """Pipelined repack + analyze (paam_pack_analyze); device tensors or None."""
