@@ -82,6 +82,11 @@ typedef void* paam_stream_t; /* a cudaStream_t (may be NULL = legacy default str
 #define PAAM_MEM_DEVICE 1
 #define PAAM_FLAG_BLOCKING_SOUND 0x1u /* B_c charges an LP callback's accelerator handling time
                                           (SURVEY.md §8(c) A10); default = the paper's B_c */
+#define PAAM_FLAG_WFD_UNITS 0x2u      /* assign accelerator segments to units by Worst-Fit-Decreasing
+                                           instead of seg_unit: per accelerator,
+                                          callbacks by decreasing (sum A << 24) / T onto the least-
+                                          loaded unit (ties: lowest unit); a callback's segments stay
+                                          together */
 
 /* Raw batch: the paper's system model as flat CSR arrays.  `mem` says whether the
  * pointers are host or device memory.  Sizes n_chains..n_accels are the totals (= last entries

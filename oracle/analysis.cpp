@@ -301,7 +301,9 @@ SetResult analyze_system(const System& s) {
   out.sched = 0;
   out.mu_literal = out.mu_regrouped = out.iters = 0;
   if (out.status != OR_OK) return out;
-  Analysis an(s);
+  System sw = s;
+  if (s.flags & OR_FLAG_WFD_UNITS) apply_wfd(sw);  // units by WFD
+  Analysis an(sw);
   an.run();
   int sched = 1;
   for (int c = 0; c < (int)s.chains.size(); c++) {
@@ -363,6 +365,7 @@ extern "C" int32_t oracle_analyze_detail(const or_batch* b, uint32_t set_index, 
   System s = read_set(b, set_index);
   out->status = validate(s);
   if (out->status != OR_OK) return 0;
+  if (s.flags & OR_FLAG_WFD_UNITS) apply_wfd(s);
   Analysis an(s);
   an.run();
   if (an.subs.size() > OR_DMAX || an.asegs.size() > OR_DMAX) return -2;

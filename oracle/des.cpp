@@ -399,6 +399,7 @@ extern "C" int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, ui
       if (out_digest) out_digest[i] = 0;
       return;
     }
+    if (s.flags & OR_FLAG_WFD_UNITS) apply_wfd(s);
     std::vector<u64> ph(m);
     for (size_t c = 0; c < m; c++)
       ph[c] = phases_or_null ? phases_or_null[c0 + c] : pg_phase(seed, first_index + i, (uint32_t)c, s.chains[c].T);

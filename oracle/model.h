@@ -184,4 +184,30 @@ inline std::vector<std::vector<int>> bucket_map(const System& s) {
   return bucket;
 }
 
+// Worst-Fit-Decreasing assignment of accelerator segments to units ("bin-packing heuristics
+// such as WFD"): per accelerator, items = (callback, accelerator) with the callback's
+// summed WCET on it (all its segments go to one unit), utilisation u = (A << 24) / T (integer, exact
+// ordering key), sorted by u descending (ties: callback order), each placed on the unit with the least
+// summed u (ties: lowest unit index).  Overrides the input units (flag PAAM_FLAG_WFD_UNITS).
+inline void apply_wfd(System& s) {
+  for (int a = 0; a < (int)s.accels.size(); a++) {
+    struct Item { int c, j; u64 u; };
+    std::vector<Item> items;
+    for (int c = 0; c < (int)s.chains.size(); c++)
+      for (int j = 0; j < (int)s.chains[c].cbs.size(); j++) {
+        u64 A = 0;
+        for (const Seg& g : s.chains[c].cbs[j].segs) if (g.kind == 1 && g.accel == a) A += g.wcet;
+        if (A) items.push_back(Item{c, j, (A << 24) / s.chains[c].T});
+      }
+    std::stable_sort(items.begin(), items.end(), [](const Item& x, const Item& y) { return x.u > y.u; });
+    std::vector<u64> load(s.accels[a].units, 0);
+    for (const Item& it : items) {
+      int best = 0;
+      for (int k = 1; k < (int)load.size(); k++) if (load[k] < load[best]) best = k;
+      load[best] += it.u;
+      for (Seg& g : s.chains[it.c].cbs[it.j].segs) if (g.kind == 1 && g.accel == a) g.unit = best;
+    }
+  }
+}
+
 }  // namespace oracle_model

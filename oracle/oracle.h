@@ -22,6 +22,7 @@ extern "C" {
 enum { OR_OK = 0, OR_ERANGE = 1, OR_EDANGLING = 2, OR_EACCEL = 3, OR_ESHAPE = 4, OR_EDUPPRIO = 5,
        OR_EDEADLINE = 6, OR_ECORE = 7 };
 #define OR_FLAG_BLOCKING_SOUND 0x1u
+#define OR_FLAG_WFD_UNITS 0x2u
 
 typedef struct {
   uint32_t n_sets;

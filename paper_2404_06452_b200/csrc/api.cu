@@ -73,7 +73,7 @@ int check_batch(const paam_batch* b) {
   if (!b) return fail(PAAM_EINVAL, "NULL batch");
   if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
   if (b->comm_cost >= LIM) return fail(PAAM_EINVAL, "batch.comm_cost must be < 2^31 - 1 ns");
-  if (b->flags & ~PAAM_FLAG_BLOCKING_SOUND) return fail(PAAM_EINVAL, "unknown flag");
+  if (b->flags & ~(PAAM_FLAG_BLOCKING_SOUND | PAAM_FLAG_WFD_UNITS)) return fail(PAAM_EINVAL, "unknown flag");
   if (b->set_bin && b->n_bins == 0) return fail(PAAM_EINVAL, "set_bin given with n_bins == 0");
   paam_batch c = *b;
   Field f[32];

@@ -59,6 +59,28 @@ __host__ __device__ inline void make_magic(uint32_t T, uint32_t* M, uint32_t* L)
 #endif
 }
 
+// Worst-Fit-Decreasing unit assignment (flag PAAM_FLAG_WFD_UNITS), run by one
+// lane: items (one per callback using accelerator a, in callback order) with utilisation key
+// u = (sum A << 24) / T are taken by decreasing u (stable), each onto the least-loaded unit of a
+// (ties: lowest unit).  Writes the chosen unit (0-based within a) to unit_of[item].
+__device__ inline void wfd_place(uint32_t n_items, const uint64_t* u, uint32_t n_units, uint8_t* order, uint8_t* unit_of) {
+  for (uint32_t i = 0; i < n_items; i++) order[i] = (uint8_t)i;
+  for (uint32_t i = 1; i < n_items; i++) {  // stable insertion sort by u desc
+    const uint8_t v = order[i];
+    int k = (int)i - 1;
+    while (k >= 0 && u[order[k]] < u[v]) { order[k + 1] = order[k]; k--; }
+    order[k + 1] = v;
+  }
+  uint64_t load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t i = 0; i < n_items; i++) {
+    const uint32_t it = order[i];
+    uint32_t best = 0;
+    for (uint32_t k = 1; k < n_units; k++) if (load[k] < load[best]) best = k;
+    load[best] += u[it];
+    unit_of[it] = (uint8_t)best;
+  }
+}
+
 // ---- packed per-set record (written by pack.cu, read by analyze.cu / simulate.cu) ------------------
 // Fixed stride, structure-of-arrays inside the record; everything a warp needs is one contiguous
 // 16-byte-aligned block that it bulk-loads into shared memory.

@@ -35,8 +35,10 @@ struct Scratch {
   uint32_t bE[MAXCB];
   uint8_t bExec[MAXCB], bNa[MAXCB], bA0[MAXCB + 1], bSub[MAXCB];
   // accelerator segments (callback order)
-  uint32_t qAstar[MAXA];
+  uint32_t qAstar[MAXA], qA[MAXA];
   uint8_t qUnit[MAXA], qAcc[MAXA], qCb[MAXA], qRank[MAXA];
+  uint64_t wfdU[MAXCB];
+  uint8_t wfdOrder[MAXCB], wfdUnit[MAXCB], wfdCb[MAXCB];
   // executors
   uint32_t xPrio[MAXX];
   uint8_t xCore[MAXX], xWait[MAXX], xPPrank[MAXX];
@@ -300,11 +302,34 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
           const uint32_t a = b.seg_accel[k];
           const uint32_t w = (uint32_t)min(b.seg_wcet[k], (uint64_t)SAT);
           s.qAstar[q] = sadd(w, sadd(s.aKeff[a], s.aKeff[a]));  // A* = A + 2 kappa_eff
+          s.qA[q] = w;
           s.qUnit[q] = (uint8_t)(s.aUbase[a] + b.seg_unit[k]);
           s.qAcc[q] = (uint8_t)a;
           s.qCb[q] = (uint8_t)j;
           s.qRank[q] = (uint8_t)rk;
           q++;
+        }
+      }
+    }
+    __syncwarp();
+    if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) {  // WFD unit assignment, per accelerator
+      for (uint32_t a = 0; a < nac; a++) {
+        uint32_t ni = 0;
+        for (uint32_t j = 0; j < ncb; j++) {
+          if (!s.bNa[j]) continue;
+          const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1, rk = s.rank_of[c];
+          const uint32_t q0 = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
+          uint64_t A = 0;
+          for (uint32_t q = q0; q < q0 + s.bNa[j]; q++) if (s.qAcc[q] == a) A += s.qA[q];
+          if (A) { s.wfdU[ni] = (A << 24) / s.rT[rk]; s.wfdCb[ni] = (uint8_t)j; ni++; }
+        }
+        wfd_place(ni, s.wfdU, s.aUnits[a], s.wfdOrder, s.wfdUnit);
+        for (uint32_t i = 0; i < ni; i++) {
+          const uint32_t j = s.wfdCb[i];
+          const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1, rk = s.rank_of[c];
+          const uint32_t q0 = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
+          for (uint32_t q = q0; q < q0 + s.bNa[j]; q++)
+            if (s.qAcc[q] == a) s.qUnit[q] = (uint8_t)(s.aUbase[a] + s.wfdUnit[i]);
         }
       }
     }

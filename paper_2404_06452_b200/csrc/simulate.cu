@@ -237,6 +237,31 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
       S.gUnit[g] = kind == 1 ? (uint8_t)(ubase[b.seg_accel[sg0 + g]] + b.seg_unit[sg0 + g]) : (uint8_t)0;
     }
     __syncwarp();
+    if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) {  // WFD unit assignment, as pack_kernel
+      __shared__ uint64_t wu_all[SW][MAXCB];
+      __shared__ uint8_t wo_all[SW][MAXCB], wn_all[SW][MAXCB], wc_all[SW][MAXCB];
+      uint64_t* wu = wu_all[threadIdx.x >> 5];
+      uint8_t *wo = wo_all[threadIdx.x >> 5], *wn = wn_all[threadIdx.x >> 5], *wc = wc_all[threadIdx.x >> 5];
+      for (uint32_t a = 0; a < nac; a++) {
+        const uint32_t nu = b.accel_units[a0 + a];
+        uint32_t ni = 0;
+        for (uint32_t j = 0; j < ncb; j++) {
+          uint32_t k = 0;
+          for (uint32_t q = 0; q < nch; q++) if (S.cCb0[q] <= j && j < S.cCb0[q] + S.cNcb[q]) k = q;
+          uint64_t A = 0;
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1 && b.seg_accel[sg0 + g] == a) A += S.gW[g];
+          if (A) { wu[ni] = (A << 24) / S.cT[k]; wc[ni] = (uint8_t)j; ni++; }
+        }
+        wfd_place(ni, wu, nu, wo, wn);
+        for (uint32_t i = 0; i < ni; i++) {
+          const uint32_t j = wc[i];
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1 && b.seg_accel[sg0 + g] == a) S.gUnit[g] = (uint8_t)(ubase[a] + wn[i]);
+        }
+      }
+    }
+    __syncwarp();
     // buckets (A5): per accelerator, chains using it ranked by priority, groups of ceil(m_a/n)
     {
       uint32_t use = 0;  // lane = rank

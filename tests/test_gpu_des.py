@@ -119,3 +119,10 @@ def test_fifo_direct_parity_and_comparison():
     paam_r = gpu_sim(cs, 3_000 * MS, 1)
     fifo_r = gpu_sim_fifo(cs, 3_000 * MS, 1)
     assert paam_r["resp"][0] <= paam_r["bound"][0] and paam_r["resp"][0] <= 0.8 * fifo_r[0][0]
+
+
+def test_des_wfd_units_parity():
+    rng = random.Random(55)
+    systems = [random_small_system(rng, max_chains=6, tmax=60) for _ in range(300)]
+    b = flatten(systems, comm_cost=1, flags=2)
+    check(b, 400, 3)

@@ -215,3 +215,15 @@ def test_pipelined_pack_analyze_matches_oracle():
     m = np.diff(off)
     idx = np.repeat(np.arange(n), m) * 32 + (np.arange(len(gw)) - np.repeat(off[:-1], m))
     assert np.array_equal(gw, ow.reshape(-1)[idx])
+
+
+@pytest.mark.parametrize("flags", [2, 3])
+def test_wfd_units_parity(flags):
+    rng = random.Random(100 + flags)
+    systems = [random_small_system(rng, max_chains=6, tmax=200) for _ in range(2000)]
+    b = flatten(systems, comm_cost=3, flags=flags)
+    assert_same(b, gpu_host_path(b))
+    p = make_params(accels=((6, 3, 391 * US, 130 * US), (1, 2, 391 * US, 0)))
+    g = generate_host(p, 3, 0, 5000)
+    g["flags"] = flags
+    assert_same(g, gpu_host_path(g))

@@ -223,3 +223,27 @@ def test_empty_set_is_vacuously_schedulable():
     s = System(); s.accel(server_core=0)
     _, (wcrt, sched, status, _) = run([s])
     assert status[0] == 0 and sched[0] == 1 and wcrt.size == 0
+
+
+def _wfd_system(utils):
+    s = System()
+    a = s.accel(buckets=1, units=2, server_core=0)
+    for i, A in enumerate(utils):
+        x = s.executor(core=1 + i)
+        s.chain(T=100, prio=len(utils) - i, cbs=[cb(x, acc(a, A))])
+    return s
+
+
+def test_wfd_unit_assignment():
+    """PAAM_FLAG_WFD_UNITS: by decreasing utilisation onto the least-loaded unit.
+    [0.4, 0.3, 0.2] -> {0.4} and {0.3, 0.2} (the rule of S:101; the example at S:104 lists
+    {0.4, 0.2}/{0.3}, which is not worst fit -- DESIGN.md reading W).  Observed through LP blocking:
+    only chains sharing a unit block each other (one bucket)."""
+    d = O.detail(flatten([_wfd_system([40, 30, 20])], comm_cost=0, flags=2))
+    assert d["aseg_LPB"] == [0, 20, 0]
+    # S:106: equal utilisations alternate units: u0 {c0, c2}, u1 {c1, c3}
+    d = O.detail(flatten([_wfd_system([20, 20, 20, 20])], comm_cost=0, flags=2))
+    assert d["aseg_LPB"] == [20, 20, 0, 0]
+    # without the flag the input units (all 0) are used: everyone blocks everyone below
+    d = O.detail(flatten([_wfd_system([20, 20, 20, 20])], comm_cost=0, flags=0))
+    assert d["aseg_LPB"] == [20, 20, 20, 0]
