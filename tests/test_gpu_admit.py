@@ -42,7 +42,9 @@ def test_spec_examples():
     base = cs3_system(6)  # schedulable (Case Study 3)
     x = base.executor(core=7)
     g = 0
-    tiny = with_candidate(base, T=2000 * MS, prio=7, cbs=[cb(x, cpu(1), acc(g, 1))])       # S:243 ACCEPT
+    # a vanishing candidate (1 ns of CPU, huge period, lowest priority, own core) is accepted;
+    # one that also used the GPU would change the bucket map (7 users of 6 buckets) and break chain 2
+    tiny = with_candidate(base, T=2000 * MS, prio=0, cbs=[cb(x, cpu(1))])
     hog = with_candidate(base, T=100 * MS, prio=100, cbs=[cb(x, cpu(1 * MS), acc(g, 10 * MS))])
     selfish = with_candidate(base, T=10 * MS, D=10 * MS, prio=8, cbs=[cb(x, cpu(20 * MS))])   # S:244 REJECT(itself)
     dup = with_candidate(base, T=1000 * MS, prio=6, cbs=[cb(x, cpu(1))])                     # duplicate priority
