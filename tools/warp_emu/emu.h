@@ -17,7 +17,7 @@
 #define __host__
 #define __global__
 #define __forceinline__ inline
-#define __launch_bounds__(x)
+#define __launch_bounds__(...)
 #define __restrict__ __restrict
 #define __align__(n) alignas(n)
 #define __shared__ static
