@@ -37,8 +37,7 @@ struct Scratch {
   // accelerator segments (callback order)
   uint32_t qAstar[MAXA], qA[MAXA];
   uint8_t qUnit[MAXA], qAcc[MAXA], qCb[MAXA], qRank[MAXA];
-  uint64_t wfdU[MAXCB];
-  uint8_t wfdOrder[MAXCB], wfdUnit[MAXCB], wfdCb[MAXCB];
+
   // executors
   uint32_t xPrio[MAXX];
   uint8_t xCore[MAXX], xWait[MAXX], xPPrank[MAXX];
@@ -48,8 +47,13 @@ struct Scratch {
   // per (rank, unit) / (unit, rank)
   uint32_t W[MAXC][MAXU];
   uint32_t maxA[MAXU][MAXC];
-  uint32_t lpb[MAXU][MAXC];
-  uint32_t pre2[MAXU][MAXC];
+  union {  // WFD scratch is dead before pre2 is computed
+    uint32_t pre2[MAXU][MAXC];
+    struct {
+      uint64_t wfdU[MAXCB];
+      uint8_t wfdOrder[MAXCB], wfdUnit[MAXCB], wfdCb[MAXCB];
+    };
+  };
   uint32_t cmp[MAXC];
   // sub-chains (callback order of their first callback)
   uint8_t sRank[MAXS], sCanon[MAXS], sExec[MAXS];
@@ -76,22 +80,31 @@ __device__ __forceinline__ uint32_t scan_excl(uint32_t v, int lane) {  // plain 
   return x - v;
 }
 
-__global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* __restrict__ recs,
+__global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Record* __restrict__ recs,
                                                           int32_t* __restrict__ status_out) {
   __shared__ Scratch smem[WARPS];
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   Scratch& s = smem[threadIdx.x >> 5];
-  const uint32_t nwarps = gridDim.x * WARPS;
-  for (uint32_t set = blockIdx.x * WARPS + (threadIdx.x >> 5); set < b.n_sets; set += nwarps) {
+  // Blocked assignment: warp w owns the contiguous sets [lo, hi).  Consecutive sets are adjacent in
+  // every CSR array, so the next set's start offsets are this set's end offsets: after the first set
+  // no dependent offset loads remain, and the next set's lines are often already in L2.
+  const uint32_t nwarps = gridDim.x * WARPS, wid = blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const uint32_t lo = (uint32_t)((uint64_t)b.n_sets * wid / nwarps);
+  const uint32_t hi = (uint32_t)((uint64_t)b.n_sets * (wid + 1) / nwarps);
+  uint32_t c0 = 0, x0 = 0, a0 = 0, cb0 = 0, sg0 = 0;
+  if (lo < hi) {
+    c0 = b.set_chain_off[lo]; x0 = b.set_exec_off[lo]; a0 = b.set_accel_off[lo];
+    cb0 = b.chain_cb_off[c0];
+    sg0 = b.cb_seg_off[cb0];
+  }
+  for (uint32_t set = lo; set < hi; set++) {
     Record* r = recs + set;
-    const uint32_t c0 = b.set_chain_off[set], c1 = b.set_chain_off[set + 1];
-    const uint32_t x0 = b.set_exec_off[set], x1 = b.set_exec_off[set + 1];
-    const uint32_t a0 = b.set_accel_off[set], a1 = b.set_accel_off[set + 1];
+    const uint32_t c1 = b.set_chain_off[set + 1], x1 = b.set_exec_off[set + 1], a1 = b.set_accel_off[set + 1];
     const uint32_t nch = c1 - c0, nex = x1 - x0, nac = a1 - a0;
-    const uint32_t cb0 = b.chain_cb_off[c0], cb1 = b.chain_cb_off[c1];
+    const uint32_t cb1 = b.chain_cb_off[c1];
     const uint32_t ncb = cb1 - cb0;
-    const uint32_t sg0 = b.cb_seg_off[cb0], sg1 = b.cb_seg_off[cb1];
+    const uint32_t sg1 = b.cb_seg_off[cb1];
     const uint32_t nseg = sg1 - sg0;
     int st = PAAM_SET_OK;
 
@@ -246,6 +259,7 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
     }
     if (st != PAAM_SET_OK) {
       __syncwarp();
+      c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
       continue;
     }
 
@@ -378,7 +392,7 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
         __syncwarp();
         if ((uint32_t)lane < ma) s.cmp[lane] = ex;
         __syncwarp();
-        s.lpb[u][lane] = user ? s.cmp[p] : 0u;
+        s.maxA[u][lane] = user ? s.cmp[p] : 0u;  // in place: maxA becomes LP blocking
         __syncwarp();
       }
     }
@@ -435,7 +449,7 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
       for (uint32_t q = qa; q < qa + qn; q++) {
         const uint32_t u = s.qUnit[q];
         eps = sadd(eps, s.aEps[s.qAcc[q]]);
-        base3 = sadd(base3, sadd(s.qAstar[q], s.lpb[u][s_rank]));
+        base3 = sadd(base3, sadd(s.qAstar[q], s.maxA[u][s_rank]));
         umask |= 1u << u;
       }
       uint32_t hp = 0, lp = 0, hpp = 0, B = 0;
@@ -483,13 +497,14 @@ __global__ void __launch_bounds__(WARPS * 32) pack_kernel(paam_batch b, Record* 
     // ---- accelerator segments (rank order) ------------------------------------------------------------
     for (uint32_t q = lane; q < n_aseg; q += 32) {
       const uint32_t u = s.qUnit[q], rk = s.qRank[q];
-      r->aBase2[q] = sadd(sadd(s.qAstar[q], s.lpb[u][rk]), s.pre2[u][rk]);
+      r->aBase2[q] = sadd(sadd(s.qAstar[q], s.maxA[u][rk]), s.pre2[u][rk]);
       r->aEps[q] = s.aEps[s.qAcc[q]];
       r->aCbE[q] = s.bE[s.qCb[q]];
       r->aMisc[q] = rk | (u << 8) | ((uint32_t)s.sCanon[s.bSub[s.qCb[q]]] << 16) | ((uint32_t)s.qCb[q] << 24);
     }
     if (lane == 0) { r->n_chain = (uint8_t)nch; r->n_sub = (uint8_t)n_sub; r->n_aseg = (uint8_t)n_aseg; r->n_unit = (uint8_t)n_unit; }
     __syncwarp();
+    c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
   }
 }
 
