@@ -349,187 +349,6 @@ def run_ours(args):
                             ("derived" if dominant is ana_roof else "fallback"),
                  "note": "kernel_ms from a sequential repack+analyze pass on the bench stream; the timed step "
                          "overlaps pack and analyze chunks on two internal streams (paam_pack_analyze)"})
-    out = {"metric": METRIC, "value": v, "unit": "chain-sets/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-           "impl": "reference",
-           "config": {"workload": f"config-3 recipe, seed {SEED}, {per_step} sets per step (bounded sample)",
-                      "sets_per_step": per_step},
-           "cpu_baseline": {"value": v, "unit": "chain-sets/s", "cores": nthreads, "kind": "oracle",
-                            "sample": f"{per_step} sets per step x {args.steps} steps"},
-           "e2e": {"value": v, "unit": "chain-sets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
-
-
-def batch_bytes(c) -> int:
-    n, ch, cb, sg, ex, ac = c.n_sets, c.n_chains, c.n_cbs, c.n_segs, c.n_execs, c.n_accels
-    return (3 * 4 * (n + 1) + ch * (8 + 8 + 4 + 1) + 4 * (ch + 1) + cb * 2 + 4 * (cb + 1) + sg * (1 + 8 + 1 + 1)
-            + ex * (1 + 4 + 1) + ac * (1 + 1 + 1 + 8 + 8) + (4 * n if c.set_bin else 0))
-
-
-def run_ours(args):
-    import numpy as np
-    import torch
-    from paper_2404_06452_b200 import paam
-
-    world, rank, local = dist_setup(args.gpus)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    from paper_2404_06452_b200.shard import allreduce_bins, shard_range
-    first, n = shard_range(rank, world, args.sets_per_gpu)
-    from gen.inputs import config3_params  # workload recipe (shared input generator params)
-    gp = config3_params()
-    params = paam.PaamGenParams.from_buffer_copy(bytes(gp))
-    stream = torch.cuda.Stream(device=dev)
-
-    # ---- inputs resident in HBM (generated on device; outside the timed region) ------------------
-    with torch.cuda.stream(stream):
-        raw = paam.Raw(params, SEED, first, n, stream=stream)
-        sets = paam.Sets(raw, stream=stream)
-        wcrt = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
-        sched = torch.empty(n, dtype=torch.uint8, device=dev)
-        bins = torch.zeros(2 * gp.n_bins, dtype=torch.int64, device=dev)
-    stream.synchronize()
-    rec_bytes = paam.lib().paam_record_bytes()
-    in_bytes = batch_bytes(raw.c)
-
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-    def step():
-        # §8(a) steps 2-6 pipelined: pack_kernel of chunk i+1 overlaps analyze_kernel of chunk i
-        sets.pack_analyze(raw, wcrt, sched, bins, stream=stream)
-        if dist is not None:                                  # the one exchange: bin counts
-            allreduce_bins(bins, stream=stream)
-
-    # ---- warm-up ------------------------------------------------------------------------------------
-    for _ in range(args.warmup):
-        step()
-    stream.synchronize()
-    barrier(world)
-
-    # ---- timed region: K steps, CUDA events on the launching stream ---------------------------------
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
-    clocks.start()
-    launches0 = paam.kernel_launches()
-    torch.cuda.synchronize()
-    barrier(world)
-    start.record(stream)
-    for k in range(args.steps):
-        step()
-    end.record(stream)
-    stream.synchronize()
-    torch.cuda.synchronize()
-    barrier(world)
-    launches = paam.kernel_launches() - launches0
-    clk = clocks.stop()
-    ms_local = start.elapsed_time(end)
-    ms = max_over_ranks(ms_local, world)
-    value = world * n * args.steps / (ms / 1e3)
-
-    # ---- per-kernel durations: the same kernels launched one after the other on `stream` ------------
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    for k in range(args.steps):
-        ev[k][0].record(stream)
-        sets.repack(raw, stream=stream)
-        ev[k][1].record(stream)
-        sets.analyze(wcrt, sched, bins, stream=stream)
-        ev[k][2].record(stream)
-    stream.synchronize()
-    pack_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    ana_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    seq_ms = sum(e[0].elapsed_time(e[2]) for e in ev) / args.steps
-    bins.zero_()
-    sets.analyze(None, None, bins, stream=stream)  # one clean pass for the reported bin counts
-    if dist is not None:
-        allreduce_bins(bins, stream=stream)
-    stream.synchronize()
-
-    # ---- e2e: the same metric through the C ABI with HOST buffers (copies inside the region) ------
-    e2e = None
-    if not args.no_e2e:
-        from gen.inputs import generate_host
-
-        def pinned(nbytes):
-            return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True).numpy()
-
-        host = generate_host(gp, SEED, first, n, pinned_alloc=pinned)
-        hb = paam.Batch.from_host(host)
-        sched_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-        bins_h = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
-        hsets = paam.Sets(hb, stream=stream)
-        def e2e_step():
-            hsets.repack(hb, stream=stream)                    # H2D of the raw batch + pack kernel
-            hsets.analyze(None, sched, bins, stream=stream)
-            if dist is not None:
-                allreduce_bins(bins, stream=stream)
-            with torch.cuda.stream(stream):
-                sched_h.copy_(sched, non_blocking=True)       # D2H: verdicts + bin counts
-                bins_h.copy_(bins, non_blocking=True)
-            stream.synchronize()
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        barrier(world)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-        e2e = {"value": world * n * args.steps / e2e_s, "unit": "chain-sets/s",
-               "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
-               "ms_per_step": 1e3 * e2e_s / args.steps}
-        hsets.free()
-
-    # ---- config 5 leg: the paired DES (paam_simulate) with the sim <= bound census -------------------
-    des = None
-    if args.des_sets > 0:
-        nd = min(args.des_sets, n)
-        resp = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
-        dig = torch.empty(n, dtype=torch.int64, device=dev)
-        viol = torch.zeros(1, dtype=torch.int64, device=dev)
-        hz = int(args.des_horizon_s * 1e9)
-        sets.simulate(hz, 3, resp, None, dig, None, None, first_index=first, n=min(nd, 1024), stream=stream)  # warm-up
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        l0 = paam.kernel_launches()
-        e0.record(stream)
-        sets.simulate(hz, 3, resp, None, dig, wcrt, viol, first_index=first, n=nd, stream=stream)
-        e1.record(stream)
-        stream.synchronize()
-        des_ms = max_over_ranks(e0.elapsed_time(e1), world)
-        v = viol.clone()
-        if dist is not None:
-            dist.all_reduce(v)
-        des = {"metric": "chain-sets simulated/sec (PAAM DES, config-5 leg)", "value": world * nd / (des_ms / 1e3),
-               "unit": "chain-sets/s", "sets_per_gpu": nd, "horizon_s": args.des_horizon_s, "seed": 3,
-               "ms": des_ms, "sim_le_bound_violations": int(v.item()), "gpu_launches": paam.kernel_launches() - l0,
-               "scope": "violations counted in sets the analysis declares schedulable (every CRITICAL chain R* <= D)"}
-
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline of the dominant kernel --------------------------------------------------------------
-    pk = peaks()
-    work = work_per_set(gp, first)
-    ana_avg = sum(ana_ms) / len(ana_ms)
-    pack_avg = sum(pack_ms) / len(pack_ms)
-    sm_clock_hz = 1.965e9
-    alu_peak = 148 * 128 * sm_clock_hz / 1e12  # T lane-ops/s: 148 SMs x 4 SMSP x 32 lanes (alu + fma pipes)
-    ops = work["mu_regrouped_per_set"] * OPS_PER_MU * n
-    achieved = ops / (ana_avg / 1e3) / 1e12
-    traffic = measured_traffic_per_set()
-    roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s (int32 lane-ops)",
-            "frac": achieved / alu_peak,
-            "traffic": None if traffic is None else traffic * n,
-            "kernel": "analyze_kernel", "kernel_ms": ana_avg, "pack_kernel_ms": pack_avg,
-            "kernel_share_of_step": ana_avg / seq_ms, "sequential_step_ms": seq_ms,
-            "note": "kernel_ms from a sequential repack+analyze pass on the bench stream; the timed step "
-                    "overlaps pack and analyze chunks on two internal streams (paam_pack_analyze)",
-            "ops_per_set": work["mu_regrouped_per_set"] * OPS_PER_MU,
-            "peak_source": "derived: 148 SMs x 128 int32 lanes/clk (B300_MICROARCH alu+fma pipes) x 1.965 GHz",
-            "hbm": {"achieved_GBps": (rec_bytes * n + 9 * n) / (ana_avg / 1e3) / 1e9,
-                    "peak_GBps": pk.get("hbm_gbs", 6533.2), "of": "measured" if pk else "fallback"}}
     out = {"metric": METRIC, "value": value, "unit": "chain-sets/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -564,7 +383,7 @@ def work_per_set(gp, first, sample=4000):
 
 
 def measured_traffic_per_set():
-    """dram bytes per set per kernel from the committed ncu --set full capture, if present."""
+    """dram bytes per set of analyze_kernel from the committed ncu --set full capture, if present."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         return {k: float(v["dram_bytes_per_set"]) for k, v in d.items() if not k.startswith("_")}
