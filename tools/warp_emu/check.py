@@ -14,7 +14,7 @@ from gen.inputs import MS, config2_params, config3_params, flatten, generate_hos
 from oracle import oracle as O  # noqa
 from paper_2404_06452_b200.paam import Batch  # noqa  (only for the batch struct marshalling)
 
-L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaam_emu.so"))
+L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("PAAM_EMU_LIB", "libpaam_emu.so")))
 vp = ctypes.c_void_p
 L.emu_pack.argtypes = [vp, vp, vp]
 L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
