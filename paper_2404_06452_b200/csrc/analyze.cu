@@ -21,7 +21,8 @@ namespace paam {
 namespace {
 
 constexpr int AW = 8;          // warps per block
-constexpr int MAX_BINS = 256;  // bins accumulated in shared memory (more: direct global atomics)
+constexpr int WARP_BINS = 32;  // bins counted per warp in shared memory (more: direct global atomics)
+constexpr uint32_t TICK = 2;   // sets per work ticket
 constexpr uint64_t UNS = PAAM_UNSCHED;
 
 struct __align__(16) WarpSmem {
@@ -63,20 +64,31 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
                                                           uint64_t* __restrict__ out_wcrt,
                                                           uint8_t* __restrict__ out_sched,
                                                           int64_t* __restrict__ out_bins,
-                                                          int32_t* __restrict__ out_fail) {
+                                                          int32_t* __restrict__ out_fail,
+                                                          unsigned int* __restrict__ ticket) {
   __shared__ WarpSmem smem[AW];
-  __shared__ unsigned int sbins[2 * MAX_BINS];
-  const bool smem_bins = out_bins && n_bins <= MAX_BINS;
-  if (smem_bins)
-    for (uint32_t i = threadIdx.x; i < 2 * n_bins; i += blockDim.x) sbins[i] = 0;
-  __syncthreads();
-
+  __shared__ unsigned int wbins_all[AW][2 * WARP_BINS];
   const int lane = threadIdx.x & 31;
   WarpSmem& w = smem[threadIdx.x >> 5];
+  unsigned int* wbins = wbins_all[threadIdx.x >> 5];
+  const bool warp_bins = out_bins && n_bins <= WARP_BINS;  // per-warp counters, flushed at warp exit
+  if (warp_bins) for (uint32_t i = lane; i < 2 * n_bins; i += 32) wbins[i] = 0;
   Record& r = w.rec;
-  const uint32_t nwarps = gridDim.x * AW;
 
-  for (uint32_t set = blockIdx.x * AW + (threadIdx.x >> 5); set < n; set += nwarps) {
+  // Dynamic work distribution: warps take TICK consecutive sets per atomic ticket, so the per-set
+  // cost variance does not leave warps (and their block's resources) idle at the end.
+  uint32_t set = 0, left = 0;
+  for (;;) {
+    if (left == 0) {
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(ticket, TICK);
+      set = __shfl_sync(FULL, t, 0);
+      if (set >= n) break;
+      left = min((uint32_t)TICK, n - set);
+    } else {
+      set++;
+    }
+    left--;
     // ---- stage the record in shared memory (16-byte vector loads, coalesced) ---------------------
     {
       const uint4* src = reinterpret_cast<const uint4*>(recs + set);
@@ -288,9 +300,9 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
       if (out_bins) {
-        if (smem_bins) {
-          atomicAdd(&sbins[2 * r.bin], 1u);
-          if (sched) atomicAdd(&sbins[2 * r.bin + 1], 1u);
+        if (warp_bins) {
+          wbins[2 * r.bin]++;
+          if (sched) wbins[2 * r.bin + 1]++;
         } else {
           atomicAdd((unsigned long long*)&out_bins[2 * r.bin], 1ull);
           if (sched) atomicAdd((unsigned long long*)&out_bins[2 * r.bin + 1], 1ull);
@@ -299,10 +311,10 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
     }
     __syncwarp();
   }
-  if (smem_bins) {
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < 2 * n_bins; i += blockDim.x)
-      if (sbins[i]) atomicAdd((unsigned long long*)&out_bins[i], (unsigned long long)sbins[i]);
+  if (warp_bins) {
+    __syncwarp();
+    for (uint32_t i = lane; i < 2 * n_bins; i += 32)
+      if (wbins[i]) atomicAdd((unsigned long long*)&out_bins[i], (unsigned long long)wbins[i]);
   }
 }
 
@@ -310,8 +322,10 @@ __global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restri
 
 #ifndef PAAM_WARP_EMU
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
-                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st, int32_t* out_fail) {
+                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
+                   cudaStream_t st, int32_t* out_fail) {
   if (n == 0) return PAAM_OK;
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -320,7 +334,8 @@ int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags,
   const uint32_t need = (n + AW - 1) / AW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  analyze_kernel<<<grid, AW * 32, 0, st>>>(rec, n, comm, flags, n_bins, out_wcrt, out_sched, out_bins, out_fail);
+  analyze_kernel<<<grid, AW * 32, 0, st>>>(rec, n, comm, flags, n_bins, out_wcrt, out_sched, out_bins, out_fail,
+                                           ticket);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "analyze_kernel launch");

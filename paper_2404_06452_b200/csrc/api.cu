@@ -21,6 +21,7 @@ struct paam_sets {
   paam_batch dev;    // the packed batch with device pointers (paam_simulate reads its structure)
   cudaStream_t side[2];  // internal streams of paam_pack_analyze (created on first use)
   cudaEvent_t ev[17];
+  unsigned int* tickets;  // work-distribution counters of the analyze launches (16 chunk slots + 1)
 };
 
 namespace paam {
@@ -158,7 +159,12 @@ extern "C" int paam_pack(const paam_batch* batch, paam_sets** out, int32_t* out_
   paam_sets* s = (paam_sets*)std::calloc(1, sizeof(paam_sets));
   if (!s) return fail(PAAM_ENOMEM, "host allocation");
   s->cap = batch->n_sets;
-  cudaError_t e = cudaMalloc((void**)&s->rec, sizeof(Record) * (size_t)(batch->n_sets ? batch->n_sets : 1));
+  cudaError_t e = cudaMalloc((void**)&s->tickets, sizeof(unsigned int) * 32);
+  if (e != cudaSuccess) {
+    std::free(s);
+    return fail_cuda(e, "paam_pack: ticket cudaMalloc");
+  }
+  e = cudaMalloc((void**)&s->rec, sizeof(Record) * (size_t)(batch->n_sets ? batch->n_sets : 1));
   if (e != cudaSuccess) {
     std::free(s);
     return fail_cuda(e, "paam_pack: record cudaMalloc");
@@ -177,15 +183,15 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_analyze: n exceeds the packed sets");
   return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
-                        sets->n_bins ? out_bins : nullptr, (cudaStream_t)stream);
+                        sets->n_bins ? out_bins : nullptr, sets->tickets + 16, (cudaStream_t)stream);
 }
 
 extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_t* out_wcrt,
                           paam_stream_t stream) {
   if (!sets || !out_decision) return fail(PAAM_EINVAL, "paam_admit: NULL argument");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_admit: n exceeds the packed sets");
-  return launch_analyze(sets->rec, n, sets->comm, sets->flags, 0, out_wcrt, nullptr, nullptr, (cudaStream_t)stream,
-                        out_decision);
+  return launch_analyze(sets->rec, n, sets->comm, sets->flags, 0, out_wcrt, nullptr, nullptr,
+                        const_cast<paam_sets*>(sets)->tickets + 17, (cudaStream_t)stream, out_decision);
 }
 
 extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
@@ -238,7 +244,7 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
     cudaStreamWaitEvent(sets->side[1], sets->ev[i], 0);
     rc = launch_analyze(sets->rec + lo, hi - lo, batch->comm_cost, batch->flags, batch->set_bin ? batch->n_bins : 0,
                         out_wcrt, out_sched ? out_sched + lo : nullptr, batch->set_bin ? out_bins : nullptr,
-                        sets->side[1]);
+                        sets->tickets + i, sets->side[1]);
     if (rc) return rc;
   }
   cudaEventRecord(sets->ev[8], sets->side[1]);
@@ -266,6 +272,7 @@ extern "C" int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t*
 extern "C" void paam_free(paam_sets* sets) {
   if (!sets) return;
   if (sets->rec) cudaFree(sets->rec);
+  if (sets->tickets) cudaFree(sets->tickets);
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
   if (sets->side[0]) {

@@ -134,9 +134,10 @@ int fail(int code, const char* what);
 
 // launchers (defined in the kernel files)
 int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status, cudaStream_t st);
+// ticket: one device counter (zeroed by the launcher on `st`) for dynamic work distribution
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
-                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, cudaStream_t st,
-                   int32_t* out_fail = nullptr);
+                   uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
+                   cudaStream_t st, int32_t* out_fail = nullptr);
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
                     uint64_t first_index, uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
                     const uint64_t* bound, int64_t* out_viol, cudaStream_t st);
