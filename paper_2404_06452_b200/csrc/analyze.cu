@@ -59,7 +59,7 @@ __device__ __forceinline__ bool gor8(bool p) {
   return v != 0;
 }
 
-__global__ void __launch_bounds__(AW * 32) analyze_kernel(const Record* __restrict__ recs, uint32_t n,
+__global__ void __launch_bounds__(AW * 32, 4) analyze_kernel(const Record* __restrict__ recs, uint32_t n,
                                                           uint64_t comm, uint32_t flags, uint32_t n_bins,
                                                           uint64_t* __restrict__ out_wcrt,
                                                           uint8_t* __restrict__ out_sched,

@@ -225,7 +225,11 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
       if ((e = cudaEventCreateWithFlags(&sets->ev[i], cudaEventDisableTiming)) != cudaSuccess)
         return fail_cuda(e, "paam_pack_analyze: event");
   }
-  const int K = 8;  // chunks
+  static const int K = [] {  // chunks (PAAM_PIPELINE_CHUNKS overrides, for tuning)
+    const char* e = std::getenv("PAAM_PIPELINE_CHUNKS");
+    const int k = e ? std::atoi(e) : 2;  // measured best on B200 at 2M sets: 2 (K = 1, 4, 8 slower)
+    return k < 1 ? 1 : (k > 8 ? 8 : k);
+  }();
   const uint32_t n = batch->n_sets;
   cudaEventRecord(sets->ev[16], st);
   cudaStreamWaitEvent(sets->side[0], sets->ev[16], 0);

@@ -92,20 +92,26 @@ __global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Recor
   const uint32_t nwarps = gridDim.x * WARPS, wid = blockIdx.x * WARPS + (threadIdx.x >> 5);
   const uint32_t lo = (uint32_t)((uint64_t)b.n_sets * wid / nwarps);
   const uint32_t hi = (uint32_t)((uint64_t)b.n_sets * (wid + 1) / nwarps);
-  uint32_t c0 = 0, x0 = 0, a0 = 0, cb0 = 0, sg0 = 0;
+  uint32_t c0 = 0, x0 = 0, a0 = 0, cb0 = 0, sg0 = 0;      // start offsets of the current set
+  uint32_t nc = 0, nx = 0, na_ = 0, ncbo = 0, nsgo = 0;  // end offsets of the current set (prefetched)
   if (lo < hi) {
     c0 = b.set_chain_off[lo]; x0 = b.set_exec_off[lo]; a0 = b.set_accel_off[lo];
-    cb0 = b.chain_cb_off[c0];
-    sg0 = b.cb_seg_off[cb0];
+    nc = b.set_chain_off[lo + 1]; nx = b.set_exec_off[lo + 1]; na_ = b.set_accel_off[lo + 1];
+    cb0 = b.chain_cb_off[c0]; ncbo = b.chain_cb_off[nc];
+    sg0 = b.cb_seg_off[cb0]; nsgo = b.cb_seg_off[ncbo];
   }
   for (uint32_t set = lo; set < hi; set++) {
     Record* r = recs + set;
-    const uint32_t c1 = b.set_chain_off[set + 1], x1 = b.set_exec_off[set + 1], a1 = b.set_accel_off[set + 1];
+    const uint32_t c1 = nc, x1 = nx, a1 = na_, cb1 = ncbo, sg1 = nsgo;
     const uint32_t nch = c1 - c0, nex = x1 - x0, nac = a1 - a0;
-    const uint32_t cb1 = b.chain_cb_off[c1];
     const uint32_t ncb = cb1 - cb0;
-    const uint32_t sg1 = b.cb_seg_off[cb1];
     const uint32_t nseg = sg1 - sg0;
+    // software pipeline of the next set's end offsets: its three dependent loads are issued at three
+    // points of this set's work, so none of them is waited for
+    const bool more = set + 1 < hi;
+    uint32_t pc = c1, px = x1, pa = a1, pcb = cb1, psg = sg1;
+    if (more) { pc = b.set_chain_off[set + 2]; px = b.set_exec_off[set + 2]; pa = b.set_accel_off[set + 2]; }
+    bool st2 = !more, st3 = !more;
     int st = PAAM_SET_OK;
 
     if (nch > MAXC || ncb > MAXCB || nseg > 192 || nex > MAXX || nac > 4) st = PAAM_SET_ERANGE;
@@ -249,6 +255,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Recor
       else if (__any_sync(FULL, ecore)) st = PAAM_SET_ECORE;
     }
 
+    if (!st2) { pcb = b.chain_cb_off[pc]; st2 = true; }
     if (lane == 0) {
       r->status = st;
       r->chain_base = c0;
@@ -259,7 +266,9 @@ __global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Recor
     }
     if (st != PAAM_SET_OK) {
       __syncwarp();
+      if (!st3) psg = b.cb_seg_off[pcb];
       c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
+      nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
       continue;
     }
 
@@ -368,6 +377,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Recor
       for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
     }
     __syncwarp();
+    if (!st3) { psg = b.cb_seg_off[pcb]; st3 = true; }
     // ---- buckets (A5) and LP blocking per (unit, rank) ---------------------------------
     for (uint32_t a = 0; a < nac; a++) {
       const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
@@ -505,6 +515,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Recor
     if (lane == 0) { r->n_chain = (uint8_t)nch; r->n_sub = (uint8_t)n_sub; r->n_aseg = (uint8_t)n_aseg; r->n_unit = (uint8_t)n_unit; }
     __syncwarp();
     c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
+    nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
   }
 }
 
