@@ -59,7 +59,10 @@ __device__ __forceinline__ bool gor8(bool p) {
   return v != 0;
 }
 
-__global__ void __launch_bounds__(AW * 32, 4) analyze_kernel(const Record* __restrict__ recs, uint32_t n,
+#ifndef ANA_MINB
+#define ANA_MINB 4
+#endif
+__global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record* __restrict__ recs, uint32_t n,
                                                           uint64_t comm, uint32_t flags, uint32_t n_bins,
                                                           uint64_t* __restrict__ out_wcrt,
                                                           uint8_t* __restrict__ out_sched,

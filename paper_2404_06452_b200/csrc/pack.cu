@@ -80,7 +80,10 @@ __device__ __forceinline__ uint32_t scan_excl(uint32_t v, int lane) {  // plain 
   return x - v;
 }
 
-__global__ void __launch_bounds__(WARPS * 32, 8) pack_kernel(paam_batch b, Record* __restrict__ recs,
+#ifndef PACK_MINB
+#define PACK_MINB 8
+#endif
+__global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch b, Record* __restrict__ recs,
                                                           int32_t* __restrict__ status_out) {
   __shared__ Scratch smem[WARPS];
   const int lane = threadIdx.x & 31;
