@@ -38,11 +38,6 @@ struct __align__(16) WarpSmem {
 
 constexpr uint32_t FULL = 0xffffffffu;
 // 8-lane group reductions (xor within aligned groups of 8)
-__device__ __forceinline__ uint32_t gsum8(uint32_t v) {
-  v = sadd(v, __shfl_xor_sync(FULL, v, 4));
-  v = sadd(v, __shfl_xor_sync(FULL, v, 2));
-  return sadd(v, __shfl_xor_sync(FULL, v, 1));
-}
 __device__ __forceinline__ void gsum8x2(uint32_t& a, uint32_t& b) {
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) {
@@ -116,7 +111,11 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       // floor(.) = 0 is <= the least fixed point, so the lfp is unchanged (A3).  Products are
       // 64-bit; a product >= 2^32 (high word != 0) is far above every cutoff, and without one the
       // 64-bit sum of <= 31 products cannot overflow.
-      for (uint32_t i = lane; i < nas; i += 32) {
+      // Segments are in rank order (rank = number of HP chains = loop length), so the loop cost of a
+      // round is set by its highest rank: the first round takes segments [0, nas-32) (short loops),
+      // the second the last 32 (nas <= 64).
+      const uint32_t f = nas > 32 ? nas - 32 : 0;
+      for (uint32_t i = lane < f ? lane : f + lane; i < nas; i = (i < f) ? f + lane : nas) {
         const uint32_t misc = r.aMisc[i];
         const uint32_t rk = misc & 0xffu, u = (misc >> 8) & 0xffu;
         const uint32_t base = r.aBase2[i], cut = r.cCut[rk];
@@ -231,15 +230,18 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
               }
             }
           }
-          uint32_t wu_sum = 0;
+          // Start value (A3): R >= 1 on every iterate, so every mu >= 2 and
+          // F(R) >= B + E + min(S, base3 + 2 sum WU) + eps + 2 sum X for all R >= 1; that value is
+          // therefore <= the least fixed point and one iteration closer to it than the paper's start.
+          uint32_t wu_sum = 0, x_sum = 0;
 #pragma unroll
-          for (uint32_t j = 0; j < 4; j++) wu_sum = sadd(wu_sum, WU[j]);
+          for (uint32_t j = 0; j < 4; j++) { wu_sum = sadd(wu_sum, WU[j]); x_sum = sadd(x_sum, X[j]); }
           pois = gor8(pois);
-          const uint32_t A0 = gsum8(wu_sum);  // mu(0) = 1: the paper's start B + E + H*(0)
+          gsum8x2(wu_sum, x_sum);
           const uint32_t BE = act ? sadd(w.Bc[c], r.sE[c]) : 0u;
           const uint32_t S = act ? w.S[c] : 0u, base3 = act ? r.sBase3[c] : 0u, eps = act ? r.sEps[c] : 0u;
           const uint32_t cut = act ? r.cCut[rk] : 0u;
-          uint32_t R = sadd(BE, sadd(min(S, sadd(base3, A0)), eps)), Hst = 0;
+          uint32_t R = sadd(sadd(BE, sadd(min(S, sadd(base3, sadd(wu_sum, wu_sum))), eps)), sadd(x_sum, x_sum)), Hst = 0;
           bool done = !act || pois;
           if (pois) R = SAT;
           while (__any_sync(FULL, !done)) {
