@@ -214,6 +214,11 @@ int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t 
 int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins);
 void paam_free(paam_sets* sets);
 
+/* Make `device` current for this thread in the library's CUDA runtime.  paam_generate and paam_pack
+ * allocate on the current device; every later call on a handle switches to the handle's device
+ * itself.  (The library links its own runtime: a caller's cudaSetDevice does not reach it.) */
+int paam_set_device(int device);
+
 /* Utility: synchronous copy between any two memory spaces (cudaMemcpyDefault) on `stream`. */
 int paam_copy(void* dst, const void* src, size_t bytes, paam_stream_t stream);
 uint32_t paam_record_bytes(void); /* size of one packed per-set record in device memory */

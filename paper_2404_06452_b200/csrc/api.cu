@@ -22,6 +22,7 @@ struct paam_sets {
   cudaStream_t side[2];  // internal streams of paam_pack_analyze (created on first use)
   cudaEvent_t ev[17];
   unsigned int* tickets;  // work-distribution counters of the analyze launches (16 chunk slots + 1)
+  int device;             // the CUDA device the handle lives on (made current by every call)
 };
 
 namespace paam {
@@ -44,6 +45,13 @@ int fail_cuda(cudaError_t e, const char* what) {
 namespace {
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Every call on a handle runs on the handle's device.  This library links its own CUDA runtime, whose
+// per-thread current device is independent of the caller's (e.g. torch's), so it is set explicitly.
+inline int use_device(const paam_sets* s) {
+  const cudaError_t e = cudaSetDevice(s->device);
+  return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "cudaSetDevice");
+}
 
 struct Field { const void** ptr; size_t elems, size; };
 
@@ -95,6 +103,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
   if (rc) return rc;
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (batch->n_sets > sets->cap) return fail(PAAM_EINVAL, "paam_repack: handle capacity too small");
+  if ((rc = use_device(sets))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   paam_batch d = *batch;
@@ -159,7 +168,12 @@ extern "C" int paam_pack(const paam_batch* batch, paam_sets** out, int32_t* out_
   paam_sets* s = (paam_sets*)std::calloc(1, sizeof(paam_sets));
   if (!s) return fail(PAAM_ENOMEM, "host allocation");
   s->cap = batch->n_sets;
-  cudaError_t e = cudaMalloc((void**)&s->tickets, sizeof(unsigned int) * 32);
+  cudaError_t e = cudaGetDevice(&s->device);
+  if (e != cudaSuccess) {
+    std::free(s);
+    return fail_cuda(e, "paam_pack: cudaGetDevice");
+  }
+  e = cudaMalloc((void**)&s->tickets, sizeof(unsigned int) * 32);
   if (e != cudaSuccess) {
     std::free(s);
     return fail_cuda(e, "paam_pack: ticket cudaMalloc");
@@ -182,6 +196,7 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
                             int64_t* out_bins, paam_stream_t stream) {
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_analyze: n exceeds the packed sets");
+  if (int rc = use_device(sets)) return rc;
   return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
                         sets->n_bins ? out_bins : nullptr, sets->tickets + 16, (cudaStream_t)stream);
 }
@@ -190,6 +205,7 @@ extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decisi
                           paam_stream_t stream) {
   if (!sets || !out_decision) return fail(PAAM_EINVAL, "paam_admit: NULL argument");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_admit: n exceeds the packed sets");
+  if (int rc = use_device(sets)) return rc;
   return launch_analyze(sets->rec, n, sets->comm, sets->flags, 0, out_wcrt, nullptr, nullptr,
                         const_cast<paam_sets*>(sets)->tickets + 17, (cudaStream_t)stream, out_decision);
 }
@@ -200,6 +216,7 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_simulate: n exceeds the packed sets");
   if (sim_flags & ~(uint32_t)PAAM_SIM_FIFO_DIRECT) return fail(PAAM_EINVAL, "paam_simulate: unknown sim flag");
+  if (int rc = use_device(sets)) return rc;
   return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
                          bound, out_violations, (cudaStream_t)stream);
 }
@@ -210,6 +227,7 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   if (rc) return rc;
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (batch->n_sets > sets->cap) return fail(PAAM_EINVAL, "paam_pack_analyze: handle capacity too small");
+  if ((rc = use_device(sets))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (batch->mem == PAAM_MEM_HOST || batch->n_sets < 4096) {  // small or host batch: sequential
     rc = paam_repack(batch, sets, out_status, stream);
@@ -275,6 +293,7 @@ extern "C" int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t*
 
 extern "C" void paam_free(paam_sets* sets) {
   if (!sets) return;
+  cudaSetDevice(sets->device);
   if (sets->rec) cudaFree(sets->rec);
   if (sets->tickets) cudaFree(sets->tickets);
   if (sets->stage) cudaFree(sets->stage);
@@ -301,6 +320,11 @@ extern "C" const char* paam_last_error(void) { return g_err; }
 extern "C" uint64_t paam_kernel_launches(void) { return g_launches.load(); }
 
 extern "C" uint32_t paam_record_bytes(void) { return (uint32_t)sizeof(Record); }
+
+extern "C" int paam_set_device(int device) {
+  const cudaError_t e = cudaSetDevice(device);
+  return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "paam_set_device");
+}
 
 extern "C" int paam_copy(void* dst, const void* src, size_t bytes, paam_stream_t stream) {
   if ((!dst || !src) && bytes) return fail(PAAM_EINVAL, "paam_copy: NULL pointer");

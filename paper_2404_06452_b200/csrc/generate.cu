@@ -15,6 +15,7 @@ struct paam_raw {
   paam_batch b;
   void* buf;
   size_t bytes;
+  int device;
 };
 
 namespace paam {
@@ -174,6 +175,7 @@ extern "C" int paam_generate(const paam_gen_params* params, uint64_t seed, uint6
   if (!raw) return fail(PAAM_ENOMEM, "paam_generate: host allocation");
   if ((e = cudaMalloc(&raw->buf, bytes)) != cudaSuccess) { std::free(raw); return fail_cuda(e, "paam_generate: cudaMalloc"); }
   raw->bytes = bytes;
+  cudaGetDevice(&raw->device);
   char* base = (char*)raw->buf;
   pg_arrays o;
   void** slots[NP] = {(void**)&o.set_chain_off, (void**)&o.set_exec_off, (void**)&o.set_accel_off,
@@ -227,6 +229,7 @@ extern "C" int paam_raw_batch(const paam_raw* raw, paam_batch* out) {
 
 extern "C" void paam_raw_free(paam_raw* raw) {
   if (!raw) return;
+  cudaSetDevice(raw->device);
   cudaFree(raw->buf);
   std::free(raw);
 }

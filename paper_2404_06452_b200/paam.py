@@ -94,6 +94,7 @@ def lib():
         L.paam_kernel_launches.restype = ctypes.c_uint64
         L.paam_record_bytes.restype = ctypes.c_uint32
         L.paam_copy.argtypes = [_vp, _vp, ctypes.c_size_t, _vp]
+        L.paam_set_device.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -102,6 +103,13 @@ def check(rc: int, what: str):
     if rc != 0:
         L = lib()
         raise PaamError(f"{what}: {L.paam_strerror(rc).decode()} ({rc}): {L.paam_last_error().decode()}")
+
+
+def set_device_from_torch():
+    """Make torch's current CUDA device the library's current device (one process per GPU)."""
+    import torch
+    if torch.cuda.is_available():  # without a device the next library call fails with PAAM_ECUDA
+        check(lib().paam_set_device(torch.cuda.current_device()), "paam_set_device")
 
 
 def kernel_launches() -> int:
@@ -178,6 +186,7 @@ class Raw:
 
     def __init__(self, params: PaamGenParams, seed: int, first: int, n: int, comm_cost=100_000, flags=0, stream=None):
         self.h = _vp()
+        set_device_from_torch()
         check(lib().paam_generate(ctypes.byref(params), seed, first, n, comm_cost, flags, ctypes.byref(self.h),
                                   _stream_ptr(stream)), "paam_generate")
         self.c = PaamBatch()
@@ -230,6 +239,7 @@ class Sets:
         c = batch.c
         st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
                                              else out_status.data_ptr())
+        set_device_from_torch()
         check(lib().paam_pack(ctypes.byref(c), ctypes.byref(self.h), st, _stream_ptr(stream)), "paam_pack")
         self.n_sets = c.n_sets
         self.n_chains = c.n_chains
