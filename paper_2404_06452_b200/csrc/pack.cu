@@ -56,7 +56,7 @@ struct Scratch {
   };
   uint32_t cmp[MAXC];
   // sub-chains (callback order of their first callback)
-  uint8_t sRank[MAXS], sCanon[MAXS], sExec[MAXS];
+  uint8_t sRank[MAXS], sCanon[MAXS], sExec[MAXS], sJ0[MAXS];
   uint32_t sMaxE[MAXS];
 };
 
@@ -313,7 +313,11 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       if (k < nch) { s.rA0[k] = f; s.rNa[k] = (uint8_t)na; }
     }
     // sub-chain id of every callback
-    for (uint32_t j = lane; j < ncb; j += 32) s.bSub[j] = (uint8_t)(__popcll(runstart & ((2ull << j) - 1)) - 1);
+    for (uint32_t j = lane; j < ncb; j += 32) {
+      const uint32_t sid = __popcll(runstart & ((2ull << j) - 1)) - 1;
+      s.bSub[j] = (uint8_t)sid;
+      if ((runstart >> j) & 1ull) s.sJ0[sid] = (uint8_t)j;  // first callback of each sub-chain
+    }
     __syncwarp();
     // ---- accelerator segments: A*, unit, rank; written in rank order --------------------------------
     for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
@@ -420,22 +424,16 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     __syncwarp();
 
     // ---- sub-chains (lane = sub-chain id, callback order) -------------------------------------------
-    uint32_t s_exec = 0, s_rank = 0, s_key = 0xffffffffu, s_j0 = 0, s_nj = 0;
+    uint32_t s_exec = 0, s_rank = 0, s_key = 0xffffffffu, s_j0 = 0, s_nj = 0, s_E = 0;
     if ((uint32_t)lane < n_sub) {
-      // position of the lane-th set bit of runstart
-      const uint32_t lo = (uint32_t)runstart, hi = (uint32_t)(runstart >> 32);
-      const uint32_t nlo = __popc(lo);
-      s_j0 = (uint32_t)lane < nlo ? __fns(lo, 0, lane + 1) : 32 + __fns(hi, 0, lane + 1 - nlo);
-      const uint64_t later = runstart & ~((2ull << s_j0) - 1);
+      s_j0 = s.sJ0[lane];
+      s_nj = ((uint32_t)lane + 1 < n_sub ? s.sJ0[lane + 1] : ncb) - s_j0;  // runs never span two chains
       const uint32_t c = __popcll(cstart & ((2ull << s_j0) - 1)) - 1;
-      const uint32_t chain_end = s.rCbo[s.rank_of[c]] + s.rNcb[s.rank_of[c]];
-      const uint32_t nxt = later ? (uint32_t)__ffsll(later) - 1 : ncb;
-      s_nj = min(nxt, chain_end) - s_j0;
       s_exec = s.bExec[s_j0];
       s_rank = s.rank_of[c];
       s_key = ((uint32_t)s.xCore[s_exec] << 16) | ((uint32_t)s.xPPrank[s_exec] << 8) | s_rank;
       uint32_t mE = 0;
-      for (uint32_t j = s_j0; j < s_j0 + s_nj; j++) mE = max(mE, s.bE[j]);
+      for (uint32_t j = s_j0; j < s_j0 + s_nj; j++) { mE = max(mE, s.bE[j]); s_E = sadd(s_E, s.bE[j]); }
       s.sMaxE[lane] = mE;
       s.sRank[lane] = (uint8_t)s_rank;
       s.sExec[lane] = (uint8_t)s_exec;
@@ -456,8 +454,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       // sub-chain's accelerator segments: contiguous in rank order
       const uint32_t qa = s.rA0[s_rank] + (s.bA0[s_j0] - s.cA0[c]);
       const uint32_t qn = s.bA0[s_j0 + s_nj] - s.bA0[s_j0];
-      uint32_t E = 0;
-      for (uint32_t j = s_j0; j < s_j0 + s_nj; j++) E = sadd(E, s.bE[j]);
+      const uint32_t E = s_E;
       uint32_t eps = 0, base3 = 0, umask = 0;
       for (uint32_t q = qa; q < qa + qn; q++) {
         const uint32_t u = s.qUnit[q];
