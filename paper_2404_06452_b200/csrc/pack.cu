@@ -33,7 +33,8 @@ struct Scratch {
   uint8_t bucket[MAXC][4];
   // callbacks (set-local order)
   uint32_t bE[MAXCB];
-  uint8_t bExec[MAXCB], bNa[MAXCB], bA0[MAXCB + 1], bSub[MAXCB];
+  uint8_t bExec[MAXCB], bNa[MAXCB], bA0[MAXCB + 1], bSub[MAXCB], bFa[MAXCB], bFu[MAXCB];
+  uint32_t bFw[MAXCB];
   // accelerator segments (callback order)
   uint32_t qAstar[MAXA], qA[MAXA];
   uint8_t qUnit[MAXA], qAcc[MAXA], qCb[MAXA], qRank[MAXA];
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       uint32_t prev_exec = 0xffffffffu;
       for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
         const uint32_t j = pass * 32 + lane;
-        uint32_t exec = 0xffffffffu, E = 0, na = 0;
+        uint32_t exec = 0xffffffffu, E = 0, na = 0, fa = 0, fu = 0, fw = 0;  // fa/fu/fw: first ACCEL segment
         if (j < ncb) {
           exec = b.cb_exec[cb0 + j];
           const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
             if (kind == 0) E = sadd(E, (uint32_t)min(w, (uint64_t)SAT));
             if (kind == 1) {
               const uint32_t a = b.seg_accel[k], u = b.seg_unit[k];
+              if (na == 0) { fa = a; fu = u; fw = (uint32_t)min(w, (uint64_t)SAT); }
               na++;
               if (a >= nac) eaccel = true;
               else edang |= (u >= s.aUnits[a]);
@@ -200,6 +202,9 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
           s.bExec[j] = (uint8_t)min(exec, 255u);
           s.bE[j] = E;
           s.bNa[j] = (uint8_t)min(na, 255u);
+          s.bFa[j] = (uint8_t)min(fa, 255u);
+          s.bFu[j] = (uint8_t)min(fu, 255u);
+          s.bFw[j] = fw;
         }
         // previous callback's executor (shuffle; the pass boundary carries lane 31 over)
         uint32_t pe = __shfl_up_sync(FULL, exec, 1);
@@ -326,18 +331,21 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1;  // chain index of callback j
         const uint32_t rk = s.rank_of[c];
         uint32_t q = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
-        const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
-        for (uint32_t k = so; k < se; k++) {
-          if (b.seg_kind[k] != 1) continue;
-          const uint32_t a = b.seg_accel[k];
-          const uint32_t w = (uint32_t)min(b.seg_wcet[k], (uint64_t)SAT);
+        auto put = [&](uint32_t a, uint32_t u, uint32_t w) {
           s.qAstar[q] = sadd(w, sadd(s.aKeff[a], s.aKeff[a]));  // A* = A + 2 kappa_eff
           s.qA[q] = w;
-          s.qUnit[q] = (uint8_t)(s.aUbase[a] + b.seg_unit[k]);
+          s.qUnit[q] = (uint8_t)(s.aUbase[a] + u);
           s.qAcc[q] = (uint8_t)a;
           s.qCb[q] = (uint8_t)j;
           s.qRank[q] = (uint8_t)rk;
           q++;
+        };
+        if (s.bNa[j] == 1) {  // the common case: its one segment was kept by the callback pass
+          put(s.bFa[j], s.bFu[j], s.bFw[j]);
+        } else {
+          const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
+          for (uint32_t k = so; k < se; k++)
+            if (b.seg_kind[k] == 1) put(b.seg_accel[k], b.seg_unit[k], (uint32_t)min(b.seg_wcet[k], (uint64_t)SAT));
         }
       }
     }
