@@ -237,14 +237,15 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         edup |= (lane < nch && eq > 1);
       }
       // executors: duplicate (core, priority) and process-priority rank on the core; R1 (ECORE)
-      {
-        uint32_t pr = 0;
-        for (uint32_t y = 0; y < nex; y++) {
-          const uint32_t cy = __shfl_sync(FULL, xcore, y), py = __shfl_sync(FULL, xprio, y);
-          if (y != (uint32_t)lane && cy == xcore) {
-            edup |= (py == xprio);
-            pr += (py > xprio);
-          }
+      {  // executors sharing a core are found by match; only those are compared
+        const uint32_t same_core = __match_any_sync(FULL, xcore) & ~(1u << lane);
+        uint32_t pr = 0, m = lane < nex ? same_core : 0u;
+        while (m) {
+          const uint32_t y = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t py = s.xPrio[y];
+          edup |= (py == xprio);
+          pr += (py > xprio);
         }
         if (lane < nex) {
           s.xPPrank[lane] = (uint8_t)pr;
@@ -398,11 +399,12 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
       const uint32_t ma = __popc(U), n = s.aN[a];
       const uint32_t g = ma ? (ma + n - 1) / n : 1u;
+      const uint32_t ginv = (1u << 16) / g + 1u;  // (p * ginv) >> 16 == p / g for p < 64, g <= 32
       const bool user = (U >> lane) & 1u;
       const uint32_t p = __popc(U & lt);  // position among users in rank order
-      if (is_chain) s.bucket[lane][a] = user ? (uint8_t)(n - 1 - p / g) : (uint8_t)0xFF;
+      if (is_chain) s.bucket[lane][a] = user ? (uint8_t)(n - 1 - ((p * ginv) >> 16)) : (uint8_t)0xFF;
       // users of a form aligned blocks of g consecutive positions, one block per bucket
-      const uint32_t blk_end = min(((uint32_t)lane / g + 1) * g, ma);
+      const uint32_t blk_end = min(((((uint32_t)lane * ginv) >> 16) + 1) * g, ma);
       for (uint32_t u = s.aUbase[a]; u < s.aUbase[a] + s.aUnits[a]; u++) {
         if (user) s.cmp[p] = s.maxA[u][lane];
         __syncwarp();

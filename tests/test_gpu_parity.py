@@ -64,7 +64,7 @@ def test_random_small_systems(flags):
 
 def mutate_invalid(s: System, rng):
     """Break one validation rule (or none)."""
-    k = rng.randrange(10)
+    k = rng.randrange(11)
     if k == 0 and len(s.chains) > 1:
         s.chains[1].prio = s.chains[0].prio
     elif k == 1:
@@ -82,6 +82,8 @@ def mutate_invalid(s: System, rng):
         s.chains[0].T = 1 << 31
     elif k == 7:
         s.chains[0].cbs[0].segs.append(Seg(s.chains[0].cbs[0].segs[-1].kind, 1))
+    elif k == 8 and len(s.execs) > 1:
+        s.execs[1] = (s.execs[0][0], s.execs[0][1], s.execs[1][2])  # same core, same process priority
     return s
 
 
