@@ -253,6 +253,64 @@ def run_ours(args):
         allreduce_bins(bins, stream=stream)
     stream.synchronize()
 
+    # ---- verdict-only sweep mode (PAAM_FLAG_VERDICT_ONLY: no WCRTs, early exit at the first miss) ----
+    import types
+    vb = paam.PaamBatch.from_buffer_copy(raw.c)
+    vb.flags |= paam.PAAM_FLAG_VERDICT_ONLY
+    vbatch = types.SimpleNamespace(c=vb)
+    vbins = torch.zeros_like(bins)
+    for _ in range(args.warmup):
+        sets.pack_analyze(vbatch, None, sched, vbins, stream=stream)
+    stream.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        sets.pack_analyze(vbatch, None, sched, vbins, stream=stream)
+        if dist is not None:
+            allreduce_bins(vbins, stream=stream)
+    e1.record(stream)
+    stream.synchronize()
+    vo_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    verdict_only = {"value": world * n * args.steps / (vo_ms / 1e3), "unit": "chain-sets/s",
+                    "ms_per_step": vo_ms / args.steps,
+                    "note": "paam_pack_analyze with PAAM_FLAG_VERDICT_ONLY: verdicts + bins only, analysis of a "
+                            "set stops at its first CRITICAL deadline miss"}
+
+    # ---- e2e including device generation: paam_generate -> paam_pack_analyze -> D2H of the verdicts --
+    e2e_gen = None
+    if not args.no_e2e:
+        sched_g = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        bins_g = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
+
+        gbins = torch.zeros_like(bins)
+
+        def gen_step():
+            graw = paam.Raw(params, SEED, first, n, stream=stream)
+            with torch.cuda.stream(stream):
+                gbins.zero_()
+            sets.pack_analyze(graw, None, sched, gbins, stream=stream)
+            if dist is not None:
+                allreduce_bins(gbins, stream=stream)
+            with torch.cuda.stream(stream):
+                sched_g.copy_(sched, non_blocking=True)
+                bins_g.copy_(gbins, non_blocking=True)
+            stream.synchronize()
+            graw.free()
+        for _ in range(max(1, args.warmup)):
+            gen_step()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            gen_step()
+        gen_s = max_over_ranks(time.perf_counter() - t0, world)
+        e2e_gen = {"value": world * n * args.steps / gen_s, "unit": "chain-sets/s", "ms_per_step": 1e3 * gen_s / args.steps,
+                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
+                   "note": "host wall clock per step: device generation (incl. its allocation) + pack + analyze + "
+                           "D2H of verdicts and bins"}
+    sets.pack_analyze(raw, wcrt, sched, vbins, stream=stream)  # the handle again describes `raw` (DES leg)
+    stream.synchronize()
+
     # ---- e2e: the same metric through the C ABI with HOST buffers (copies inside the region) ------
     e2e = None
     if not args.no_e2e:
@@ -266,14 +324,18 @@ def run_ours(args):
         sched_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         bins_h = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
         hsets = paam.Sets(hb, stream=stream)
+        ebins = torch.zeros_like(bins)
+
         def e2e_step():
             hsets.repack(hb, stream=stream)                    # H2D of the raw batch + pack kernel
-            hsets.analyze(None, sched, bins, stream=stream)
+            with torch.cuda.stream(stream):
+                ebins.zero_()
+            hsets.analyze(None, sched, ebins, stream=stream)
             if dist is not None:
-                allreduce_bins(bins, stream=stream)
+                allreduce_bins(ebins, stream=stream)
             with torch.cuda.stream(stream):
                 sched_h.copy_(sched, non_blocking=True)       # D2H: verdicts + bin counts
-                bins_h.copy_(bins, non_blocking=True)
+                bins_h.copy_(ebins, non_blocking=True)
             stream.synchronize()
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -362,10 +424,15 @@ def run_ours(args):
            "bins": bins.cpu().tolist()}
     if e2e:
         out["e2e"] = e2e
+    if e2e_gen:
+        out["e2e_device_generate"] = e2e_gen
+    out["verdict_only"] = verdict_only
     if des:
         out["des"] = des
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(gp, first, budget_s=args.cpu_budget)
+    if sum(out["bins"][0::2]) != world * n:
+        raise RuntimeError(f"bin totals {sum(out['bins'][0::2])} != sets {world * n}")
     print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -87,6 +87,12 @@ typedef void* paam_stream_t; /* a cudaStream_t (may be NULL = legacy default str
                                           callbacks by decreasing (sum A << 24) / T onto the least-
                                           loaded unit (ties: lowest unit); a callback's segments stay
                                           together */
+#define PAAM_FLAG_VERDICT_ONLY 0x4u   /* verdict-only sweeps: the analysis of a
+                                          set stops at its first CRITICAL sub-chain whose Eq.5 iterate
+                                          exceeds D (R* > D follows), so out_sched and
+                                          out_bins are identical to the full mode; out_wcrt must be
+                                          NULL (PAAM_EINVAL otherwise).  paam_admit ignores the flag
+                                          (its decision names the first failing chain). */
 
 /* Raw batch: the paper's system model as flat CSR arrays.  `mem` says whether the
  * pointers are host or device memory.  Sizes n_chains..n_accels are the totals (= last entries

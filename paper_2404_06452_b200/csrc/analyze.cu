@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const uint32_t gstart = __ballot_sync(FULL, is_sub && (lane == 0 || my_core != prev_core));
       const uint32_t ngroups = __popc(gstart);
       const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
-      for (uint32_t gb = 0; gb < ngroups; gb += 4) {
+      bool miss = false;  // verdict-only: a CRITICAL sub-chain already exceeded its deadline
+      for (uint32_t gb = 0; gb < ngroups && !miss; gb += 4) {
         const uint32_t grp = gb + gi;
         uint32_t g0 = 0, glen = 0;
         if (grp < ngroups) {
@@ -274,11 +275,16 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
             w.Hs[c] = (R == SAT) ? SAT : Hst;
           }
           __syncwarp();
+          if (flags & PAAM_FLAG_VERDICT_ONLY) {  // R_c > D_c of a CRITICAL chain => R* > D
+            miss = __any_sync(FULL, act && gl == 0 && R == SAT && ((r.cMisc[rk] >> 8) & 0xffu) == 0);
+            if (miss) break;
+          }
         }
       }
       __syncwarp();
 
       // ---- step 5: end to end and verdict ---------------------------------------------------------
+      if (miss) goto verdict_done;  // verdict-only early exit: sched stays 0 (out_wcrt is NULL here)
       if (lane < nch) { w.sum[lane] = 0; w.uns[lane] = 0; }
       __syncwarp();
       if (is_sub) {
@@ -302,6 +308,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
         if (lane == 0) out_fail[set] = bad ? (int32_t)((r.cMisc[__ffs(bad) - 1] >> 16) & 0xffu) : -1;
       }
     }
+  verdict_done:
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
       if (out_bins) {

@@ -82,7 +82,8 @@ int check_batch(const paam_batch* b) {
   if (!b) return fail(PAAM_EINVAL, "NULL batch");
   if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
   if (b->comm_cost >= LIM) return fail(PAAM_EINVAL, "batch.comm_cost must be < 2^31 - 1 ns");
-  if (b->flags & ~(PAAM_FLAG_BLOCKING_SOUND | PAAM_FLAG_WFD_UNITS)) return fail(PAAM_EINVAL, "unknown flag");
+  if (b->flags & ~(PAAM_FLAG_BLOCKING_SOUND | PAAM_FLAG_WFD_UNITS | PAAM_FLAG_VERDICT_ONLY))
+    return fail(PAAM_EINVAL, "unknown flag");
   if (b->set_bin && b->n_bins == 0) return fail(PAAM_EINVAL, "set_bin given with n_bins == 0");
   paam_batch c = *b;
   Field f[32];
@@ -196,6 +197,8 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
                             int64_t* out_bins, paam_stream_t stream) {
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_analyze: n exceeds the packed sets");
+  if ((sets->flags & PAAM_FLAG_VERDICT_ONLY) && out_wcrt)
+    return fail(PAAM_EINVAL, "paam_analyze: PAAM_FLAG_VERDICT_ONLY writes no WCRTs (out_wcrt must be NULL)");
   if (int rc = use_device(sets)) return rc;
   return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
                         sets->n_bins ? out_bins : nullptr, sets->tickets + 16, (cudaStream_t)stream);
@@ -206,7 +209,7 @@ extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decisi
   if (!sets || !out_decision) return fail(PAAM_EINVAL, "paam_admit: NULL argument");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_admit: n exceeds the packed sets");
   if (int rc = use_device(sets)) return rc;
-  return launch_analyze(sets->rec, n, sets->comm, sets->flags, 0, out_wcrt, nullptr, nullptr,
+  return launch_analyze(sets->rec, n, sets->comm, sets->flags & ~PAAM_FLAG_VERDICT_ONLY, 0, out_wcrt, nullptr, nullptr,
                         const_cast<paam_sets*>(sets)->tickets + 17, (cudaStream_t)stream, out_decision);
 }
 
@@ -227,6 +230,8 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   if (rc) return rc;
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (batch->n_sets > sets->cap) return fail(PAAM_EINVAL, "paam_pack_analyze: handle capacity too small");
+  if ((batch->flags & PAAM_FLAG_VERDICT_ONLY) && out_wcrt)
+    return fail(PAAM_EINVAL, "paam_pack_analyze: PAAM_FLAG_VERDICT_ONLY writes no WCRTs (out_wcrt must be NULL)");
   if ((rc = use_device(sets))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (batch->mem == PAAM_MEM_HOST || batch->n_sets < 4096) {  // small or host batch: sequential

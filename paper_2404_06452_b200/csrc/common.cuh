@@ -17,7 +17,10 @@
 
 namespace paam {
 
-#ifndef PAAM_WARP_EMU
+#ifdef PAAM_WARP_EMU
+#define PAAM_COLD
+#else
+#define PAAM_COLD __noinline__  // rarely taken paths: kept out of the hot loop's instruction stream
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

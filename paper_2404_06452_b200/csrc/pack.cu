@@ -81,6 +81,29 @@ __device__ __forceinline__ uint32_t scan_excl(uint32_t v, int lane) {  // plain 
   return x - v;
 }
 
+// WFD unit assignment, per accelerator (PAAM_FLAG_WFD_UNITS; one lane, out of line: not the default path)
+__device__ PAAM_COLD void wfd_units(Scratch& s, uint32_t nac, uint32_t ncb, uint64_t cstart) {
+  for (uint32_t a = 0; a < nac; a++) {
+    uint32_t ni = 0;
+    for (uint32_t j = 0; j < ncb; j++) {
+      if (!s.bNa[j]) continue;
+      const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1, rk = s.rank_of[c];
+      const uint32_t q0 = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
+      uint64_t A = 0;
+      for (uint32_t q = q0; q < q0 + s.bNa[j]; q++) if (s.qAcc[q] == a) A += s.qA[q];
+      if (A) { s.wfdU[ni] = (A << 24) / s.rT[rk]; s.wfdCb[ni] = (uint8_t)j; ni++; }
+    }
+    wfd_place(ni, s.wfdU, s.aUnits[a], s.wfdOrder, s.wfdUnit);
+    for (uint32_t i = 0; i < ni; i++) {
+      const uint32_t j = s.wfdCb[i];
+      const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1, rk = s.rank_of[c];
+      const uint32_t q0 = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
+      for (uint32_t q = q0; q < q0 + s.bNa[j]; q++)
+        if (s.qAcc[q] == a) s.qUnit[q] = (uint8_t)(s.aUbase[a] + s.wfdUnit[i]);
+    }
+  }
+}
+
 #ifndef PACK_MINB
 #define PACK_MINB 8
 #endif
@@ -351,27 +374,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       }
     }
     __syncwarp();
-    if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) {  // WFD unit assignment, per accelerator
-      for (uint32_t a = 0; a < nac; a++) {
-        uint32_t ni = 0;
-        for (uint32_t j = 0; j < ncb; j++) {
-          if (!s.bNa[j]) continue;
-          const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1, rk = s.rank_of[c];
-          const uint32_t q0 = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
-          uint64_t A = 0;
-          for (uint32_t q = q0; q < q0 + s.bNa[j]; q++) if (s.qAcc[q] == a) A += s.qA[q];
-          if (A) { s.wfdU[ni] = (A << 24) / s.rT[rk]; s.wfdCb[ni] = (uint8_t)j; ni++; }
-        }
-        wfd_place(ni, s.wfdU, s.aUnits[a], s.wfdOrder, s.wfdUnit);
-        for (uint32_t i = 0; i < ni; i++) {
-          const uint32_t j = s.wfdCb[i];
-          const uint32_t c = __popcll(cstart & ((2ull << j) - 1)) - 1, rk = s.rank_of[c];
-          const uint32_t q0 = s.rA0[rk] + (s.bA0[j] - s.cA0[c]);
-          for (uint32_t q = q0; q < q0 + s.bNa[j]; q++)
-            if (s.qAcc[q] == a) s.qUnit[q] = (uint8_t)(s.aUbase[a] + s.wfdUnit[i]);
-        }
-      }
-    }
+    if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) wfd_units(s, nac, ncb, cstart);
     if (lane < (int)n_unit) {
       uint32_t a = 0;
       for (uint32_t x = 1; x < nac; x++) if (s.aUbase[x] <= (uint32_t)lane) a = x;

@@ -18,6 +18,7 @@ UNSCHED = (1 << 64) - 1
 PAAM_MEM_HOST, PAAM_MEM_DEVICE = 0, 1
 PAAM_FLAG_BLOCKING_SOUND = 0x1
 PAAM_FLAG_WFD_UNITS = 0x2
+PAAM_FLAG_VERDICT_ONLY = 0x4
 PAAM_SIM_FIFO_DIRECT = 0x1
 SET_STATUS = {0: "OK", 1: "ERANGE", 2: "EDANGLING", 3: "EACCEL", 4: "ESHAPE", 5: "EDUPPRIO",
               6: "EDEADLINE", 7: "ECORE"}

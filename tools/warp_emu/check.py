@@ -35,6 +35,12 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     L.emu_analyze(rec.ctypes.data, n, hb.c.comm_cost, hb.c.flags, hb.c.n_bins if hb.c.set_bin else 0,
                   w.ctypes.data, sc.ctypes.data, bins.ctypes.data if hb.c.set_bin else None)
     out = dict(status=st[:n], wcrt=w[:hb.c.n_chains], sched=sc[:n], bins=bins[:2 * hb.c.n_bins])
+    # PAAM_FLAG_VERDICT_ONLY (0x4): no WCRTs, early exit at the first CRITICAL miss; same verdicts / bins
+    sv = np.zeros(max(n, 1), np.uint8)
+    bv = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
+    L.emu_analyze(rec.ctypes.data, n, hb.c.comm_cost, hb.c.flags | 0x4, hb.c.n_bins if hb.c.set_bin else 0,
+                  None, sv.ctypes.data, bv.ctypes.data if hb.c.set_bin else None)
+    out.update(sched_v=sv[:n], bins_v=bv[:2 * hb.c.n_bins])
     if horizon is not None:
         resp = np.zeros(nch, np.uint64)
         cnt = np.zeros(nch, np.uint64)
@@ -50,6 +56,7 @@ def compare(batch, horizon=None, seed=0, first=0, label="", fifo=False):
     e = emu_run(batch, horizon, seed, first, fifo)
     ow, osch, ost, ob = O.analyze(batch)
     ok = np.array_equal(ost, e["status"]) and np.array_equal(ow, e["wcrt"]) and np.array_equal(osch, e["sched"])
+    ok = ok and np.array_equal(osch, e["sched_v"]) and np.array_equal(e["bins"], e["bins_v"])
     msg = [f"{label}: analyze {'OK' if ok else 'MISMATCH'}"]
     if not ok:
         bad = np.nonzero(ow != e["wcrt"])[0][:5]
