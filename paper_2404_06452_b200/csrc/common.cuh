@@ -6,6 +6,7 @@
 // An unbounded Lemma-2 value (UNB) is represented by SAT as well: min(SAT, C) behaves exactly like
 // the paper's min(UNB, C) because any C >= SAT is itself above the cutoff.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #ifdef PAAM_WARP_EMU
 #include "../../tools/warp_emu/emu.h"  // host-side debugging emulation of the warp intrinsics
@@ -128,6 +129,7 @@ struct __align__(16) Record {
   uint32_t aMisc[MAXA];   // rank | unit << 8 | sub << 16 | callback << 24
 };
 static_assert(sizeof(Record) % 16 == 0, "record must be 16-byte aligned");
+static_assert(offsetof(Record, W) % 16 == 0, "W rows are copied as 16-byte vectors");
 
 // ---- launch bookkeeping ---------------------------------------------------------------------------
 #ifndef PAAM_WARP_EMU

@@ -30,7 +30,6 @@ struct Scratch {
   uint8_t rCls[MAXC], rIdx[MAXC], rNcb[MAXC], rNa[MAXC];
   uint8_t rank_of[MAXC];  // chain index -> rank
   uint32_t cA0[MAXC];     // chain index -> first accelerator segment in callback order
-  uint8_t bucket[MAXC][4];
   // callbacks (set-local order)
   uint32_t bE[MAXCB];
   uint8_t bExec[MAXCB], bNa[MAXCB], bA0[MAXCB + 1], bSub[MAXCB], bFa[MAXCB], bFu[MAXCB];
@@ -44,9 +43,8 @@ struct Scratch {
   uint8_t xCore[MAXX], xWait[MAXX], xPPrank[MAXX];
   // accelerators
   uint32_t aN[4], aUnits[4], aUbase[4], aEps[4], aKeff[4], aServer[4];
-  uint8_t unitAcc[MAXU];
   // per (rank, unit) / (unit, rank)
-  uint32_t W[MAXC][MAXU];
+  alignas(16) uint32_t W[MAXC][MAXU];
   uint32_t maxA[MAXU][MAXC];
   union {  // WFD scratch is dead before pre2 is computed
     uint32_t pre2[MAXU][MAXC];
@@ -213,10 +211,10 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
             erange |= (w >= LIM);
             eshape |= (kind > 1) || (w == 0) || (kind == prev_kind);
             prev_kind = kind;
-            if (kind == 0) E = sadd(E, (uint32_t)min(w, (uint64_t)SAT));
+            if (kind == 0) E = sadd(E, (uint32_t)w);  // w < LIM in a valid set: E stays exact
             if (kind == 1) {
               const uint32_t a = b.seg_accel[k], u = b.seg_unit[k];
-              if (na == 0) { fa = a; fu = u; fw = (uint32_t)min(w, (uint64_t)SAT); }
+              if (na == 0) { fa = a; fu = u; fw = (uint32_t)w; }
               na++;
               if (a >= nac) eaccel = true;
               else edang |= (u >= s.aUnits[a]);
@@ -250,14 +248,12 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       }
       // chain ranks and duplicate priorities
       {
-        uint32_t rk = 0, eq = 0;
-        for (uint32_t d = 0; d < nch; d++) {
-          const uint32_t pd = __shfl_sync(FULL, prio, d);
-          rk += (pd > prio);
-          eq += (pd == prio);
-        }
+        uint32_t rk = 0;
+        for (uint32_t d = 0; d < nch; d++) rk += (__shfl_sync(FULL, prio, d) > prio);
         rank = rk;
-        edup |= (lane < nch && eq > 1);
+        const uint32_t valid = nch >= 32 ? FULL : (1u << nch) - 1u;
+        const uint32_t same = __match_any_sync(FULL, prio) & valid & ~(1u << lane);
+        edup |= (lane < nch && same != 0);
       }
       // executors: duplicate (core, priority) and process-priority rank on the core; R1 (ECORE)
       {  // executors sharing a core are found by match; only those are compared
@@ -375,25 +371,20 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     }
     __syncwarp();
     if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) wfd_units(s, nac, ncb, cstart);
-    if (lane < (int)n_unit) {
-      uint32_t a = 0;
-      for (uint32_t x = 1; x < nac; x++) if (s.aUbase[x] <= (uint32_t)lane) a = x;
-      s.unitAcc[lane] = (uint8_t)a;
-    }
     __syncwarp();
     // ---- per chain (lane = rank): W[k][u], max A*[u][k], accelerator use mask ------------------------
     uint32_t use = 0;
+    for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
     if (is_chain) {
       const uint32_t k = lane;
-      for (uint32_t u = 0; u < n_unit; u++) { s.W[k][u] = 0; s.maxA[u][k] = 0; }
+      reinterpret_cast<uint4*>(s.W[k])[0] = uint4{0u, 0u, 0u, 0u};
+      reinterpret_cast<uint4*>(s.W[k])[1] = uint4{0u, 0u, 0u, 0u};
       for (uint32_t q = s.rA0[k]; q < s.rA0[k] + s.rNa[k]; q++) {
         const uint32_t u = s.qUnit[q], a = s.qAstar[q];
         use |= 1u << s.qAcc[q];
         s.maxA[u][k] = max(s.maxA[u][k], a);
         s.W[k][u] = sadd(s.W[k][u], a);  // saturating sums are exact (associative on [0, SAT])
       }
-    } else {
-      for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
     }
     __syncwarp();
     if (!st3) { psg = b.cb_seg_off[pcb]; st3 = true; }
@@ -405,8 +396,8 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       const uint32_t ginv = (1u << 16) / g + 1u;  // (p * ginv) >> 16 == p / g for p < 64, g <= 32
       const bool user = (U >> lane) & 1u;
       const uint32_t p = __popc(U & lt);  // position among users in rank order
-      if (is_chain) s.bucket[lane][a] = user ? (uint8_t)(n - 1 - ((p * ginv) >> 16)) : (uint8_t)0xFF;
-      // users of a form aligned blocks of g consecutive positions, one block per bucket
+      // users of a form aligned blocks of g consecutive positions, one block per bucket: the user at
+      // position p is in bucket n - 1 - p / g (A5)
       const uint32_t blk_end = min(((((uint32_t)lane * ginv) >> 16) + 1) * g, ma);
       for (uint32_t u = s.aUbase[a]; u < s.aUbase[a] + s.aUnits[a]; u++) {
         if (user) s.cmp[p] = s.maxA[u][lane];
