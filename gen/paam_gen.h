@@ -279,6 +279,23 @@ PG_FN void pg_generate_set(const pg_params* p, uint64_t seed, uint64_t index, pg
   s->n_seg = nseg;
 }
 
+/* The sizes pg_generate_set produces for set `index` -- {chains, callbacks, segments, executors,
+ * accelerators} -- from the same draws (m, and the CPU-only coin of every callback), without
+ * generating the rest of the set.  Checked against pg_generate_set by tests/test_generator.py. */
+PG_FN void pg_set_sizes(const pg_params* p, uint64_t seed, uint64_t index, uint32_t out[5]) {
+  const uint64_t key = pg_key(seed, index);
+  const uint32_t K = p->cbs_per_chain;
+  const uint32_t m = p->m_lo + pg_bounded(pg_draw(key, PG_D_M, 0), p->m_hi - p->m_lo + 1);
+  uint32_t nseg = 0;
+  for (uint32_t cb = 0; cb < m * K; cb++)
+    nseg += (p->cpu_only_frac_q16 && pg_coin(pg_draw(key, PG_D_CPUONLY, cb), p->cpu_only_frac_q16)) ? 1u : 3u;
+  out[0] = m;
+  out[1] = m * K;
+  out[2] = nseg;
+  out[3] = p->exec_mode == 0 ? m : p->n_exec;
+  out[4] = p->n_accel;
+}
+
 /* Flat CSR raw-batch arrays (same meaning as paam_batch in include/paam.h). */
 typedef struct {
   uint32_t *set_chain_off, *set_exec_off, *set_accel_off;      /* [n+1] */

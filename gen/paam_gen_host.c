@@ -7,15 +7,29 @@
 /* Totals of sets [first, first+n): out[0..4] = chains, callbacks, segments, executors, accelerators. */
 int pg_batch_totals(const pg_params* p, uint64_t seed, uint64_t first, uint32_t n, uint64_t* out) {
   if (!p || !out || pg_check_params(p)) return -1;
-  pg_set* s = (pg_set*)malloc(sizeof(pg_set));
-  if (!s) return -2;
   for (int k = 0; k < 5; k++) out[k] = 0;
   for (uint32_t i = 0; i < n; i++) {
+    uint32_t z[5];
+    pg_set_sizes(p, seed, first + i, z);
+    for (int k = 0; k < 5; k++) out[k] += z[k];
+  }
+  return 0;
+}
+
+/* Number of sets in [first, first+n) whose pg_set_sizes differ from pg_generate_set's (tests: 0). */
+int64_t pg_sizes_mismatch(const pg_params* p, uint64_t seed, uint64_t first, uint32_t n) {
+  if (!p || pg_check_params(p)) return -1;
+  pg_set* s = (pg_set*)malloc(sizeof(pg_set));
+  if (!s) return -2;
+  int64_t bad = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    uint32_t z[5];
     pg_generate_set(p, seed, first + i, s);
-    out[0] += s->m; out[1] += s->n_cb; out[2] += s->n_seg; out[3] += s->n_exec; out[4] += s->n_accel;
+    pg_set_sizes(p, seed, first + i, z);
+    bad += (z[0] != s->m || z[1] != s->n_cb || z[2] != s->n_seg || z[3] != s->n_exec || z[4] != s->n_accel);
   }
   free(s);
-  return 0;
+  return bad;
 }
 
 /* Fill caller-allocated arrays (sizes from pg_batch_totals), including the offset sentinels. */

@@ -156,6 +156,11 @@ typedef struct paam_sets paam_sets;
  * caps.  *out receives a handle; paam_raw_batch() exposes its arrays as a paam_batch (mem = DEVICE). */
 int paam_generate(const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
                   uint64_t comm_cost, uint32_t flags, paam_raw** out, paam_stream_t stream);
+/* paam_regenerate -- paam_generate into an existing handle (for timed loops): its device buffers are
+ * reused when the new batch fits them (else they grow).  Same arguments and errors as paam_generate;
+ * previously obtained paam_raw_batch views of the handle become invalid. */
+int paam_regenerate(paam_raw* raw, const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
+                    uint64_t comm_cost, uint32_t flags, paam_stream_t stream);
 int paam_raw_batch(const paam_raw* raw, paam_batch* out);
 void paam_raw_free(paam_raw* raw);
 

@@ -1,10 +1,15 @@
 // generate.cu -- §8(a) step 1: device-side synthetic chain-set generation (paam_generate).
 //
-// Runs the shared counter-based generator gen/paam_gen.h (input generation only -- it holds none of
-// the analysed method) on the device, one thread per set: pass 1 sizes every set, five exclusive
-// scans turn the sizes into CSR offsets, pass 2 regenerates each set and writes it at its offsets.
-// Every set is a pure function of (seed, global index), so ranks generate disjoint index ranges
-// with no communication, and the bytes equal the host generator's (tests/test_gpu_parity.py).
+// The workload recipe is gen/paam_gen.h (input generation only -- it holds none of the analysed
+// method).  Pass 1 sizes every set (pg_set_sizes: only the draws that decide sizes, one thread per
+// set), five exclusive scans turn the sizes into CSR offsets, and pass 2 writes every set at its
+// offsets.  Pass 2 is a warp-per-set re-implementation of pg_generate_set + pg_write_set: the same
+// counter-based draws (each a pure function of (seed, set, purpose, index)) and the same integer
+// steps, spread over lanes (lane = chain, lane = callback, lane = executor) so that the writes are
+// coalesced and no per-thread set image lives in local memory; the short inherently sequential
+// steps (Fisher-Yates swaps, worst-fit placement) run on lane 0 over shared memory.  The bytes equal
+// the host generator's (tests/test_gpu_parity.py::test_device_generator_matches_host_bytes).
+// Ranks generate disjoint index ranges with no communication.
 #include <cstdlib>
 #include <cstring>
 
@@ -13,8 +18,10 @@
 
 struct paam_raw {
   paam_batch b;
-  void* buf;
+  void* buf;       // every array of the batch (capacity `bytes`)
   size_t bytes;
+  void* scr;       // sizes / offsets / scan scratch (capacity `scr_bytes`)
+  size_t scr_bytes;
   int device;
 };
 
@@ -24,25 +31,235 @@ namespace {
 __global__ void gen_sizes_kernel(pg_params p, uint64_t seed, uint64_t first, uint32_t n, uint32_t* __restrict__ cnt) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  pg_set s;
-  pg_generate_set(&p, seed, first + i, &s);
-  cnt[0 * (size_t)n + i] = s.m;
-  cnt[1 * (size_t)n + i] = s.n_cb;
-  cnt[2 * (size_t)n + i] = s.n_seg;
-  cnt[3 * (size_t)n + i] = s.n_exec;
-  cnt[4 * (size_t)n + i] = s.n_accel;
+  uint32_t z[5];
+  pg_set_sizes(&p, seed, first + i, z);
+#pragma unroll
+  for (int k = 0; k < 5; k++) cnt[k * (size_t)n + i] = z[k];
 }
 
-__global__ void gen_fill_kernel(pg_params p, uint64_t seed, uint64_t first, uint32_t n, pg_arrays o,
-                                const uint32_t* __restrict__ cb_off, const uint32_t* __restrict__ sg_off) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  pg_set s;
-  pg_generate_set(&p, seed, first + i, &s);
-  pg_write_set(&s, i, o.set_chain_off[i], cb_off[i], sg_off[i], o.set_exec_off[i], o.set_accel_off[i], &o);
-  if (i == n - 1) {  // CSR sentinels
-    o.chain_cb_off[o.set_chain_off[n]] = cb_off[n];
-    o.cb_seg_off[cb_off[n]] = sg_off[n];
+constexpr int GW = 4;  // warps per block of the fill kernel
+constexpr uint32_t FULL = 0xffffffffu;
+
+struct GenWarp {
+  uint64_t ccpu[PG_MAX_CHAINS];   // CPU WCET per chain
+  uint64_t util[PG_MAX_CHAINS];   // CPU utilisation (Q20) per chain
+  uint64_t load[32];              // worst-fit loads (cores or executors)
+  uint32_t sorted[PG_MAX_CHAINS]; // sorted cut points
+  uint32_t prio[PG_MAX_CHAINS];
+  uint32_t pk[PG_MAX_CHAINS];     // Fisher-Yates draw of step j
+  uint8_t order[PG_MAX_CHAINS];   // chains by utilisation desc, index asc
+  uint8_t best[PG_MAX_CHAINS], second[PG_MAX_CHAINS], split[PG_MAX_CHAINS];
+};
+
+// Warp-per-set generation; mirrors pg_generate_set + pg_write_set step for step (same draws, same
+// integer expressions, same tie rules).
+__global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t seed, uint64_t first, uint32_t n,
+                                                        pg_arrays o, const uint32_t* __restrict__ cb_off,
+                                                        const uint32_t* __restrict__ sg_off) {
+  __shared__ GenWarp smem[GW];
+  GenWarp& w = smem[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t K = p.cbs_per_chain;
+  const uint32_t units[PG_MAX_ACCEL] = {p.units[0], p.units[1], p.units[2], p.units[3]};
+  for (uint32_t i = blockIdx.x * GW + (threadIdx.x >> 5); i < n; i += gridDim.x * GW) {
+    const uint64_t index = first + i;
+    const uint64_t key = pg_key(seed, index);
+    const uint32_t bin = p.n_bins ? (uint32_t)(index % p.n_bins) : 0u;
+    const uint64_t U = (uint64_t)p.u_lo_q20 + (uint64_t)bin * p.u_step_q20;
+    const uint32_t m = p.m_lo + pg_bounded(pg_draw(key, PG_D_M, 0), p.m_hi - p.m_lo + 1);
+    const bool isc = lane < m;
+    const uint32_t ch0 = o.set_chain_off[i], cb0 = cb_off[i], sg0 = sg_off[i];
+    const uint32_t ex0 = o.set_exec_off[i], ac0 = o.set_accel_off[i];
+
+    // per-chain utilisation: the m-1 cut points, sorted (equal cut values are interchangeable)
+    const bool iscut = lane + 1 < m;
+    const uint32_t cutv = iscut ? pg_bounded(pg_draw(key, PG_D_CUT, lane), (uint32_t)U + 1u) : 0u;
+    {
+      uint32_t rk = 0;
+      for (uint32_t j = 0; j + 1 < m; j++) {
+        const uint32_t cj = __shfl_sync(FULL, cutv, j);
+        rk += (cj < cutv) || (cj == cutv && j < lane);
+      }
+      if (iscut) w.sorted[rk] = cutv;
+      if (isc) w.ccpu[lane] = 0;
+    }
+    __syncwarp();
+    uint64_t share = 0, T = 0;
+    if (isc) {
+      const uint64_t hi = iscut ? (uint64_t)w.sorted[lane] : U;
+      share = hi - (lane > 0 ? (uint64_t)w.sorted[lane - 1] : 0ull);
+      // log-uniform period rounded to 1 us; D = T
+      const uint32_t x = pg_bounded(pg_draw(key, PG_D_PERIOD, lane), p.period_span_q12 + 1);
+      const uint32_t oct = x >> 12, frac = x & 4095u;
+      uint64_t t_us = (((uint64_t)p.period_min_us * PG_TABLE(frac)) << oct) >> 30;
+      if (t_us < 1) t_us = 1;
+      T = t_us * 1000ull;
+    }
+    const uint64_t C = (share * T) >> 20;
+    const uint64_t base = C / K, rem = C % K;
+
+    // callbacks (lane = callback, passes of 32): budget, segments, accelerator and unit draws
+    const uint32_t ncb = m * K;
+    uint32_t carry = 0;
+    for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
+      const uint32_t cb = pass * 32 + lane;
+      const bool iscb = cb < ncb;
+      const uint32_t c = iscb ? cb / K : 0u, j = iscb ? cb - c * K : 0u;
+      const uint64_t bc = __shfl_sync(FULL, base, c), rc = __shfl_sync(FULL, rem, c);
+      const uint64_t budget = bc + (j < rc ? 1 : 0);
+      uint32_t nseg = 0, acc = 0, unit = 0;
+      uint64_t w0 = 0, w1 = 0, w2 = 0;
+      if (iscb) {
+        if (p.cpu_only_frac_q16 && pg_coin(pg_draw(key, PG_D_CPUONLY, cb), p.cpu_only_frac_q16)) {
+          nseg = 1;
+          w0 = budget ? budget : 1;
+          atomicAdd((unsigned long long*)&w.ccpu[c], (unsigned long long)w0);
+        } else {
+          uint64_t A = budget * p.ratio_acc / (p.ratio_acc + p.ratio_cpu);
+          uint64_t E = budget - A;
+          uint64_t e1 = E / 2, e2 = E - E / 2;
+          nseg = 3;
+          w0 = e1 ? e1 : 1;
+          w1 = A ? A : 1;
+          w2 = e2 ? e2 : 1;
+          acc = pg_bounded(pg_draw(key, PG_D_ACC, cb), p.n_accel);
+          unit = pg_bounded(pg_draw(key, PG_D_UNIT, cb), units[acc]);
+          atomicAdd((unsigned long long*)&w.ccpu[c], (unsigned long long)(w0 + w2));
+        }
+      }
+      uint32_t incl = nseg;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= (uint32_t)d) incl += y;
+      }
+      const uint32_t sg = sg0 + carry + incl - nseg;
+      carry += __shfl_sync(FULL, incl, 31);
+      if (iscb) {
+        o.cb_seg_off[cb0 + cb] = sg;
+        if (nseg == 1) {
+          o.seg_kind[sg] = 0; o.seg_wcet[sg] = w0; o.seg_accel[sg] = 0; o.seg_unit[sg] = 0;
+        } else {
+          o.seg_kind[sg] = 0; o.seg_wcet[sg] = w0; o.seg_accel[sg] = 0; o.seg_unit[sg] = 0;
+          o.seg_kind[sg + 1] = 1; o.seg_wcet[sg + 1] = w1; o.seg_accel[sg + 1] = (uint8_t)acc; o.seg_unit[sg + 1] = (uint8_t)unit;
+          o.seg_kind[sg + 2] = 0; o.seg_wcet[sg + 2] = w2; o.seg_accel[sg + 2] = 0; o.seg_unit[sg + 2] = 0;
+        }
+      }
+    }
+    __syncwarp();
+
+    // unique priorities: rate-monotonic, or the CAPA-random Fisher-Yates permutation
+    uint32_t prio = 0;
+    if (p.rm_priorities) {
+      uint32_t rank = 0;
+      for (uint32_t d = 0; d < m; d++) {
+        const uint64_t Td = __shfl_sync(FULL, T, d);
+        rank += (Td < T) || (Td == T && d < lane);
+      }
+      prio = m - rank;
+    } else {
+      if (isc) {
+        w.prio[lane] = lane + 1;
+        w.pk[lane] = lane >= 1 ? pg_bounded(pg_draw(key, PG_D_PERM, lane), lane + 1) : 0u;
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (uint32_t j = m - 1; j >= 1; j--) {
+          const uint32_t k = w.pk[j], t = w.prio[j];
+          w.prio[j] = w.prio[k];
+          w.prio[k] = t;
+        }
+      __syncwarp();
+      prio = isc ? w.prio[lane] : 0u;
+    }
+    const uint32_t n_be = (uint32_t)(((uint64_t)m * p.be_frac_q16) >> 16);
+
+    // CPU utilisation and the worst-fit order (utilisation desc, index asc)
+    const uint64_t util = isc ? (w.ccpu[lane] << 20) / T : 0ull;
+    {
+      uint32_t rk = 0;
+      for (uint32_t d = 0; d < m; d++) {
+        const uint64_t ud = __shfl_sync(FULL, util, d);
+        rk += (ud > util) || (ud == util && d < lane);
+      }
+      if (isc) { w.order[rk] = (uint8_t)lane; w.util[lane] = util; }
+    }
+    __syncwarp();
+    uint32_t n_exec, n_client;
+    if (p.exec_mode == 0) {  // one executor per chain, worst-fit onto the client cores
+      if (lane == 0) {
+        for (uint32_t k = 0; k < p.n_cores; k++) w.load[k] = 0;
+        for (uint32_t jj = 0; jj < m; jj++) {
+          const uint32_t c = w.order[jj];
+          uint32_t best = 0;
+          for (uint32_t k = 1; k < p.n_cores; k++) if (w.load[k] < w.load[best]) best = k;
+          w.load[best] += w.util[c];
+          w.best[c] = (uint8_t)best;
+        }
+      }
+      n_exec = m;
+      n_client = p.n_cores;
+    } else {  // n_exec single-threaded executors on their own cores; some chains split across two
+      const uint32_t X = p.n_exec;
+      if (lane == 0) {
+        for (uint32_t x = 0; x < X; x++) w.load[x] = 0;
+        for (uint32_t jj = 0; jj < m; jj++) {
+          const uint32_t c = w.order[jj];
+          uint32_t best = 0;
+          for (uint32_t x = 1; x < X; x++) if (w.load[x] < w.load[best]) best = x;
+          const int split = p.xexec_frac_q16 && K >= 2 && pg_coin(pg_draw(key, PG_D_XEXEC, c), p.xexec_frac_q16);
+          w.best[c] = (uint8_t)best;
+          w.split[c] = (uint8_t)split;
+          if (!split) {
+            w.load[best] += w.util[c];
+          } else {
+            uint32_t second = (best == 0) ? 1 : 0;
+            for (uint32_t x = 0; x < X; x++) if (x != best && w.load[x] < w.load[second]) second = x;
+            w.second[c] = (uint8_t)second;
+            w.load[best] += w.util[c] / 2;
+            w.load[second] += w.util[c] - w.util[c] / 2;
+          }
+        }
+      }
+      n_exec = X;
+      n_client = X;
+    }
+    __syncwarp();
+
+    // ---- writes (coalesced by lane) ----
+    if (lane == 0 && o.set_bin) o.set_bin[i] = bin;
+    if (isc) {
+      o.chain_T[ch0 + lane] = T;
+      o.chain_D[ch0 + lane] = T;
+      o.chain_prio[ch0 + lane] = prio;
+      o.chain_class[ch0 + lane] = (prio <= n_be) ? 1 : 0;
+      o.chain_cb_off[ch0 + lane] = cb0 + lane * K;
+    }
+    for (uint32_t cb = lane; cb < ncb; cb += 32) {
+      const uint32_t c = cb / K, j = cb - c * K;
+      uint32_t x;
+      if (p.exec_mode == 0) x = c;
+      else x = (w.split[c] && j >= (K + 1) / 2) ? w.second[c] : w.best[c];
+      o.cb_exec[cb0 + cb] = (uint16_t)x;
+    }
+    if (lane < n_exec) {
+      const uint32_t pr = (p.exec_mode == 0) ? prio : lane + 1;
+      o.exec_core[ex0 + lane] = (p.exec_mode == 0) ? w.best[lane] : (uint8_t)lane;
+      o.exec_prio[ex0 + lane] = pr;
+      o.exec_wait[ex0 + lane] = (uint8_t)(p.spin_frac_q16 && pg_coin(pg_draw(key, PG_D_SPIN, lane), p.spin_frac_q16));
+    }
+    if (lane < p.n_accel) {
+      o.accel_buckets[ac0 + lane] = (uint8_t)p.buckets[lane];
+      o.accel_units[ac0 + lane] = (uint8_t)units[lane];
+      o.accel_server_core[ac0 + lane] = (uint8_t)(n_client + lane);
+      o.accel_eps[ac0 + lane] = p.eps[lane];
+      o.accel_kappa[ac0 + lane] = p.kappa[lane];
+    }
+    if (i == n - 1 && lane == 0) {  // CSR sentinels
+      o.chain_cb_off[o.set_chain_off[n]] = cb_off[n];
+      o.cb_seg_off[cb_off[n]] = sg_off[n];
+    }
+    __syncwarp();
   }
 }
 
@@ -126,28 +343,26 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 using namespace paam;
 
-extern "C" int paam_generate(const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
-                             uint64_t comm_cost, uint32_t flags, paam_raw** out, paam_stream_t stream) {
-  static_assert(sizeof(paam_gen_params) == sizeof(pg_params), "paam_gen_params must mirror pg_params");
-  if (!params || !out) return fail(PAAM_EINVAL, "paam_generate: NULL argument");
-  *out = nullptr;
-  pg_params p;
-  std::memcpy(&p, params, sizeof(p));
-  if (pg_check_params(&p)) return fail(PAAM_EINVAL, "paam_generate: generator parameters out of range");
-  if (comm_cost >= LIM) return fail(PAAM_EINVAL, "paam_generate: comm_cost >= 2^31 - 1");
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e;
+namespace paam {
+namespace {
 
-  // pass 1: sizes, then offsets
-  uint32_t *cnt = nullptr, *offs = nullptr, *tmp = nullptr;
+// Generate into `raw`, reusing its device buffers when the new batch fits (paam_regenerate).
+int generate_into(paam_raw* raw, const pg_params& p, uint64_t seed, uint64_t first_index, uint32_t n,
+                  uint64_t comm_cost, uint32_t flags, cudaStream_t st) {
+  cudaError_t e;
+  // pass 1: sizes, then offsets (scratch: cnt[5n], offs[5(n+1)], scan temporaries)
   const size_t nn = (size_t)n + 1;
-  const size_t tw = scan_tmp_words(n);
-  if ((e = cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * 5 * (size_t)(n ? n : 1), st)) != cudaSuccess)
-    return fail_cuda(e, "paam_generate: cudaMallocAsync");
-  if ((e = cudaMallocAsync((void**)&offs, sizeof(uint32_t) * 5 * nn, st)) != cudaSuccess)
-    return fail_cuda(e, "paam_generate: cudaMallocAsync");
-  if ((e = cudaMallocAsync((void**)&tmp, sizeof(uint32_t) * tw, st)) != cudaSuccess)
-    return fail_cuda(e, "paam_generate: cudaMallocAsync");
+  const size_t scr_words = 5 * (size_t)(n ? n : 1) + 5 * nn + scan_tmp_words(n);
+  if (raw->scr_bytes < 4 * scr_words) {
+    if (raw->scr) cudaFree(raw->scr);
+    raw->scr = nullptr;
+    raw->scr_bytes = 0;
+    if ((e = cudaMalloc(&raw->scr, 4 * scr_words)) != cudaSuccess) return fail_cuda(e, "paam_generate: scratch cudaMalloc");
+    raw->scr_bytes = 4 * scr_words;
+  }
+  uint32_t* cnt = (uint32_t*)raw->scr;
+  uint32_t* offs = cnt + 5 * (size_t)(n ? n : 1);
+  uint32_t* tmp = offs + 5 * nn;
   if (n) {
     gen_sizes_kernel<<<(n + 127) / 128, 128, 0, st>>>(p, seed, first_index, n, cnt);
     count_launch();
@@ -171,11 +386,13 @@ extern "C" int paam_generate(const paam_gen_params* params, uint64_t seed, uint6
   constexpr int NP = sizeof(parts) / sizeof(parts[0]);
   size_t off[NP], bytes = 0;
   for (int i = 0; i < NP; i++) { off[i] = bytes; bytes += align256(parts[i].elems * parts[i].size + 1); }
-  paam_raw* raw = (paam_raw*)std::calloc(1, sizeof(paam_raw));
-  if (!raw) return fail(PAAM_ENOMEM, "paam_generate: host allocation");
-  if ((e = cudaMalloc(&raw->buf, bytes)) != cudaSuccess) { std::free(raw); return fail_cuda(e, "paam_generate: cudaMalloc"); }
-  raw->bytes = bytes;
-  cudaGetDevice(&raw->device);
+  if (raw->bytes < bytes) {
+    if (raw->buf) cudaFree(raw->buf);
+    raw->buf = nullptr;
+    raw->bytes = 0;
+    if ((e = cudaMalloc(&raw->buf, bytes)) != cudaSuccess) return fail_cuda(e, "paam_generate: cudaMalloc");
+    raw->bytes = bytes;
+  }
   char* base = (char*)raw->buf;
   pg_arrays o;
   void** slots[NP] = {(void**)&o.set_chain_off, (void**)&o.set_exec_off, (void**)&o.set_accel_off,
@@ -186,20 +403,23 @@ extern "C" int paam_generate(const paam_gen_params* params, uint64_t seed, uint6
                       (void**)&o.accel_buckets, (void**)&o.accel_units, (void**)&o.accel_server_core,
                       (void**)&o.accel_eps, (void**)&o.accel_kappa, (void**)&o.set_bin};
   for (int i = 0; i < NP; i++) *slots[i] = base + off[i];
+  if (!p.n_bins) o.set_bin = nullptr;
   cudaMemcpyAsync(o.set_chain_off, offs + 0 * nn, nn * 4, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(o.set_exec_off, offs + 3 * nn, nn * 4, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(o.set_accel_off, offs + 4 * nn, nn * 4, cudaMemcpyDeviceToDevice, st);
   if (n) {
-    gen_fill_kernel<<<(n + 127) / 128, 128, 0, st>>>(p, seed, first_index, n, o, offs + 1 * nn, offs + 2 * nn);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gen_fill_kernel, GW * 32, 0);
+    const uint32_t need = (n + GW - 1) / GW, cap = (uint32_t)sms * (uint32_t)(per_sm > 0 ? per_sm : 1);
+    gen_fill_kernel<<<need < cap ? need : cap, GW * 32, 0, st>>>(p, seed, first_index, n, o, offs + 1 * nn, offs + 2 * nn);
     count_launch();
   } else {
     cudaMemsetAsync(o.chain_cb_off, 0, 4, st);
     cudaMemsetAsync(o.cb_seg_off, 0, 4, st);
   }
-  cudaFreeAsync(cnt, st);
-  cudaFreeAsync(offs, st);
-  cudaFreeAsync(tmp, st);
-  if ((e = cudaGetLastError()) != cudaSuccess) { cudaFree(raw->buf); std::free(raw); return fail_cuda(e, "paam_generate: fill"); }
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "paam_generate: fill");
 
   paam_batch& b = raw->b;
   std::memset(&b, 0, sizeof(b));
@@ -214,11 +434,49 @@ extern "C" int paam_generate(const paam_gen_params* params, uint64_t seed, uint6
   b.exec_core = o.exec_core; b.exec_prio = o.exec_prio; b.exec_wait = o.exec_wait;
   b.accel_buckets = o.accel_buckets; b.accel_units = o.accel_units; b.accel_server_core = o.accel_server_core;
   b.accel_eps = o.accel_eps; b.accel_kappa = o.accel_kappa;
-  b.set_bin = p.n_bins ? o.set_bin : nullptr;
+  b.set_bin = o.set_bin;
   b.comm_cost = comm_cost;
   b.flags = flags;
+  return PAAM_OK;
+}
+
+int check_gen_args(const paam_gen_params* params, uint64_t comm_cost, pg_params* p) {
+  static_assert(sizeof(paam_gen_params) == sizeof(pg_params), "paam_gen_params must mirror pg_params");
+  if (!params) return fail(PAAM_EINVAL, "paam_generate: NULL params");
+  std::memcpy(p, params, sizeof(*p));
+  if (pg_check_params(p)) return fail(PAAM_EINVAL, "paam_generate: generator parameters out of range");
+  if (comm_cost >= LIM) return fail(PAAM_EINVAL, "paam_generate: comm_cost >= 2^31 - 1");
+  return PAAM_OK;
+}
+
+}  // namespace
+}  // namespace paam
+
+extern "C" int paam_generate(const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
+                             uint64_t comm_cost, uint32_t flags, paam_raw** out, paam_stream_t stream) {
+  if (!out) return fail(PAAM_EINVAL, "paam_generate: NULL out");
+  *out = nullptr;
+  pg_params p;
+  if (int rc = check_gen_args(params, comm_cost, &p)) return rc;
+  paam_raw* raw = (paam_raw*)std::calloc(1, sizeof(paam_raw));
+  if (!raw) return fail(PAAM_ENOMEM, "paam_generate: host allocation");
+  cudaGetDevice(&raw->device);
+  if (int rc = generate_into(raw, p, seed, first_index, n, comm_cost, flags, (cudaStream_t)stream)) {
+    paam_raw_free(raw);
+    return rc;
+  }
   *out = raw;
   return PAAM_OK;
+}
+
+extern "C" int paam_regenerate(paam_raw* raw, const paam_gen_params* params, uint64_t seed, uint64_t first_index,
+                               uint32_t n, uint64_t comm_cost, uint32_t flags, paam_stream_t stream) {
+  if (!raw) return fail(PAAM_EINVAL, "paam_regenerate: NULL handle");
+  pg_params p;
+  if (int rc = check_gen_args(params, comm_cost, &p)) return rc;
+  cudaError_t e = cudaSetDevice(raw->device);
+  if (e != cudaSuccess) return fail_cuda(e, "paam_regenerate: cudaSetDevice");
+  return generate_into(raw, p, seed, first_index, n, comm_cost, flags, (cudaStream_t)stream);
 }
 
 extern "C" int paam_raw_batch(const paam_raw* raw, paam_batch* out) {
@@ -230,6 +488,7 @@ extern "C" int paam_raw_batch(const paam_raw* raw, paam_batch* out) {
 extern "C" void paam_raw_free(paam_raw* raw) {
   if (!raw) return;
   cudaSetDevice(raw->device);
-  cudaFree(raw->buf);
+  if (raw->buf) cudaFree(raw->buf);
+  if (raw->scr) cudaFree(raw->scr);
   std::free(raw);
 }

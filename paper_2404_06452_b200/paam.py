@@ -76,6 +76,8 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         L.paam_generate.argtypes = [ctypes.POINTER(PaamGenParams), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                     ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_vp), _vp]
+        L.paam_regenerate.argtypes = [_vp, ctypes.POINTER(PaamGenParams), ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _vp]
         L.paam_raw_batch.argtypes = [_vp, ctypes.POINTER(PaamBatch)]
         L.paam_raw_free.argtypes = [_vp]
         L.paam_raw_free.restype = None
@@ -191,6 +193,13 @@ class Raw:
         check(lib().paam_generate(ctypes.byref(params), seed, first, n, comm_cost, flags, ctypes.byref(self.h),
                                   _stream_ptr(stream)), "paam_generate")
         self.c = PaamBatch()
+        check(lib().paam_raw_batch(self.h, ctypes.byref(self.c)), "paam_raw_batch")
+
+    def regenerate(self, params: PaamGenParams, seed: int, first: int, n: int, comm_cost=100_000, flags=0,
+                   stream=None):
+        """paam_regenerate: generate into this handle, reusing its device buffers."""
+        check(lib().paam_regenerate(self.h, ctypes.byref(params), seed, first, n, comm_cost, flags,
+                                    _stream_ptr(stream)), "paam_regenerate")
         check(lib().paam_raw_batch(self.h, ctypes.byref(self.c)), "paam_raw_batch")
 
     @property

@@ -62,3 +62,14 @@ def test_null_arguments_rejected():
     L = paam.lib()
     assert L.paam_pack(None, None, None, None) == -1
     assert L.paam_analyze(None, 0, None, None, None, None) == -1
+
+
+def test_binding_surface():
+    """The thin binding exposes every entry point the tests and bench.py call (no GPU needed)."""
+    from paper_2404_06452_b200 import paam
+    for cls, names in ((paam.Raw, ("regenerate", "free", "to_host")),
+                       (paam.Sets, ("repack", "pack_analyze", "analyze", "admit", "simulate", "free")),
+                       (paam.Batch, ("from_host", "from_host_to_device"))):
+        for nm in names:
+            assert callable(getattr(cls, nm, None)), (cls.__name__, nm)
+    assert paam.PAAM_FLAG_VERDICT_ONLY == 0x4

@@ -69,3 +69,16 @@ def test_periods_log_uniform_range():
     # log-uniform on [2, 3]: each of 4 quarter-decades holds ~25%
     h, _ = np.histogram(lg, bins=4, range=(2, 3))
     assert np.all(np.abs(h / h.sum() - 0.25) < 0.03)
+
+
+def test_sizes_only_path_matches_full_generator():
+    """pg_set_sizes (used to size the CSR batch without generating the sets) == pg_generate_set's sizes."""
+    import ctypes
+    from gen.inputs import _genlib, config2_params, config3_params
+    lib = _genlib()
+    lib.pg_sizes_mismatch.restype = ctypes.c_int64
+    lib.pg_sizes_mismatch.argtypes = [ctypes.POINTER(type(make_params())), ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint32]
+    for p, seed in ((config3_params(), 3), (config2_params(0.25), 2), (make_params(exec_mode=1, xexec_frac=0.5), 8),
+                    (make_params(m_lo=1, m_hi=32, cbs_per_chain=2, cpu_only_frac=0.5), 5)):
+        assert lib.pg_sizes_mismatch(ctypes.byref(p), seed, 0, 5000) == 0

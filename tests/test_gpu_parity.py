@@ -144,15 +144,41 @@ def gen_gpu(p, seed, first, n):
     return paam.Raw(pp, seed, first, n)
 
 
+GEN_CASES = ((config3_params(), 3), (config2_params(0.25), 2), (make_params(exec_mode=1, xexec_frac=0.5), 8),
+             (make_params(rm=True, spin_frac=0.5), 9),                                   # rate-monotonic
+             (make_params(m_lo=1, m_hi=21, cbs_per_chain=3, cpu_only_frac=0.3), 10),     # K=3: passes straddle chains
+             (make_params(m_lo=32, m_hi=32, cbs_per_chain=2, n_cores=32, n_bins=0), 11),  # maximum m, no bins
+             (make_params(exec_mode=1, n_exec=32, xexec_frac=1.0, ratio_acc=3, ratio_cpu=1,
+                          accels=((6, 4, 391 * US, 130 * US), (1, 2, 391 * US, 0), (3, 8, 5, 7), (32, 1, 0, 0))), 12))
+
+
 def test_device_generator_matches_host_bytes():
-    for p, seed in ((config3_params(), 3), (config2_params(0.25), 2), (make_params(exec_mode=1, xexec_frac=0.5), 8)):
+    for p, seed in GEN_CASES:
         h = generate_host(p, seed, 1000, 5000)
         raw = gen_gpu(p, seed, 1000, 5000)
         d = raw.to_host()
         for k, v in h.items():
-            if isinstance(v, np.ndarray):
-                assert np.array_equal(v, d[k]), k
+            if k == "set_bin" and p.n_bins == 0:
+                assert d[k] is None  # no bins: the device batch has no bin array
+            elif isinstance(v, np.ndarray):
+                assert np.array_equal(v, d[k]), (k, seed)
         raw.free()
+
+
+def test_regenerate_reuses_handle():
+    p = config3_params()
+    pp = paam.PaamGenParams.from_buffer_copy(bytes(p))
+    raw = gen_gpu(p, 3, 0, 3000)
+    for first, n in ((100, 2000), (7, 9000), (0, 0), (5, 1)):  # shrink, grow, empty, one set
+        raw.regenerate(pp, 4, first, n)
+        d = raw.to_host()
+        h = generate_host(p, 4, first, n)
+        for k, v in h.items():
+            if k == "set_bin" and n == 0:
+                assert d[k] is None or len(d[k]) == 0
+            elif isinstance(v, np.ndarray):
+                assert np.array_equal(v, d[k]), (k, first, n)
+    raw.free()
 
 
 def test_device_pipeline_generate_pack_analyze_bins():
