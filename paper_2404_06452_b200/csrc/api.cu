@@ -21,7 +21,7 @@ struct paam_sets {
   paam_batch dev;    // the packed batch with device pointers (paam_simulate reads its structure)
   cudaStream_t side[2];  // internal streams of paam_pack_analyze (created on first use)
   cudaEvent_t ev[17];
-  unsigned int* tickets;  // work-distribution counters of the analyze launches (16 chunk slots + 1)
+  unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18
   int device;             // the CUDA device the handle lives on (made current by every call)
 };
 
@@ -221,7 +221,7 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
   if (sim_flags & ~(uint32_t)PAAM_SIM_FIFO_DIRECT) return fail(PAAM_EINVAL, "paam_simulate: unknown sim flag");
   if (int rc = use_device(sets)) return rc;
   return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
-                         bound, out_violations, (cudaStream_t)stream);
+                         bound, out_violations, const_cast<paam_sets*>(sets)->tickets + 18, (cudaStream_t)stream);
 }
 
 extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,

@@ -145,12 +145,19 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
                                                            uint32_t sim_flags, uint64_t* __restrict__ out_resp, uint64_t* __restrict__ out_count,
                                                            uint64_t* __restrict__ out_digest,
                                                            const uint64_t* __restrict__ bound,
-                                                           int64_t* __restrict__ out_viol) {
+                                                           int64_t* __restrict__ out_viol,
+                                                           unsigned int* __restrict__ ticket) {
   __shared__ DesSmem smem[SW];
   const uint32_t lane = threadIdx.x & 31;
   DesSmem& S = smem[threadIdx.x >> 5];
-  const uint32_t nwarps = gridDim.x * SW;
-  for (uint32_t set = blockIdx.x * SW + (threadIdx.x >> 5); set < n; set += nwarps) {
+  // dynamic work distribution: a set's simulation cost varies by orders of magnitude (chains,
+  // periods, horizon), so warps take one set per atomic ticket instead of a fixed stride
+  auto next_set = [&]() {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  for (uint32_t set = next_set(); set < n; set = next_set()) {
     const Record& rec = recs[set];
     const uint32_t c0 = b.set_chain_off[set], c1 = b.set_chain_off[set + 1];
     const uint32_t nch = c1 - c0;
@@ -627,8 +634,9 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
 #ifndef PAAM_WARP_EMU
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
                     uint64_t first_index, uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
-                    const uint64_t* bound, int64_t* out_viol, cudaStream_t st) {
+                    const uint64_t* bound, int64_t* out_viol, unsigned int* ticket, cudaStream_t st) {
   if (n == 0) return PAAM_OK;
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -638,7 +646,7 @@ int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
   simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
-                                           bound, out_viol);
+                                           bound, out_viol, ticket);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "simulate_kernel launch");
