@@ -322,7 +322,6 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
     for (;;) {
       // ===================== settle time t (D15) =====================
       for (;;) {
-        bool anyA = false;
         for (;;) {
           bool ch = false;
           // (1) units
@@ -417,7 +416,6 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           }
           __syncwarp();
           if (!__any_sync(FULL, ch)) break;
-          anyA = true;
         }
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
         bool chB = false;
@@ -461,14 +459,9 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           __syncwarp();
           chB = true;
         }
-        // (6) core dispatch (D5): highest process priority runnable executor per core
+        // (6) core dispatch (D5): highest process priority runnable executor per core.  ready_x is
+        // current: (5) recomputed it on every chain lane whose instance it started.
         {
-          ready_x = 0;
-          if (is_chain)
-            for (int q = 0; q < QCAP; q++) {
-              const Inst& I = S.inst[lane][q];
-              if (I.state == I_READY) ready_x |= 1u << S.bExec[S.cCb0[lane] + I.cb];
-            }
           const uint32_t hr = __reduce_or_sync(FULL, ready_x);
           bool run = false;
           if (is_exec) {
@@ -576,7 +569,9 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           }
           __syncwarp();
         }
-        if (!anyA && !__any_sync(FULL, chB)) break;
+        // phase A ended stable and B changed nothing: the timestamp is settled (a further A/B round
+        // would be a no-op)
+        if (!__any_sync(FULL, chB)) break;
       }
       // ===================== advance time =====================
       uint64_t nt = NONE64;
