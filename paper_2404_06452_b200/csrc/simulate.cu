@@ -321,8 +321,25 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
 
     for (;;) {
       // ===================== settle time t (D15) =====================
+      // A phase-A pass can leave work due at t only on an executor it advanced (a zero-length eps)
+      // -- units settle in (1), transits made in (1)/(2) arrive in (3) of the same pass, and releases
+      // are spaced by T -- and phase B can create due-now phase-A work only through a zero eps or
+      // kappa.  Passes are repeated exactly when such work exists, so every skipped pass is a no-op.
+      auto pending_a = [&]() {
+        bool p = false;
+        if (is_exec) {
+          const uint32_t ph = S.exPhase[lane];
+          p = ((ph == P_CPU || ph == P_EPS_SPIN) && S.exRem[lane] == 0) || (ph == P_EPS_SUSP && S.exTimer[lane] == C.t);
+        }
+        if (is_unit) {
+          const uint32_t us = S.unState[lane];
+          p = p || ((us == U_SWOUT || us == U_SWIN) && S.unEnd[lane] == C.t) || (us == U_RUN && S.unRem[lane] == 0);
+        }
+        return __any_sync(FULL, p);
+      };
+      bool run_a = true;
       for (;;) {
-        for (;;) {
+        while (run_a) {
           bool ch = false;
           // (1) units
           if (is_unit) {
@@ -415,7 +432,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             }
           }
           __syncwarp();
-          if (!__any_sync(FULL, ch)) break;
+          run_a = __any_sync(FULL, ch) && pending_a();
         }
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
         bool chB = false;
@@ -572,6 +589,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
         // phase A ended stable and B changed nothing: the timestamp is settled (a further A/B round
         // would be a no-op)
         if (!__any_sync(FULL, chB)) break;
+        run_a = pending_a();
       }
       // ===================== advance time =====================
       uint64_t nt = NONE64;
