@@ -37,11 +37,28 @@ enum { P_NONE = 0, P_CPU, P_EPS_SPIN, P_EPS_SUSP, P_WAIT };
 enum { U_IDLE = 0, U_RUN, U_SWOUT, U_SWIN };
 enum { I_FREE = 0, I_READY, I_RUN, I_TRANSIT };
 
-struct Inst {
-  uint64_t release, ready_at;
-  uint32_t k, seq, rem;  // rem: remaining accelerator work of a preempted request
-  uint8_t cb, state, waiting, started, unit, pad[3];
+// Instance slot q of chain c: the wide fields per slot, the byte fields packed per chain (byte q of
+// a word), so that the per-lane scans over a chain's QCAP slots are one word load + a byte compare.
+// The release time is not stored: instance k of chain c is released at phase_c + k T_c (D2).
+struct InstWide {
+  uint32_t k, seq;
+  union {
+    uint64_t ready_at;  // I_TRANSIT: arrival of the next callback (D13)
+    uint32_t rem;       // a preempted request: its remaining accelerator work
+  };
 };
+struct InstRef {
+  uint8_t &state, &cb, &waiting, &started, &unit;
+  uint64_t& ready_at;
+  uint32_t &k, &seq, &rem;
+};
+__device__ __forceinline__ uint8_t& byte_of(uint32_t& w, uint32_t q) { return reinterpret_cast<uint8_t*>(&w)[q]; }
+__device__ __forceinline__ uint32_t rep4(uint32_t v) { return v * 0x01010101u; }
+// slots whose byte in w equals v, as a bit mask over slots (bit q = slot q)
+__device__ __forceinline__ uint32_t slots_eq(uint32_t w, uint32_t v) {
+  const uint32_t m = __vcmpeq4(w, rep4(v));
+  return (m & 1u) | ((m >> 7) & 2u) | ((m >> 14) & 4u) | ((m >> 21) & 8u);
+}
 
 struct DesSmem {
   // static (per set)
@@ -56,7 +73,19 @@ struct DesSmem {
   uint8_t xWait[MAXX];
   uint32_t uEps[MAXU], uKap[MAXU], uN[MAXU];
   // dynamic
-  Inst inst[MAXC][QCAP];
+  union {
+    InstWide iw[MAXC][QCAP];
+    struct {  // WFD scratch of the static staging (dead before the dynamic state exists)
+      uint64_t wu[MAXCB];
+      uint8_t wo[MAXCB], wn[MAXCB], wc[MAXCB];
+    } wfd;
+  };
+  uint32_t iState[MAXC], iCb[MAXC], iWait[MAXC], iStarted[MAXC], iUnit[MAXC];
+  __device__ __forceinline__ InstRef ref(uint32_t c, uint32_t q) {
+    InstWide& w = iw[c][q];
+    return InstRef{byte_of(iState[c], q), byte_of(iCb[c], q), byte_of(iWait[c], q), byte_of(iStarted[c], q),
+                   byte_of(iUnit[c], q), w.ready_at, w.k, w.seq, w.rem};
+  }
   uint32_t exRem[MAXX];
   uint64_t exTimer[MAXX];
   uint8_t exChain[MAXX], exSlot[MAXX], exSeg[MAXX], exPhase[MAXX];
@@ -103,7 +132,7 @@ struct Ctx {
   // executor x starts segment exSeg[x] of its job's callback
   __device__ void begin_segment(uint32_t x) {
     const uint32_t c = S.exChain[x], sl = S.exSlot[x];
-    const uint32_t j = S.cCb0[c] + S.inst[c][sl].cb;
+    const uint32_t j = S.cCb0[c] + S.ref(c, sl).cb;
     const uint32_t g = S.bSeg0[j] + S.exSeg[x];
     if (S.gKind[g] == 0) {
       S.exPhase[x] = P_CPU;
@@ -117,7 +146,7 @@ struct Ctx {
   // executor x finished the current segment (D12, D13, D16)
   __device__ void advance_segment(uint32_t x) {
     const uint32_t c = S.exChain[x], sl = S.exSlot[x];
-    Inst& I = S.inst[c][sl];
+    InstRef I = S.ref(c, sl);
     const uint32_t j = S.cCb0[c] + I.cb;
     ev(EV_SEG_DONE, c, I.cb, S.exSeg[x], FULL, FULL);
     S.exSeg[x]++;
@@ -129,7 +158,7 @@ struct Ctx {
       if (nx == x) I.state = I_READY;
       else { I.state = I_TRANSIT; I.ready_at = t + comm; }
     } else {
-      const uint64_t resp = t - I.release;
+      const uint64_t resp = t - (S.cPhase[c] + (uint64_t)I.k * S.cT[c]);  // D16
       atomicMax(&S.maxResp[c], (unsigned long long)resp);
       atomicAdd(&S.cnt[c], 1u);
       ev(EV_CHAIN_DONE, c, FULL, FULL, FULL, FULL);
@@ -140,7 +169,10 @@ struct Ctx {
   }
 };
 
-__global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
+#ifndef SIM_MINB
+#define SIM_MINB 8  // measured: 8 blocks of 4 warps (64 registers) beat 6 and 7; 9 spills
+#endif
+__global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
                                                            uint64_t horizon, uint64_t seed, uint64_t first_index,
                                                            uint32_t sim_flags, uint64_t* __restrict__ out_resp, uint64_t* __restrict__ out_count,
                                                            uint64_t* __restrict__ out_digest,
@@ -245,10 +277,8 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
     }
     __syncwarp();
     if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) {  // WFD unit assignment, as pack_kernel
-      __shared__ uint64_t wu_all[SW][MAXCB];
-      __shared__ uint8_t wo_all[SW][MAXCB], wn_all[SW][MAXCB], wc_all[SW][MAXCB];
-      uint64_t* wu = wu_all[threadIdx.x >> 5];
-      uint8_t *wo = wo_all[threadIdx.x >> 5], *wn = wn_all[threadIdx.x >> 5], *wc = wc_all[threadIdx.x >> 5];
+      uint64_t* wu = S.wfd.wu;
+      uint8_t *wo = S.wfd.wo, *wn = S.wfd.wn, *wc = S.wfd.wc;
       for (uint32_t a = 0; a < nac; a++) {
         const uint32_t nu = b.accel_units[a0 + a];
         uint32_t ni = 0;
@@ -300,7 +330,8 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
     }
     // dynamic state
     if (lane < MAXC) {
-      for (int q = 0; q < QCAP; q++) { S.inst[lane][q].state = I_FREE; S.inst[lane][q].waiting = 0; }
+      S.iState[lane] = rep4(I_FREE);
+      S.iWait[lane] = 0;
       S.maxResp[lane] = 0;
       S.cnt[lane] = 0;
       S.exPhase[lane] = P_NONE;
@@ -346,12 +377,12 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             const uint32_t u = lane;
             if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
               if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
-              else { S.unState[u] = U_RUN; S.unRem[u] = S.inst[S.unChain[u]][S.unSlot[u]].rem; }
+              else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; }
               ch = true;
             }
             if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
               const uint32_t c = S.unChain[u], sl = S.unSlot[u];
-              Inst& I = S.inst[c][sl];
+              InstRef I = S.ref(c, sl);
               const uint32_t j = S.cCb0[c] + I.cb;
               uint32_t x = S.bExec[j];
               // the request's segment: the executor's current segment
@@ -373,7 +404,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
               S.exPhase[x] = P_WAIT;
               enq = true;
-              enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.inst[S.exChain[x]][S.exSlot[x]].k & 0xffffffu);
+              enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.ref(S.exChain[x], S.exSlot[x]).k & 0xffffffu);
               ch = true;
             }
           }
@@ -388,7 +419,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             }
             if (enq) {
               const uint32_t x = lane, c = S.exChain[x], sl = S.exSlot[x];
-              Inst& I = S.inst[c][sl];
+              InstRef I = S.ref(c, sl);
               const uint32_t g = S.bSeg0[S.cCb0[c] + I.cb] + S.exSeg[x];
               I.seq = seq + pos;
               I.waiting = 1;
@@ -402,29 +433,26 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           // (3) comm arrivals, (4) releases (D2, D14)
           if (is_chain) {
             const uint32_t c = lane;
-            for (int q = 0; q < QCAP; q++) {
-              Inst& I = S.inst[c][q];
-              if (I.state == I_TRANSIT && I.ready_at == C.t) { I.state = I_READY; ch = true; }
+            for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
+              const uint32_t q = __ffs(tm) - 1;
+              if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; ch = true; }
             }
             const uint64_t r = S.cPhase[c] + (uint64_t)next_k * S.cT[c];
             if (r == C.t && r < horizon) {
               if (S.cCls[c] == 1)
-                for (int q = 0; q < QCAP; q++) {
-                  Inst& I = S.inst[c][q];
-                  if (I.state == I_READY && I.cb == 0) {
-                    I.state = I_FREE;
-                    drops++;
-                    C.ev(EV_DROP, c, FULL, FULL, FULL, FULL);
-                  }
+                for (uint32_t dm = slots_eq(S.iState[c], I_READY) & slots_eq(S.iCb[c], 0); dm; dm &= dm - 1) {
+                  byte_of(S.iState[c], __ffs(dm) - 1) = I_FREE;
+                  drops++;
+                  C.ev(EV_DROP, c, FULL, FULL, FULL, FULL);
                 }
-              int slot = -1;
-              for (int q = QCAP - 1; q >= 0; q--) if (S.inst[c][q].state == I_FREE) slot = q;
+              const uint32_t fm = slots_eq(S.iState[c], I_FREE);
+              const int slot = fm ? __ffs(fm) - 1 : -1;
               if (slot < 0) {
                 ovf++;
                 C.ev(EV_OVERFLOW, c, FULL, FULL, FULL, FULL);
               } else {
-                Inst& I = S.inst[c][slot];
-                I.state = I_READY; I.release = C.t; I.k = next_k; I.cb = 0; I.waiting = 0;
+                InstRef I = S.ref(c, slot);
+                I.state = I_READY; I.k = next_k; I.cb = 0; I.waiting = 0;
                 C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
               }
               next_k++;
@@ -437,11 +465,11 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
         bool chB = false;
         uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
-        if (is_chain)
-          for (int q = 0; q < QCAP; q++) {
-            const Inst& I = S.inst[lane][q];
-            if (I.state == I_READY) ready_x |= 1u << S.bExec[S.cCb0[lane] + I.cb];
-          }
+        if (is_chain) {
+          const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
+          for (uint32_t rm = slots_eq(S.iState[lane], I_READY); rm; rm &= rm - 1)
+            ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * (__ffs(rm) - 1))) & 0xffu)];
+        }
         const uint32_t has_ready = __reduce_or_sync(FULL, ready_x);
         const uint32_t want = __ballot_sync(FULL, is_exec && on_core && S.exPhase[lane] == P_NONE && ((has_ready >> lane) & 1u));
         uint32_t wm = want;
@@ -452,14 +480,15 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           const uint32_t c = __ffs(cand) - 1;
           if (lane == c) {
             int best = -1;
-            for (int q = 0; q < QCAP; q++) {
-              const Inst& I = S.inst[c][q];
-              if (I.state != I_READY || S.bExec[S.cCb0[c] + I.cb] != x) continue;
-              if (best < 0) { best = q; continue; }
-              const Inst& B = S.inst[c][best];
-              if (I.release < B.release || (I.release == B.release && I.cb < B.cb)) best = q;
+            const uint32_t cbw = S.iCb[c];
+            for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1) {
+              const uint32_t q = __ffs(rm) - 1, qcb = (cbw >> (8 * q)) & 0xffu;
+              if (S.bExec[S.cCb0[c] + qcb] != x) continue;
+              if (best < 0) { best = (int)q; continue; }
+              const uint32_t kq = S.iw[c][q].k, kb = S.iw[c][best].k;  // older release = smaller k
+              if (kq < kb || (kq == kb && qcb < ((cbw >> (8 * best)) & 0xffu))) best = (int)q;
             }
-            Inst& I = S.inst[c][best];
+            InstRef I = S.ref(c, best);
             I.state = I_RUN;
             S.exChain[x] = (uint8_t)c;
             S.exSlot[x] = (uint8_t)best;
@@ -468,9 +497,10 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             C.begin_segment(x);
             // this chain no longer offers that instance
             ready_x = 0;
-            for (int q = 0; q < QCAP; q++) {
-              const Inst& J = S.inst[c][q];
-              if (J.state == I_READY) ready_x |= 1u << S.bExec[S.cCb0[c] + J.cb];
+            {
+              const uint32_t cbw2 = S.iCb[c], cb0 = S.cCb0[c];
+              for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1)
+                ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * (__ffs(rm) - 1))) & 0xffu)];
             }
           }
           __syncwarp();
@@ -500,14 +530,14 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
             uint32_t myseq = 0xffffffffu;
             int fslot = -1;
             if (is_chain)
-              for (int q = 0; q < QCAP; q++) {
-                const Inst& I = S.inst[lane][q];
-                if (I.waiting && I.unit == u && I.seq < myseq) { myseq = I.seq; fslot = q; }
+              for (uint32_t wm = slots_eq(S.iWait[lane], 1) & slots_eq(S.iUnit[lane], u); wm; wm &= wm - 1) {
+                const uint32_t q = __ffs(wm) - 1;
+                if (S.iw[lane][q].seq < myseq) { myseq = S.iw[lane][q].seq; fslot = (int)q; }
               }
             const uint32_t oldest = __reduce_min_sync(FULL, myseq);
             if (oldest == 0xffffffffu) continue;
             if (myseq == oldest) {
-              Inst& I = S.inst[lane][fslot];
+              InstRef I = S.ref(lane, fslot);
               const uint32_t j = S.cCb0[lane] + I.cb, x = S.bExec[j], seg = S.exSeg[x];
               S.unChain[u] = (uint8_t)lane;
               S.unSlot[u] = (uint8_t)fslot;
@@ -525,17 +555,17 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           uint32_t key = 0;
           int bslot = -1;
           if (is_chain) {
-            for (int q = 0; q < QCAP; q++) {
-              const Inst& I = S.inst[lane][q];
-              if (!I.waiting || I.unit != u) continue;
+            const uint32_t sw = S.iStarted[lane];
+            for (uint32_t wm = slots_eq(S.iWait[lane], 1) & slots_eq(S.iUnit[lane], u); wm; wm &= wm - 1) {
+              const int q = __ffs(wm) - 1;
               if (ust == U_RUN && S.unChain[u] == lane && S.unSlot[u] == q) continue;
               if (bslot < 0) { bslot = q; continue; }
-              const Inst& B = S.inst[lane][bslot];
-              if (I.started != B.started) { if (I.started) bslot = q; }
-              else if (I.seq < B.seq) bslot = q;
+              const uint32_t sq = (sw >> (8 * q)) & 0xffu, sb = (sw >> (8 * bslot)) & 0xffu;
+              if (sq != sb) { if (sq) bslot = q; }
+              else if (S.iw[lane][q].seq < S.iw[lane][bslot].seq) bslot = q;
             }
             if (bslot >= 0) {
-              const Inst& I = S.inst[lane][bslot];
+              InstRef I = S.ref(lane, bslot);
               const uint32_t g = S.bSeg0[S.cCb0[lane] + I.cb];  // bucket is per (chain, accelerator)
               uint32_t bkt = 0;
               for (uint32_t gg = g; gg < g + S.bNseg[S.cCb0[lane] + I.cb]; gg++)
@@ -548,7 +578,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           const uint32_t wc = 31u - ((best - 1u) & 31u);
           const uint32_t wbkt = (best - 1u) >> 6;
           if (lane == wc) {
-            Inst& I = S.inst[wc][bslot];
+            InstRef I = S.ref(wc, bslot);
             const uint32_t j = S.cCb0[wc] + I.cb;
             const uint32_t x = S.bExec[j];
             const uint32_t seg = S.exSeg[x];
@@ -569,7 +599,7 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
           }
           if (ust == U_RUN) {  // D9: preempt a lower bucket
             const uint32_t rc = S.unChain[u];
-            Inst& R = S.inst[rc][S.unSlot[u]];
+            InstRef R = S.ref(rc, S.unSlot[u]);
             const uint32_t rj = S.cCb0[rc] + R.cb, rx = S.bExec[rj], rseg = S.exSeg[rx];
             const uint32_t rbkt = S.gBkt[S.bSeg0[rj] + rseg];
             if (wbkt > rbkt) {
@@ -596,8 +626,8 @@ __global__ void __launch_bounds__(SW * 32) simulate_kernel(paam_batch b, const R
       if (is_chain) {
         const uint64_t r = S.cPhase[lane] + (uint64_t)next_k * S.cT[lane];
         if (r < horizon) nt = r;
-        for (int q = 0; q < QCAP; q++)
-          if (S.inst[lane][q].state == I_TRANSIT) nt = min(nt, S.inst[lane][q].ready_at);
+        for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
+          nt = min(nt, S.iw[lane][__ffs(tm) - 1].ready_at);
       }
       if (is_exec) {
         const uint32_t ph = S.exPhase[lane];

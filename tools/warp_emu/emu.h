@@ -113,6 +113,11 @@ inline int __popcll(unsigned long long x) { return __builtin_popcountll(x); }
 inline int __clz(unsigned x) { return x ? __builtin_clz(x) : 32; }
 inline int __clzll(unsigned long long x) { return x ? __builtin_clzll(x) : 64; }
 inline int __ffs(unsigned x) { return x ? __builtin_ctz(x) + 1 : 0; }
+inline unsigned __vcmpeq4(unsigned a, unsigned b) {  // per byte: 0xff where equal
+  unsigned r = 0;
+  for (int i = 0; i < 4; i++) if (((a >> (8 * i)) & 0xffu) == ((b >> (8 * i)) & 0xffu)) r |= 0xffu << (8 * i);
+  return r;
+}
 inline int __ffsll(unsigned long long x) { return x ? __builtin_ctzll(x) + 1 : 0; }
 inline unsigned __fns(unsigned mask, unsigned base, int offset) {
   for (unsigned i = base; i < 32; i++)
