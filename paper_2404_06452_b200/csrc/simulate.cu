@@ -36,6 +36,7 @@ enum { EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_EN
 enum { P_NONE = 0, P_CPU, P_EPS_SPIN, P_EPS_SUSP, P_WAIT };
 enum { U_IDLE = 0, U_RUN, U_SWOUT, U_SWIN };
 enum { I_FREE = 0, I_READY, I_RUN, I_TRANSIT };
+constexpr uint32_t NOQ = 0xffu;  // wunit of a request that is not queued
 
 // Instance slot q of chain c: the wide fields per slot, the byte fields packed per chain (byte q of
 // a word), so that the per-lane scans over a chain's QCAP slots are one word load + a byte compare.
@@ -48,17 +49,15 @@ struct InstWide {
   };
 };
 struct InstRef {
-  uint8_t &state, &cb, &waiting, &started, &unit;
+  uint8_t &state, &cb, &wunit, &started;  // wunit: the unit a waiting request is queued on, else NOQ
   uint64_t& ready_at;
   uint32_t &k, &seq, &rem;
 };
 __device__ __forceinline__ uint8_t& byte_of(uint32_t& w, uint32_t q) { return reinterpret_cast<uint8_t*>(&w)[q]; }
 __device__ __forceinline__ uint32_t rep4(uint32_t v) { return v * 0x01010101u; }
-// slots whose byte in w equals v, as a bit mask over slots (bit q = slot q)
-__device__ __forceinline__ uint32_t slots_eq(uint32_t w, uint32_t v) {
-  const uint32_t m = __vcmpeq4(w, rep4(v));
-  return (m & 1u) | ((m >> 7) & 2u) | ((m >> 14) & 4u) | ((m >> 21) & 8u);
-}
+// slots whose byte in w equals v: bit 8q set for slot q (iterate with m &= m - 1, slot_of(m))
+__device__ __forceinline__ uint32_t slots_eq(uint32_t w, uint32_t v) { return __vcmpeq4(w, rep4(v)) & 0x01010101u; }
+__device__ __forceinline__ uint32_t slot_of(uint32_t m) { return (uint32_t)(__ffs(m) - 1) >> 3; }
 
 struct DesSmem {
   // static (per set)
@@ -80,11 +79,11 @@ struct DesSmem {
       uint8_t wo[MAXCB], wn[MAXCB], wc[MAXCB];
     } wfd;
   };
-  uint32_t iState[MAXC], iCb[MAXC], iWait[MAXC], iStarted[MAXC], iUnit[MAXC];
+  uint32_t iState[MAXC], iCb[MAXC], iWUnit[MAXC], iStarted[MAXC];
   __device__ __forceinline__ InstRef ref(uint32_t c, uint32_t q) {
     InstWide& w = iw[c][q];
-    return InstRef{byte_of(iState[c], q), byte_of(iCb[c], q), byte_of(iWait[c], q), byte_of(iStarted[c], q),
-                   byte_of(iUnit[c], q), w.ready_at, w.k, w.seq, w.rem};
+    return InstRef{byte_of(iState[c], q), byte_of(iCb[c], q), byte_of(iWUnit[c], q), byte_of(iStarted[c], q),
+                   w.ready_at, w.k, w.seq, w.rem};
   }
   uint32_t exRem[MAXX];
   uint64_t exTimer[MAXX];
@@ -170,7 +169,7 @@ struct Ctx {
 };
 
 #ifndef SIM_MINB
-#define SIM_MINB 8  // measured: 8 blocks of 4 warps (64 registers) beat 6 and 7; 9 spills
+#define SIM_MINB 8  // measured: 8 blocks of 4 warps (64 registers) beat 6, 7 and 9
 #endif
 __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
                                                            uint64_t horizon, uint64_t seed, uint64_t first_index,
@@ -331,7 +330,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     // dynamic state
     if (lane < MAXC) {
       S.iState[lane] = rep4(I_FREE);
-      S.iWait[lane] = 0;
+      S.iWUnit[lane] = rep4(NOQ);
       S.maxResp[lane] = 0;
       S.cnt[lane] = 0;
       S.exPhase[lane] = P_NONE;
@@ -388,7 +387,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               // the request's segment: the executor's current segment
               const uint32_t g = S.bSeg0[j] + S.exSeg[x];
               C.ev(EV_ACC_DONE, c, I.cb, S.exSeg[x], u, S.gBkt[g]);
-              I.waiting = 0;
+              I.wunit = NOQ;
               S.unState[u] = U_IDLE;
               C.advance_segment(x);
               ch = true;
@@ -422,9 +421,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               InstRef I = S.ref(c, sl);
               const uint32_t g = S.bSeg0[S.cCb0[c] + I.cb] + S.exSeg[x];
               I.seq = seq + pos;
-              I.waiting = 1;
+              I.wunit = S.gUnit[g];
               I.started = 0;
-              I.unit = S.gUnit[g];
               C.ev(EV_REQ_ENQUEUE, c, I.cb, S.exSeg[x], S.gUnit[g], S.gBkt[g]);
             }
             seq += __popc(enq_mask);
@@ -434,25 +432,25 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           if (is_chain) {
             const uint32_t c = lane;
             for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
-              const uint32_t q = __ffs(tm) - 1;
+              const uint32_t q = slot_of(tm);
               if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; ch = true; }
             }
             const uint64_t r = S.cPhase[c] + (uint64_t)next_k * S.cT[c];
             if (r == C.t && r < horizon) {
               if (S.cCls[c] == 1)
                 for (uint32_t dm = slots_eq(S.iState[c], I_READY) & slots_eq(S.iCb[c], 0); dm; dm &= dm - 1) {
-                  byte_of(S.iState[c], __ffs(dm) - 1) = I_FREE;
+                  byte_of(S.iState[c], slot_of(dm)) = I_FREE;
                   drops++;
                   C.ev(EV_DROP, c, FULL, FULL, FULL, FULL);
                 }
               const uint32_t fm = slots_eq(S.iState[c], I_FREE);
-              const int slot = fm ? __ffs(fm) - 1 : -1;
+              const int slot = fm ? (int)slot_of(fm) : -1;
               if (slot < 0) {
                 ovf++;
                 C.ev(EV_OVERFLOW, c, FULL, FULL, FULL, FULL);
               } else {
                 InstRef I = S.ref(c, slot);
-                I.state = I_READY; I.k = next_k; I.cb = 0; I.waiting = 0;
+                I.state = I_READY; I.k = next_k; I.cb = 0; I.wunit = NOQ;
                 C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
               }
               next_k++;
@@ -468,7 +466,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         if (is_chain) {
           const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
           for (uint32_t rm = slots_eq(S.iState[lane], I_READY); rm; rm &= rm - 1)
-            ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * (__ffs(rm) - 1))) & 0xffu)];
+            ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * slot_of(rm))) & 0xffu)];
         }
         const uint32_t has_ready = __reduce_or_sync(FULL, ready_x);
         const uint32_t want = __ballot_sync(FULL, is_exec && on_core && S.exPhase[lane] == P_NONE && ((has_ready >> lane) & 1u));
@@ -482,7 +480,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             int best = -1;
             const uint32_t cbw = S.iCb[c];
             for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1) {
-              const uint32_t q = __ffs(rm) - 1, qcb = (cbw >> (8 * q)) & 0xffu;
+              const uint32_t q = slot_of(rm), qcb = (cbw >> (8 * q)) & 0xffu;
               if (S.bExec[S.cCb0[c] + qcb] != x) continue;
               if (best < 0) { best = (int)q; continue; }
               const uint32_t kq = S.iw[c][q].k, kb = S.iw[c][best].k;  // older release = smaller k
@@ -500,7 +498,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             {
               const uint32_t cbw2 = S.iCb[c], cb0 = S.cCb0[c];
               for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1)
-                ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * (__ffs(rm) - 1))) & 0xffu)];
+                ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * slot_of(rm))) & 0xffu)];
             }
           }
           __syncwarp();
@@ -530,8 +528,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             uint32_t myseq = 0xffffffffu;
             int fslot = -1;
             if (is_chain)
-              for (uint32_t wm = slots_eq(S.iWait[lane], 1) & slots_eq(S.iUnit[lane], u); wm; wm &= wm - 1) {
-                const uint32_t q = __ffs(wm) - 1;
+              for (uint32_t wm = slots_eq(S.iWUnit[lane], u); wm; wm &= wm - 1) {
+                const uint32_t q = slot_of(wm);
                 if (S.iw[lane][q].seq < myseq) { myseq = S.iw[lane][q].seq; fslot = (int)q; }
               }
             const uint32_t oldest = __reduce_min_sync(FULL, myseq);
@@ -556,8 +554,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           int bslot = -1;
           if (is_chain) {
             const uint32_t sw = S.iStarted[lane];
-            for (uint32_t wm = slots_eq(S.iWait[lane], 1) & slots_eq(S.iUnit[lane], u); wm; wm &= wm - 1) {
-              const int q = __ffs(wm) - 1;
+            for (uint32_t wm = slots_eq(S.iWUnit[lane], u); wm; wm &= wm - 1) {
+              const int q = (int)slot_of(wm);
               if (ust == U_RUN && S.unChain[u] == lane && S.unSlot[u] == q) continue;
               if (bslot < 0) { bslot = q; continue; }
               const uint32_t sq = (sw >> (8 * q)) & 0xffu, sb = (sw >> (8 * bslot)) & 0xffu;
@@ -627,7 +625,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         const uint64_t r = S.cPhase[lane] + (uint64_t)next_k * S.cT[lane];
         if (r < horizon) nt = r;
         for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
-          nt = min(nt, S.iw[lane][__ffs(tm) - 1].ready_at);
+          nt = min(nt, S.iw[lane][slot_of(tm)].ready_at);
       }
       if (is_exec) {
         const uint32_t ph = S.exPhase[lane];
