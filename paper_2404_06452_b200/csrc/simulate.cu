@@ -91,6 +91,7 @@ struct DesSmem {
   uint64_t unEnd[MAXU];
   uint32_t unRem[MAXU];
   uint8_t unState[MAXU], unChain[MAXU], unSlot[MAXU];
+  uint32_t uQ[MAXU];  // requests queued on the unit (waiting, started or not; the running one included)
   unsigned long long maxResp[MAXC];
   uint32_t cnt[MAXC];
 };
@@ -127,6 +128,11 @@ struct Ctx {
   bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
   __device__ void ev(uint32_t kind, uint32_t c, uint32_t cb, uint32_t seg, uint32_t unit, uint32_t bk) {
     dig += fnv_record(t, kind, S.cLocal[c], cb, seg, unit, bk);
+  }
+  // executor x has phase-A work due now (a zero-length eps leaves it due right after it starts)
+  __device__ bool exec_due(uint32_t x) const {
+    const uint32_t ph = S.exPhase[x];
+    return ((ph == P_CPU || ph == P_EPS_SPIN) && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == t);
   }
   // executor x starts segment exSeg[x] of its job's callback
   __device__ void begin_segment(uint32_t x) {
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       S.exPhase[lane] = P_NONE;
       S.exChain[lane] = 0xff;
     }
-    if (lane < MAXU) S.unState[lane] = U_IDLE;
+    if (lane < MAXU) { S.unState[lane] = U_IDLE; S.uQ[lane] = 0; }
     __syncwarp();
 
     const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
@@ -355,18 +361,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       // -- units settle in (1), transits made in (1)/(2) arrive in (3) of the same pass, and releases
       // are spaced by T -- and phase B can create due-now phase-A work only through a zero eps or
       // kappa.  Passes are repeated exactly when such work exists, so every skipped pass is a no-op.
-      auto pending_a = [&]() {
-        bool p = false;
-        if (is_exec) {
-          const uint32_t ph = S.exPhase[lane];
-          p = ((ph == P_CPU || ph == P_EPS_SPIN) && S.exRem[lane] == 0) || (ph == P_EPS_SUSP && S.exTimer[lane] == C.t);
-        }
-        if (is_unit) {
-          const uint32_t us = S.unState[lane];
-          p = p || ((us == U_SWOUT || us == U_SWIN) && S.unEnd[lane] == C.t) || (us == U_RUN && S.unRem[lane] == 0);
-        }
-        return __any_sync(FULL, p);
-      };
+      // The unit queues' occupancy (uQ) lets phase B skip units with no request to dispatch.
       bool run_a = true;
       for (;;) {
         while (run_a) {
@@ -388,6 +383,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               const uint32_t g = S.bSeg0[j] + S.exSeg[x];
               C.ev(EV_ACC_DONE, c, I.cb, S.exSeg[x], u, S.gBkt[g]);
               I.wunit = NOQ;
+              S.uQ[u]--;
               S.unState[u] = U_IDLE;
               C.advance_segment(x);
               ch = true;
@@ -407,6 +403,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               ch = true;
             }
           }
+          const bool due_x = is_exec && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
           const uint32_t enq_mask = __ballot_sync(FULL, enq);
           if (enq_mask) {
             uint32_t pos = 0;
@@ -423,6 +420,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               I.seq = seq + pos;
               I.wunit = S.gUnit[g];
               I.started = 0;
+              atomicAdd(&S.uQ[S.gUnit[g]], 1u);
               C.ev(EV_REQ_ENQUEUE, c, I.cb, S.exSeg[x], S.gUnit[g], S.gBkt[g]);
             }
             seq += __popc(enq_mask);
@@ -458,10 +456,10 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             }
           }
           __syncwarp();
-          run_a = __any_sync(FULL, ch) && pending_a();
+          run_a = __any_sync(FULL, due_x);
         }
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
-        bool chB = false;
+        bool chB = false, dueB = false;  // dueB: B left phase-A work due now
         uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
         if (is_chain) {
           const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
@@ -493,6 +491,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             S.exSeg[x] = 0;
             C.ev(EV_CB_START, c, I.cb, 0, FULL, FULL);
             C.begin_segment(x);
+            dueB |= C.exec_due(x);
             // this chain no longer offers that instance
             ready_x = 0;
             {
@@ -524,7 +523,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         for (uint32_t u = 0; u < n_unit; u++) {
           const uint32_t ust = S.unState[u];
           if (fifo) {  // FIFO_DIRECT: an idle unit starts the oldest request; never preempts
-            if (ust != U_IDLE) continue;
+            if (ust != U_IDLE || S.uQ[u] == 0) continue;
             uint32_t myseq = 0xffffffffu;
             int fslot = -1;
             if (is_chain)
@@ -549,6 +548,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             continue;
           }
           if (ust != U_IDLE && !(ust == U_RUN && S.uN[u] > 1)) continue;
+          if (S.uQ[u] <= (ust == U_RUN ? 1u : 0u)) continue;  // nothing queued besides the running request
           // best waiting request on u, excluding the running one: key = bucket | started | priority
           uint32_t key = 0;
           int bslot = -1;
@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               if (I.started) {  // D10: switch back in
                 S.unState[u] = U_SWIN;
                 S.unEnd[u] = C.t + S.uKap[u];
+                dueB |= S.uKap[u] == 0;
                 C.ev(EV_ACC_RESUME, wc, I.cb, seg, u, wbkt);
               } else {
                 I.started = 1;
@@ -606,6 +607,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
                 R.rem = S.unRem[u];
                 S.unState[u] = U_SWOUT;
                 S.unEnd[u] = C.t + S.uKap[u];
+                dueB |= S.uKap[u] == 0;
               }
               chB = true;
             }
@@ -616,8 +618,9 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         }
         // phase A ended stable and B changed nothing: the timestamp is settled (a further A/B round
         // would be a no-op)
-        if (!__any_sync(FULL, chB)) break;
-        run_a = pending_a();
+        const uint32_t vb = __reduce_or_sync(FULL, (chB ? 1u : 0u) | (dueB ? 2u : 0u));
+        if (!(vb & 1u)) break;
+        run_a = (vb & 2u) != 0;
       }
       // ===================== advance time =====================
       uint64_t nt = NONE64;
