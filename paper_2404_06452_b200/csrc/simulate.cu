@@ -365,14 +365,13 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       bool run_a = true;
       for (;;) {
         while (run_a) {
-          bool ch = false;
           // (1) units
           if (is_unit) {
             const uint32_t u = lane;
             if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
               if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
               else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; }
-              ch = true;
+             
             }
             if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
               const uint32_t c = S.unChain[u], sl = S.unSlot[u];
@@ -386,7 +385,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               S.uQ[u]--;
               S.unState[u] = U_IDLE;
               C.advance_segment(x);
-              ch = true;
+             
             }
           }
           __syncwarp();
@@ -395,12 +394,12 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           uint32_t enq_key = 0xffffffffu;
           if (is_exec) {
             const uint32_t x = lane, ph = S.exPhase[x];
-            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); ch = true; }
+            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); }
             else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
               S.exPhase[x] = P_WAIT;
               enq = true;
               enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.ref(S.exChain[x], S.exSlot[x]).k & 0xffffffu);
-              ch = true;
+             
             }
           }
           const bool due_x = is_exec && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
@@ -431,7 +430,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             const uint32_t c = lane;
             for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
               const uint32_t q = slot_of(tm);
-              if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; ch = true; }
+              if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; }
             }
             const uint64_t r = S.cPhase[c] + (uint64_t)next_k * S.cT[c];
             if (r == C.t && r < horizon) {
@@ -452,7 +451,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
                 C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
               }
               next_k++;
-              ch = true;
+             
             }
           }
           __syncwarp();

@@ -255,3 +255,27 @@ def test_wfd_units_parity(flags):
     g = generate_host(p, 3, 0, 5000)
     g["flags"] = flags
     assert_same(g, gpu_host_path(g))
+
+
+@pytest.mark.parametrize("case", ["m1-24", "split"])
+def test_mixed_set_sizes(case):
+    """Batches mixing small and large sets (1-24 chains; chains split over two executors, up to 32
+    sub-chains) through the pipelined pack + analyze path, vs the oracle."""
+    if case == "m1-24":
+        p, seed = make_params(m_lo=1, m_hi=24, cbs_per_chain=2), 5
+    else:
+        p, seed = make_params(exec_mode=1, n_exec=8, xexec_frac=1.0, m_lo=8, m_hi=16), 6
+    n = 30_000
+    raw = gen_gpu(p, seed, 0, n)
+    dev = torch.device("cuda")
+    sets = paam.Sets(raw)
+    wcrt = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
+    sched = torch.empty(n, dtype=torch.uint8, device=dev)
+    status = torch.full((n,), -9, dtype=torch.int32, device=dev)
+    sets.pack_analyze(raw, wcrt, sched, None, out_status=status)
+    torch.cuda.synchronize()
+    h = generate_host(p, seed, 0, n)
+    ow, osch, ost, _ = O.analyze(h, nthreads=NPROC)
+    assert np.array_equal(status.cpu().numpy(), ost)
+    assert np.array_equal(sched.cpu().numpy(), osch)
+    assert np.array_equal(wcrt.cpu().numpy().view(np.uint64), ow)

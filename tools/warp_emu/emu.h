@@ -8,6 +8,8 @@
 #include <barrier>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <thread>
@@ -30,30 +32,45 @@ struct uint4 { uint32_t x, y, z, w; };
 template <class T> inline T __ldg(const T* p) { return *p; }
 
 namespace emu {
+// A warp: one 32-thread barrier for full-warp collectives and one 16-thread barrier per half for
+// the masks 0x0000ffff / 0xffff0000 (half-warp groups); any other mask is unsupported here.
 struct Warp {
   std::barrier<> bar{32};
+  std::barrier<> half[2] = {std::barrier<>(16), std::barrier<>(16)};
   uint64_t slot[32];
 };
 inline std::vector<Warp*>& warps() { static std::vector<Warp*> w; return w; }
 inline std::barrier<>*& block_bar() { static std::barrier<>* b = nullptr; return b; }
 inline Warp& W() { return *warps()[threadIdx.x / 32]; }
 inline int lane() { return threadIdx.x & 31; }
+inline std::barrier<>& bar_of(unsigned mask) {
+  Warp& w = W();
+  if (mask == 0xffffffffu) return w.bar;
+  if (mask == 0x0000ffffu || mask == 0xffff0000u) {
+    if (!((mask >> lane()) & 1u)) { std::fprintf(stderr, "emu: lane %d not in mask %08x\n", lane(), mask); std::abort(); }
+    return w.half[mask == 0xffff0000u];
+  }
+  std::fprintf(stderr, "emu: unsupported collective mask %08x\n", mask);
+  std::abort();
+}
 template <class T> inline uint64_t bits(T v) { uint64_t b = 0; std::memcpy(&b, &v, sizeof(T)); return b; }
 template <class T> inline T unbits(uint64_t b) { T v; std::memcpy(&v, &b, sizeof(T)); return v; }
-template <class T> inline T exch(T v, int src) {
+template <class T> inline T exch(unsigned mask, T v, int src) {
   Warp& w = W();
+  std::barrier<>& b = bar_of(mask);
   w.slot[lane()] = bits(v);
-  w.bar.arrive_and_wait();
+  b.arrive_and_wait();
   const T r = unbits<T>(w.slot[src]);
-  w.bar.arrive_and_wait();
+  b.arrive_and_wait();
   return r;
 }
-template <class F> inline uint64_t collect(uint64_t v, F f) {  // all lanes get f(slots)
+template <class F> inline uint64_t collect(unsigned mask, uint64_t v, F f) {  // lanes in mask get f(slots, mask)
   Warp& w = W();
+  std::barrier<>& b = bar_of(mask);
   w.slot[lane()] = v;
-  w.bar.arrive_and_wait();
-  const uint64_t r = f(w.slot);
-  w.bar.arrive_and_wait();
+  b.arrive_and_wait();
+  const uint64_t r = f(w.slot, mask);
+  b.arrive_and_wait();
   return r;
 }
 
@@ -72,40 +89,48 @@ inline void launch_block(unsigned block, unsigned threads, const std::function<v
 }
 }  // namespace emu
 
-inline void __syncwarp(unsigned = 0xffffffffu) { emu::W().bar.arrive_and_wait(); }
-template <class T> inline T __shfl_sync(unsigned, T v, int src, int width = 32) {
-  return emu::exch(v, (emu::lane() & ~(width - 1)) + (src & (width - 1)));
+inline void __syncwarp(unsigned m = 0xffffffffu) { emu::bar_of(m).arrive_and_wait(); }
+template <class T> inline T __shfl_sync(unsigned m, T v, int src, int width = 32) {
+  return emu::exch(m, v, (emu::lane() & ~(width - 1)) + (src & (width - 1)));
 }
-template <class T> inline T __shfl_xor_sync(unsigned, T v, int m, int = 32) { return emu::exch(v, emu::lane() ^ m); }
-template <class T> inline T __shfl_up_sync(unsigned, T v, unsigned d, int = 32) {
+template <class T> inline T __shfl_xor_sync(unsigned m, T v, int x, int width = 32) {
+  const int s = emu::lane() ^ x;
+  return emu::exch(m, v, ((s & ~(width - 1)) == (emu::lane() & ~(width - 1))) ? s : emu::lane());
+}
+template <class T> inline T __shfl_up_sync(unsigned m, T v, unsigned d, int width = 32) {
   const int s = emu::lane() - (int)d;
-  const T r = emu::exch(v, s < 0 ? emu::lane() : s);
-  return r;
+  return emu::exch(m, v, (s < (emu::lane() & ~(width - 1))) ? emu::lane() : s);
 }
-template <class T> inline T __shfl_down_sync(unsigned, T v, unsigned d, int = 32) {
+template <class T> inline T __shfl_down_sync(unsigned m, T v, unsigned d, int width = 32) {
   const int s = emu::lane() + (int)d;
-  return emu::exch(v, s > 31 ? emu::lane() : s);
+  return emu::exch(m, v, (s > (emu::lane() | (width - 1))) ? emu::lane() : s);
 }
-inline unsigned __ballot_sync(unsigned, int p) {
-  return (unsigned)emu::collect(p ? 1 : 0, [](uint64_t* s) { uint64_t m = 0; for (int i = 0; i < 32; i++) m |= (s[i] & 1) << i; return m; });
+inline unsigned __ballot_sync(unsigned m, int p) {
+  return (unsigned)emu::collect(m, p ? 1 : 0, [](uint64_t* s, unsigned mk) {
+    uint64_t r = 0; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) r |= (s[i] & 1) << i; return r; });
 }
 inline int __any_sync(unsigned m, int p) { return __ballot_sync(m, p) != 0; }
-inline int __all_sync(unsigned m, int p) { return __ballot_sync(m, p) == 0xffffffffu; }
-inline unsigned __reduce_add_sync(unsigned, unsigned v) {
-  return (unsigned)emu::collect(v, [](uint64_t* s) { uint32_t a = 0; for (int i = 0; i < 32; i++) a += (uint32_t)s[i]; return (uint64_t)a; });
+inline int __all_sync(unsigned m, int p) { return __ballot_sync(m, p) == m; }
+inline unsigned __reduce_add_sync(unsigned m, unsigned v) {
+  return (unsigned)emu::collect(m, v, [](uint64_t* s, unsigned mk) {
+    uint32_t a = 0; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) a += (uint32_t)s[i]; return (uint64_t)a; });
 }
-inline unsigned __reduce_min_sync(unsigned, unsigned v) {
-  return (unsigned)emu::collect(v, [](uint64_t* s) { uint32_t a = 0xffffffffu; for (int i = 0; i < 32; i++) a = std::min(a, (uint32_t)s[i]); return (uint64_t)a; });
+inline unsigned __reduce_min_sync(unsigned m, unsigned v) {
+  return (unsigned)emu::collect(m, v, [](uint64_t* s, unsigned mk) {
+    uint32_t a = 0xffffffffu; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) a = std::min(a, (uint32_t)s[i]); return (uint64_t)a; });
 }
-inline unsigned __reduce_max_sync(unsigned, unsigned v) {
-  return (unsigned)emu::collect(v, [](uint64_t* s) { uint32_t a = 0; for (int i = 0; i < 32; i++) a = std::max(a, (uint32_t)s[i]); return (uint64_t)a; });
+inline unsigned __reduce_max_sync(unsigned m, unsigned v) {
+  return (unsigned)emu::collect(m, v, [](uint64_t* s, unsigned mk) {
+    uint32_t a = 0; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) a = std::max(a, (uint32_t)s[i]); return (uint64_t)a; });
 }
-inline unsigned __reduce_or_sync(unsigned, unsigned v) {
-  return (unsigned)emu::collect(v, [](uint64_t* s) { uint32_t a = 0; for (int i = 0; i < 32; i++) a |= (uint32_t)s[i]; return (uint64_t)a; });
+inline unsigned __reduce_or_sync(unsigned m, unsigned v) {
+  return (unsigned)emu::collect(m, v, [](uint64_t* s, unsigned mk) {
+    uint32_t a = 0; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) a |= (uint32_t)s[i]; return (uint64_t)a; });
 }
-inline unsigned __match_any_sync(unsigned, unsigned v) {
+inline unsigned __match_any_sync(unsigned m, unsigned v) {
   const int l = emu::lane();
-  return (unsigned)emu::collect(v, [l](uint64_t* s) { uint64_t m = 0; for (int i = 0; i < 32; i++) m |= (uint64_t)(s[i] == s[l]) << i; return m; });
+  return (unsigned)emu::collect(m, v, [l](uint64_t* s, unsigned mk) {
+    uint64_t r = 0; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) r |= (uint64_t)(s[i] == s[l]) << i; return r; });
 }
 
 inline int __popc(unsigned x) { return __builtin_popcount(x); }
