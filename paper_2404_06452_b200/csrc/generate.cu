@@ -42,14 +42,21 @@ constexpr uint32_t FULL = 0xffffffffu;
 
 struct GenWarp {
   uint64_t ccpu[PG_MAX_CHAINS];   // CPU WCET per chain
-  uint64_t util[PG_MAX_CHAINS];   // CPU utilisation (Q20) per chain
-  uint64_t load[32];              // worst-fit loads (cores or executors)
   uint32_t sorted[PG_MAX_CHAINS]; // sorted cut points
   uint32_t prio[PG_MAX_CHAINS];
   uint32_t pk[PG_MAX_CHAINS];     // Fisher-Yates draw of step j
   uint8_t order[PG_MAX_CHAINS];   // chains by utilisation desc, index asc
   uint8_t best[PG_MAX_CHAINS], second[PG_MAX_CHAINS], split[PG_MAX_CHAINS];
 };
+
+// Lowest lane holding the minimum of v over the lanes with `valid` (worst-fit's "least loaded,
+// ties to the lowest index").
+__device__ __forceinline__ uint32_t argmin_lane(uint64_t v, bool valid) {
+  const uint64_t x = valid ? v : ~0ull;
+  const uint32_t hi = __reduce_min_sync(FULL, (uint32_t)(x >> 32));
+  const uint32_t lo = __reduce_min_sync(FULL, (uint32_t)(x >> 32) == hi ? (uint32_t)x : 0xffffffffu);
+  return __ffs(__ballot_sync(FULL, valid && (uint32_t)(x >> 32) == hi && (uint32_t)x == lo)) - 1;
+}
 
 // Warp-per-set generation; mirrors pg_generate_set + pg_write_set step for step (same draws, same
 // integer expressions, same tie rules).
@@ -182,45 +189,43 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
         const uint64_t ud = __shfl_sync(FULL, util, d);
         rk += (ud > util) || (ud == util && d < lane);
       }
-      if (isc) { w.order[rk] = (uint8_t)lane; w.util[lane] = util; }
+      if (isc) w.order[rk] = (uint8_t)lane;
     }
     __syncwarp();
-    uint32_t n_exec, n_client;
+    // Worst-fit placement in the order above; lane k holds the load of core / executor k, and each
+    // step's least-loaded target (ties: lowest index, as the host loop) is a warp argmin.
+    uint32_t n_exec, n_client, my_best = 0;
+    uint64_t ld = 0;
     if (p.exec_mode == 0) {  // one executor per chain, worst-fit onto the client cores
-      if (lane == 0) {
-        for (uint32_t k = 0; k < p.n_cores; k++) w.load[k] = 0;
-        for (uint32_t jj = 0; jj < m; jj++) {
-          const uint32_t c = w.order[jj];
-          uint32_t best = 0;
-          for (uint32_t k = 1; k < p.n_cores; k++) if (w.load[k] < w.load[best]) best = k;
-          w.load[best] += w.util[c];
-          w.best[c] = (uint8_t)best;
-        }
+      for (uint32_t jj = 0; jj < m; jj++) {
+        const uint32_t c = w.order[jj];
+        const uint64_t uc = __shfl_sync(FULL, util, c);
+        const uint32_t best = argmin_lane(ld, lane < p.n_cores);
+        if (lane == best) ld += uc;
+        if (lane == c) my_best = best;
       }
       n_exec = m;
       n_client = p.n_cores;
     } else {  // n_exec single-threaded executors on their own cores; some chains split across two
       const uint32_t X = p.n_exec;
-      if (lane == 0) {
-        for (uint32_t x = 0; x < X; x++) w.load[x] = 0;
-        for (uint32_t jj = 0; jj < m; jj++) {
-          const uint32_t c = w.order[jj];
-          uint32_t best = 0;
-          for (uint32_t x = 1; x < X; x++) if (w.load[x] < w.load[best]) best = x;
-          const int split = p.xexec_frac_q16 && K >= 2 && pg_coin(pg_draw(key, PG_D_XEXEC, c), p.xexec_frac_q16);
-          w.best[c] = (uint8_t)best;
-          w.split[c] = (uint8_t)split;
-          if (!split) {
-            w.load[best] += w.util[c];
-          } else {
-            uint32_t second = (best == 0) ? 1 : 0;
-            for (uint32_t x = 0; x < X; x++) if (x != best && w.load[x] < w.load[second]) second = x;
-            w.second[c] = (uint8_t)second;
-            w.load[best] += w.util[c] / 2;
-            w.load[second] += w.util[c] - w.util[c] / 2;
-          }
+      const bool my_split = isc && p.xexec_frac_q16 && K >= 2 && pg_coin(pg_draw(key, PG_D_XEXEC, lane), p.xexec_frac_q16);
+      uint32_t my_second = 0;
+      for (uint32_t jj = 0; jj < m; jj++) {
+        const uint32_t c = w.order[jj];
+        const uint64_t uc = __shfl_sync(FULL, util, c);
+        const bool split = __shfl_sync(FULL, (uint32_t)my_split, c) != 0;
+        const uint32_t best = argmin_lane(ld, lane < X);
+        if (!split) {
+          if (lane == best) ld += uc;
+        } else {
+          const uint32_t second = argmin_lane(ld, lane < X && lane != best);
+          if (lane == best) ld += uc / 2;
+          if (lane == second) ld += uc - uc / 2;
+          if (lane == c) my_second = second;
         }
+        if (lane == c) my_best = best;
       }
+      if (isc) { w.best[lane] = (uint8_t)my_best; w.second[lane] = (uint8_t)my_second; w.split[lane] = (uint8_t)my_split; }
       n_exec = X;
       n_client = X;
     }
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
     }
     if (lane < n_exec) {
       const uint32_t pr = (p.exec_mode == 0) ? prio : lane + 1;
-      o.exec_core[ex0 + lane] = (p.exec_mode == 0) ? w.best[lane] : (uint8_t)lane;
+      o.exec_core[ex0 + lane] = (p.exec_mode == 0) ? (uint8_t)my_best : (uint8_t)lane;
       o.exec_prio[ex0 + lane] = pr;
       o.exec_wait[ex0 + lane] = (uint8_t)(p.spin_frac_q16 && pg_coin(pg_draw(key, PG_D_SPIN, lane), p.spin_frac_q16));
     }
