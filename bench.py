@@ -328,10 +328,10 @@ def run_ours(args):
         ebins = torch.zeros_like(bins)
 
         def e2e_step():
-            hsets.repack(hb, stream=stream)                    # H2D of the raw batch + pack kernel
             with torch.cuda.stream(stream):
                 ebins.zero_()
-            hsets.analyze(None, sched, ebins, stream=stream)
+            # H2D of the raw batch in chunks (copy engine) overlapped with pack + analyze of earlier chunks
+            hsets.pack_analyze(hb, None, sched, ebins, stream=stream)
             if dist is not None:
                 allreduce_bins(ebins, stream=stream)
             with torch.cuda.stream(stream):

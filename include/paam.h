@@ -195,9 +195,12 @@ int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_
 
 /* paam_pack_analyze -- steps 2-6 in one call, pipelined: the batch is cut into chunks whose
  * pack_kernel and analyze_kernel launches overlap on two internal streams (chunk i's analysis
- * runs while chunk i+1 is packed), joined back into `stream`.  Same results as paam_repack followed
- * by paam_analyze; `sets` must have capacity for batch->n_sets (from paam_pack).  Host batches are
- * staged first (synchronising, as paam_repack). */
+ * runs while chunk i+1 is packed), joined back into `stream`.  A host batch is copied to the device
+ * chunk by chunk on a third internal stream, each chunk's copy overlapping the kernels of the
+ * previous chunks; with pinned host memory the copies are asynchronous, so the caller must not
+ * modify the batch until `stream` has completed.  Same results as paam_repack followed by
+ * paam_analyze; `sets` must have capacity for batch->n_sets (from paam_pack).  out_status is in the
+ * batch's memory space; a host out_status makes the call synchronise `stream` (as paam_repack). */
 int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
                       uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream);
 

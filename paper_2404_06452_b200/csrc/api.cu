@@ -19,8 +19,8 @@ struct paam_sets {
   int32_t* dstatus;  // device status staging for host batches
   uint32_t dstatus_cap;
   paam_batch dev;    // the packed batch with device pointers (paam_simulate reads its structure)
-  cudaStream_t side[2];  // internal streams of paam_pack_analyze (created on first use)
-  cudaEvent_t ev[17];
+  cudaStream_t side[3];  // internal streams of paam_pack_analyze: pack, analyze, H2D copies (created on first use)
+  cudaEvent_t ev[17], evc[8];  // evc: chunk copies done
   unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18
   int device;             // the CUDA device the handle lives on (made current by every call)
 };
@@ -78,6 +78,39 @@ int batch_fields(paam_batch* b, Field* f) {
   return n;
 }
 
+// Grow the device staging buffer of a host batch to `bytes`.
+int ensure_stage(paam_sets* sets, size_t bytes) {
+  if (bytes <= sets->stage_bytes) return PAAM_OK;
+  if (sets->stage) cudaFree(sets->stage);
+  sets->stage = nullptr;
+  sets->stage_bytes = 0;
+  const cudaError_t e = cudaMalloc(&sets->stage, bytes);
+  if (e != cudaSuccess) return fail_cuda(e, "staging cudaMalloc");
+  sets->stage_bytes = bytes;
+  return PAAM_OK;
+}
+int ensure_dstatus(paam_sets* sets, uint32_t n) {
+  if (sets->dstatus_cap >= n) return PAAM_OK;
+  if (sets->dstatus) cudaFree(sets->dstatus);
+  sets->dstatus = nullptr;
+  sets->dstatus_cap = 0;
+  const cudaError_t e = cudaMalloc((void**)&sets->dstatus, sizeof(int32_t) * (n ? n : 1));
+  if (e != cudaSuccess) return fail_cuda(e, "status cudaMalloc");
+  sets->dstatus_cap = n;
+  return PAAM_OK;
+}
+int ensure_streams(paam_sets* sets) {
+  if (sets->side[0]) return PAAM_OK;
+  cudaError_t e;
+  for (int i = 0; i < 3; i++)
+    if ((e = cudaStreamCreateWithFlags(&sets->side[i], cudaStreamNonBlocking)) != cudaSuccess) return fail_cuda(e, "stream");
+  for (int i = 0; i < 17; i++)
+    if ((e = cudaEventCreateWithFlags(&sets->ev[i], cudaEventDisableTiming)) != cudaSuccess) return fail_cuda(e, "event");
+  for (int i = 0; i < 8; i++)
+    if ((e = cudaEventCreateWithFlags(&sets->evc[i], cudaEventDisableTiming)) != cudaSuccess) return fail_cuda(e, "event");
+  return PAAM_OK;
+}
+
 int check_batch(const paam_batch* b) {
   if (!b) return fail(PAAM_EINVAL, "NULL batch");
   if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
@@ -114,13 +147,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
     const int nf = batch_fields(&d, f);
     size_t bytes = 0;
     for (int i = 0; i < nf; i++) bytes += align256(f[i].elems * f[i].size);
-    if (bytes > sets->stage_bytes) {
-      if (sets->stage) cudaFree(sets->stage);
-      sets->stage = nullptr;
-      sets->stage_bytes = 0;
-      if ((e = cudaMalloc(&sets->stage, bytes)) != cudaSuccess) return fail_cuda(e, "paam_pack: staging cudaMalloc");
-      sets->stage_bytes = bytes;
-    }
+    if ((rc = ensure_stage(sets, bytes))) return rc;
     char* base = (char*)sets->stage;
     size_t off = 0;
     for (int i = 0; i < nf; i++) {  // one cudaMemcpyAsync per array (no batched-copy APIs)
@@ -133,14 +160,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
       off += align256(nb);
     }
     if (out_status) {
-      if (sets->dstatus_cap < batch->n_sets) {
-        if (sets->dstatus) cudaFree(sets->dstatus);
-        sets->dstatus = nullptr;
-        sets->dstatus_cap = 0;
-        if ((e = cudaMalloc((void**)&sets->dstatus, sizeof(int32_t) * (batch->n_sets ? batch->n_sets : 1))) != cudaSuccess)
-          return fail_cuda(e, "paam_pack: status cudaMalloc");
-        sets->dstatus_cap = batch->n_sets;
-      }
+      if ((rc = ensure_dstatus(sets, batch->n_sets))) return rc;
       status_dev = sets->dstatus;
     }
   }
@@ -234,38 +254,82 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
     return fail(PAAM_EINVAL, "paam_pack_analyze: PAAM_FLAG_VERDICT_ONLY writes no WCRTs (out_wcrt must be NULL)");
   if ((rc = use_device(sets))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (batch->mem == PAAM_MEM_HOST || batch->n_sets < 4096) {  // small or host batch: sequential
+  if (batch->n_sets < 4096) {  // small batch: sequential
     rc = paam_repack(batch, sets, out_status, stream);
     if (rc) return rc;
     return paam_analyze(sets, batch->n_sets, out_wcrt, out_sched, out_bins, stream);
   }
   cudaError_t e;
-  if (!sets->side[0]) {
-    for (int i = 0; i < 2; i++)
-      if ((e = cudaStreamCreateWithFlags(&sets->side[i], cudaStreamNonBlocking)) != cudaSuccess)
-        return fail_cuda(e, "paam_pack_analyze: stream");
-    for (int i = 0; i < 17; i++)
-      if ((e = cudaEventCreateWithFlags(&sets->ev[i], cudaEventDisableTiming)) != cudaSuccess)
-        return fail_cuda(e, "paam_pack_analyze: event");
-  }
-  static const int K = [] {  // chunks (PAAM_PIPELINE_CHUNKS overrides, for tuning)
+  if ((rc = ensure_streams(sets))) return rc;
+  const bool host = batch->mem == PAAM_MEM_HOST;
+  // Device batch: chunks of pack (side[0]) overlap analyze of the previous chunk (side[1]).  Host
+  // batch: in addition, each chunk's slice of every array is copied H2D on side[2] while the previous
+  // chunk is packed and analysed (copy engines alongside the SMs).
+  static const int KD = [] {  // chunks, device batch (PAAM_PIPELINE_CHUNKS overrides, for tuning)
     const char* e = std::getenv("PAAM_PIPELINE_CHUNKS");
     const int k = e ? std::atoi(e) : 2;  // measured best on B200 at 2M sets: 2 (K = 1, 4, 8 slower)
     return k < 1 ? 1 : (k > 8 ? 8 : k);
   }();
+  static const int KH = [] {  // chunks, host batch (PAAM_H2D_CHUNKS overrides, for tuning)
+    const char* e = std::getenv("PAAM_H2D_CHUNKS");
+    const int k = e ? std::atoi(e) : 4;
+    return k < 1 ? 1 : (k > 8 ? 8 : k);
+  }();
+  const int K = host ? KH : KD;
   const uint32_t n = batch->n_sets;
+  paam_batch d = *batch;  // the batch the kernels read (host: pointers into the staging buffer)
+  Field f[32];
+  const int nf = batch_fields(&d, f);
+  size_t foff[32];
+  int32_t* status_dev = out_status;
+  if (host) {
+    size_t bytes = 0;
+    for (int i = 0; i < nf; i++) { foff[i] = bytes; bytes += align256(f[i].elems * f[i].size); }
+    if ((rc = ensure_stage(sets, bytes))) return rc;
+    for (int i = 0; i < nf; i++) if (f[i].elems) *f[i].ptr = (char*)sets->stage + foff[i];
+    if (out_status) {
+      if ((rc = ensure_dstatus(sets, n))) return rc;
+      status_dev = sets->dstatus;
+    }
+  }
   cudaEventRecord(sets->ev[16], st);
-  cudaStreamWaitEvent(sets->side[0], sets->ev[16], 0);
-  cudaStreamWaitEvent(sets->side[1], sets->ev[16], 0);
+  for (int i = 0; i < 3; i++) cudaStreamWaitEvent(sets->side[i], sets->ev[16], 0);
   for (int i = 0; i < K; i++) {
     const uint32_t lo = (uint32_t)((uint64_t)n * i / K), hi = (uint32_t)((uint64_t)n * (i + 1) / K);
-    paam_batch view = *batch;  // CSR offsets stay global: a chunk is a shifted window of set offsets
+    if (host) {  // element ranges of this chunk in every array (host CSR offsets), in batch_fields order
+      const paam_batch& hb = *batch;
+      const size_t cl = hb.set_chain_off[lo], ch = hb.set_chain_off[hi];
+      const size_t xl = hb.set_exec_off[lo], xh = hb.set_exec_off[hi];
+      const size_t al = hb.set_accel_off[lo], ah = hb.set_accel_off[hi];
+      const size_t bl = hb.chain_cb_off[cl], bh = hb.chain_cb_off[ch];
+      const size_t sl = hb.cb_seg_off[bl], sh = hb.cb_seg_off[bh];
+      const size_t r[23][2] = {{lo, hi + 1ull}, {lo, hi + 1ull}, {lo, hi + 1ull},
+                               {cl, ch}, {cl, ch}, {cl, ch}, {cl, ch}, {cl, ch + 1},
+                               {bl, bh}, {bl, bh + 1},
+                               {sl, sh}, {sl, sh}, {sl, sh}, {sl, sh},
+                               {xl, xh}, {xl, xh}, {xl, xh},
+                               {al, ah}, {al, ah}, {al, ah}, {al, ah}, {al, ah},
+                               {lo, hi}};
+      Field hf[32];
+      paam_batch hcopy = *batch;
+      batch_fields(&hcopy, hf);
+      for (int k = 0; k < nf; k++) {  // one cudaMemcpyAsync per array slice (no batched-copy APIs)
+        if (!f[k].elems || r[k][1] <= r[k][0]) continue;
+        const size_t sz = f[k].size;
+        if ((e = cudaMemcpyAsync((char*)sets->stage + foff[k] + r[k][0] * sz, (const char*)*hf[k].ptr + r[k][0] * sz,
+                                 (r[k][1] - r[k][0]) * sz, cudaMemcpyHostToDevice, sets->side[2])) != cudaSuccess)
+          return fail_cuda(e, "paam_pack_analyze: H2D copy");
+      }
+      cudaEventRecord(sets->evc[i], sets->side[2]);
+      cudaStreamWaitEvent(sets->side[0], sets->evc[i], 0);
+    }
+    paam_batch view = d;  // CSR offsets stay global: a chunk is a shifted window of set offsets
     view.n_sets = hi - lo;
     view.set_chain_off += lo;
     view.set_exec_off += lo;
     view.set_accel_off += lo;
     if (view.set_bin) view.set_bin += lo;
-    rc = launch_pack(&view, sets->rec + lo, out_status ? out_status + lo : nullptr, sets->side[0]);
+    rc = launch_pack(&view, sets->rec + lo, status_dev ? status_dev + lo : nullptr, sets->side[0]);
     if (rc) return rc;
     cudaEventRecord(sets->ev[i], sets->side[0]);
     cudaStreamWaitEvent(sets->side[1], sets->ev[i], 0);
@@ -276,10 +340,17 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   }
   cudaEventRecord(sets->ev[8], sets->side[1]);
   cudaEventRecord(sets->ev[9], sets->side[0]);
+  cudaEventRecord(sets->ev[10], sets->side[2]);
   cudaStreamWaitEvent(st, sets->ev[8], 0);
   cudaStreamWaitEvent(st, sets->ev[9], 0);
+  cudaStreamWaitEvent(st, sets->ev[10], 0);
+  if (host && out_status) {  // host status, as paam_repack: copied back, the call synchronises
+    if ((e = cudaMemcpyAsync(out_status, status_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return fail_cuda(e, "paam_pack_analyze: status D2H");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_pack_analyze: synchronize");
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "paam_pack_analyze");
-  sets->dev = *batch;
+  sets->dev = d;
   sets->n_sets = n;
   sets->n_chains = batch->n_chains;
   sets->n_bins = batch->set_bin ? batch->n_bins : 0;
@@ -304,8 +375,9 @@ extern "C" void paam_free(paam_sets* sets) {
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
   if (sets->side[0]) {
-    for (int i = 0; i < 2; i++) cudaStreamDestroy(sets->side[i]);
+    for (int i = 0; i < 3; i++) cudaStreamDestroy(sets->side[i]);
     for (int i = 0; i < 17; i++) cudaEventDestroy(sets->ev[i]);
+    for (int i = 0; i < 8; i++) cudaEventDestroy(sets->evc[i]);
   }
   std::free(sets);
 }

@@ -267,9 +267,12 @@ class Sets:
                                _stream_ptr(stream)), "paam_admit")
 
     def pack_analyze(self, batch, out_wcrt=None, out_sched=None, out_bins=None, out_status=None, stream=None):
-        """Pipelined repack + analyze (paam_pack_analyze); device tensors or None."""
+        """Pipelined repack + analyze (paam_pack_analyze).  Outputs: device tensors or None; out_status in
+        the batch's memory space (numpy array for a host batch, device tensor for a device batch)."""
         ptr = lambda t: None if t is None else t.data_ptr()
-        check(lib().paam_pack_analyze(ctypes.byref(batch.c), self.h, ptr(out_status), ptr(out_wcrt), ptr(out_sched),
+        st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
+                                             else out_status.data_ptr())
+        check(lib().paam_pack_analyze(ctypes.byref(batch.c), self.h, st, ptr(out_wcrt), ptr(out_sched),
                                       ptr(out_bins), _stream_ptr(stream)), "paam_pack_analyze")
 
     def analyze(self, out_wcrt=None, out_sched=None, out_bins=None, n=None, stream=None):

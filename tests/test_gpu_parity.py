@@ -279,3 +279,33 @@ def test_mixed_set_sizes(case):
     assert np.array_equal(status.cpu().numpy(), ost)
     assert np.array_equal(sched.cpu().numpy(), osch)
     assert np.array_equal(wcrt.cpu().numpy().view(np.uint64), ow)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pack_analyze_from_host_batch_pipelined(pinned):
+    """paam_pack_analyze on a HOST batch: chunk slices copied H2D on a copy stream while earlier chunks
+    are packed and analysed; host status array; == oracle."""
+    p = config3_params()
+    n = 20_011
+    alloc = (lambda nb: torch.empty(max(nb, 1), dtype=torch.uint8, pin_memory=True).numpy()) if pinned else None
+    h = generate_host(p, 9, 3, n, pinned_alloc=alloc)
+    hb = paam.Batch.from_host(h)
+    dev = torch.device("cuda")
+    sets = paam.Sets(hb)
+    wcrt = torch.full((hb.c.n_chains,), -3, dtype=torch.int64, device=dev)
+    sched = torch.full((n,), 5, dtype=torch.uint8, device=dev)
+    bins = torch.zeros(2 * p.n_bins, dtype=torch.int64, device=dev)
+    status = np.full(n, -9, np.int32)
+    for _ in range(2):  # twice: the staging buffer is reused
+        bins.zero_()
+        sets.pack_analyze(hb, wcrt, sched, bins, out_status=status)
+    torch.cuda.synchronize()
+    ow, osch, ost, ob = O.analyze(h, nthreads=NPROC)
+    assert np.array_equal(status, ost)
+    assert np.array_equal(sched.cpu().numpy(), osch)
+    assert np.array_equal(bins.cpu().numpy(), ob)
+    assert np.array_equal(wcrt.cpu().numpy().view(np.uint64), ow)
+    # the handle now describes the staged batch: the DES reads it
+    resp = torch.empty(hb.c.n_chains, dtype=torch.int64, device=dev)
+    sets.simulate(10**9, 3, resp, n=64)
+    torch.cuda.synchronize()
