@@ -15,6 +15,8 @@
 //   chains      periodic releases, successors released on completion, comm delay across
 //               executors, BE overrun drops (D14), response = last callback done -
 //               release (D16).
+// Digest (D17): parity unpinned -- the record layout and hash are this implementation's definition
+// (the paper defines none); only determinism and GPU/oracle agreement are tested.
 // Same-timestamp order (D15): (A) every change due now -- unit phase ends / completions, eps and CPU
 // completions, comm arrivals, releases -- until stable, then (B) executor choice, core dispatch,
 // unit dispatch; repeat until nothing changes.  Time then jumps to the earliest next event.
