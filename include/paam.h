@@ -23,9 +23,12 @@
  *     path computes in 32-bit integers with sums saturating just above the deadline, which is exact
  *     because any value above the deadline is a miss.
  *   - Indices inside a set are set-local (executor, accelerator, unit); CSR offset arrays are global.
- *   - All calls are asynchronous on the given CUDA stream unless stated otherwise; none of them
- *     synchronises the device except paam_pack with host-resident input (it must wait for the copy
- *     before it may free its staging buffers) and the query paam_sets_info.
+ *   - All calls are asynchronous on the given CUDA stream unless stated otherwise.  Exceptions that
+ *     synchronise the stream: paam_pack / paam_repack with host-resident input, paam_pack_analyze
+ *     with a host out_status, and paam_generate / paam_regenerate (they read the batch totals back to
+ *     size the arrays).
+ *   - Calls on one paam_sets handle share its work counters and staging buffers: order them (e.g.
+ *     issue them on one stream).  Different handles are independent.
  *   - The caller owns every input and output buffer.  The library owns the opaque paam_sets handle
  *     (device memory) until paam_free.
  *   - Return value: 0 = OK, negative = the whole call failed (PAAM_E*).  Per-set validation failures

@@ -201,7 +201,7 @@ extern "C" int paam_pack(const paam_batch* batch, paam_sets** out, int32_t* out_
   }
   e = cudaMalloc((void**)&s->rec, sizeof(Record) * (size_t)(batch->n_sets ? batch->n_sets : 1));
   if (e != cudaSuccess) {
-    std::free(s);
+    paam_free(s);  // releases the tickets
     return fail_cuda(e, "paam_pack: record cudaMalloc");
   }
   rc = paam_repack(batch, s, out_status, stream);
