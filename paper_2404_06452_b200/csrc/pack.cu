@@ -27,6 +27,7 @@ constexpr int WARPS = 4;
 #endif
 constexpr int kSegUnroll = PACK_SEG_UNROLL;  // segment loop of the callback pass: measured 1 (6.91 ms) < 4 < 3 < 2
 constexpr uint32_t FULL = 0xffffffffu;
+constexpr uint32_t MAXSEG = 192;  // segments per set (validation cap)
 
 struct Scratch {
   // chains by rank
@@ -47,14 +48,22 @@ struct Scratch {
   uint8_t xCore[MAXX], xWait[MAXX], xPPrank[MAXX];
   // accelerators
   uint32_t aN[4], aUnits[4], aUbase[4], aEps[4], aKeff[4], aServer[4];
-  // per (rank, unit) / (unit, rank)
-  alignas(16) uint32_t W[MAXC][MAXU];
-  uint32_t maxA[MAXU][MAXC];
-  union {  // WFD scratch is dead before pre2 is computed
-    uint32_t pre2[MAXU][MAXC];
+  union {
     struct {
-      uint64_t wfdU[MAXCB];
-      uint8_t wfdOrder[MAXCB], wfdUnit[MAXCB], wfdCb[MAXCB];
+      // per (rank, unit) / (unit, rank)
+      alignas(16) uint32_t W[MAXC][MAXU];
+      uint32_t maxA[MAXU][MAXC];
+      union {  // WFD scratch is dead before pre2 is computed
+        uint32_t pre2[MAXU][MAXC];
+        struct {
+          uint64_t wfdU[MAXCB];
+          uint8_t wfdOrder[MAXCB], wfdUnit[MAXCB], wfdCb[MAXCB];
+        };
+      };
+    };
+    struct {  // the set's segments, staged by coalesced loads; dead before WFD / W are written
+      uint64_t gW[MAXSEG];
+      uint8_t gKind[MAXSEG], gAcc[MAXSEG], gUnit[MAXSEG];
     };
   };
   uint32_t cmp[MAXC];
@@ -143,7 +152,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     bool st2 = !more, st3 = !more;
     int st = PAAM_SET_OK;
 
-    if (nch > MAXC || ncb > MAXCB || nseg > 192 || nex > MAXX || nac > 4) st = PAAM_SET_ERANGE;
+    if (nch > MAXC || ncb > MAXCB || nseg > MAXSEG || nex > MAXX || nac > 4) st = PAAM_SET_ERANGE;
     uint32_t n_aseg = 0, n_sub = 0, n_unit = 0;
     uint64_t runstart = 0;  // bit j: callback j starts a sub-chain
     uint64_t cstart = 0;    // bit j: callback j is the first of its chain
@@ -198,6 +207,17 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       cstart = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(cstart_bit >> 32)) << 32) |
                               __reduce_or_sync(FULL, (uint32_t)cstart_bit);
       __syncwarp();
+      // ---- segments: staged with coalesced loads (one round trip for the whole set) ------------------
+#ifndef PAAM_WARP_EMU
+#pragma unroll 2
+#endif
+      for (uint32_t i = lane; i < nseg; i += 32) {
+        s.gW[i] = b.seg_wcet[sg0 + i];
+        s.gKind[i] = b.seg_kind[sg0 + i];
+        s.gAcc[i] = b.seg_accel[sg0 + i];
+        s.gUnit[i] = b.seg_unit[sg0 + i];
+      }
+      __syncwarp();
       // ---- callbacks: two passes of 32 lanes; each lane walks its segments ----------------------
       uint32_t prev_exec = 0xffffffffu;
       for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
@@ -205,19 +225,20 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         uint32_t exec = 0xffffffffu, E = 0, na = 0, fa = 0, fu = 0, fw = 0;  // fa/fu/fw: first ACCEL segment
         if (j < ncb) {
           exec = b.cb_exec[cb0 + j];
-          const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
+          uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
           edang |= (se == so) || (exec >= nex);
+          if (so < sg0 || se < so || se > sg1) { edang = true; so = se = sg0; }  // malformed CSR: no staged reads
           uint32_t prev_kind = 0xffffffffu;
 #pragma unroll kSegUnroll
-          for (uint32_t k = so; k < se; k++) {
-            const uint32_t kind = b.seg_kind[k];
-            const uint64_t w = b.seg_wcet[k];
+          for (uint32_t k = so - sg0; k < se - sg0; k++) {
+            const uint32_t kind = s.gKind[k];
+            const uint64_t w = s.gW[k];
             erange |= (w >= LIM);
             eshape |= (kind > 1) || (w == 0) || (kind == prev_kind);
             prev_kind = kind;
             if (kind == 0) E = sadd(E, (uint32_t)w);  // w < LIM in a valid set: E stays exact
             if (kind == 1) {
-              const uint32_t a = b.seg_accel[k], u = b.seg_unit[k];
+              const uint32_t a = s.gAcc[k], u = s.gUnit[k];
               if (na == 0) { fa = a; fu = u; fw = (uint32_t)w; }
               na++;
               if (a >= nac) eaccel = true;
@@ -367,9 +388,9 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         if (s.bNa[j] == 1) {  // the common case: its one segment was kept by the callback pass
           put(s.bFa[j], s.bFu[j], s.bFw[j]);
         } else {
-          const uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
-          for (uint32_t k = so; k < se; k++)
-            if (b.seg_kind[k] == 1) put(b.seg_accel[k], b.seg_unit[k], (uint32_t)min(b.seg_wcet[k], (uint64_t)SAT));
+          const uint32_t so = b.cb_seg_off[cb0 + j] - sg0, se = b.cb_seg_off[cb0 + j + 1] - sg0;
+          for (uint32_t k = so; k < se; k++)  // the staged segments are intact until WFD / W
+            if (s.gKind[k] == 1) put(s.gAcc[k], s.gUnit[k], (uint32_t)min(s.gW[k], (uint64_t)SAT));
         }
       }
     }
