@@ -25,7 +25,11 @@ constexpr int WARPS = 4;
 #ifndef PACK_SEG_UNROLL
 #define PACK_SEG_UNROLL 1
 #endif
-constexpr int kSegUnroll = PACK_SEG_UNROLL;  // segment loop of the callback pass: measured 1 (6.91 ms) < 4 < 3 < 2
+constexpr int kSegUnroll = PACK_SEG_UNROLL;  // segment loop of the callback pass (measured: 1 < 3)
+#ifndef PACK_STAGE_UNROLL
+#define PACK_STAGE_UNROLL 2
+#endif
+constexpr int kStageUnroll = PACK_STAGE_UNROLL;  // coalesced segment staging loop (measured: 2 < 3 < 1 < 6)
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t MAXSEG = 192;  // segments per set (validation cap)
 
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       __syncwarp();
       // ---- segments: staged with coalesced loads (one round trip for the whole set) ------------------
 #ifndef PAAM_WARP_EMU
-#pragma unroll 2
+#pragma unroll kStageUnroll
 #endif
       for (uint32_t i = lane; i < nseg; i += 32) {
         s.gW[i] = b.seg_wcet[sg0 + i];
