@@ -215,7 +215,8 @@ int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_sta
  * PAAM_SIM_FIFO_DIRECT (the direct-invocation baseline the paper compares against).
  *   out_resp   [n_chains total] maximum observed end-to-end response time per chain (0 if none).
  *   out_count  [n_chains total] completed instances per chain (may be NULL).
- *   out_digest [n] order-independent FNV-1a-64 digest of the event records (may be NULL).
+ *   out_digest [n] order-independent FNV-1a-64 digest of the event records (may be NULL: the events
+ *              are then not hashed at all).
  *   bound      [n_chains total] WCRTs from paam_analyze, or NULL.  In every set whose CRITICAL
  *              chains all have bound <= D (the analysis' schedulable sets, Lemma 1), each
  *              CRITICAL chain with out_resp > bound adds 1 to *out_violations (int64, +=).

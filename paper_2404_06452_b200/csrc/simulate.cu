@@ -126,8 +126,9 @@ struct Ctx {
   uint64_t t, horizon, comm;
   uint64_t dig;  // this lane's partial digest
   bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
+  bool want_dig; // the caller asked for digests (out_digest != NULL); otherwise events are not hashed
   __device__ void ev(uint32_t kind, uint32_t c, uint32_t cb, uint32_t seg, uint32_t unit, uint32_t bk) {
-    dig += fnv_record(t, kind, S.cLocal[c], cb, seg, unit, bk);
+    if (want_dig) dig += fnv_record(t, kind, S.cLocal[c], cb, seg, unit, bk);
   }
   // executor x has phase-A work due now (a zero-length eps leaves it due right after it starts)
   __device__ bool exec_due(uint32_t x) const {
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     __syncwarp();
 
     const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
-    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo};
+    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr};
     uint32_t next_k = 0;  // lane = rank
     uint32_t seq = 0;     // warp-uniform
     bool on_core = false; // lane = canonical executor
