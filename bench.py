@@ -277,20 +277,19 @@ def run_ours(args):
                     "note": "paam_pack_analyze with PAAM_FLAG_VERDICT_ONLY: verdicts + bins only, analysis of a "
                             "set stops at its first CRITICAL deadline miss"}
 
-    # ---- e2e including device generation: paam_generate -> paam_pack_analyze -> D2H of the verdicts --
+    # ---- e2e including device generation: paam_sweep (generate -> pack -> analyze, chunked, generation
+    # overlapped with analysis) -> D2H of the verdicts and bins -----------------------------------------
     e2e_gen = None
     if not args.no_e2e:
         sched_g = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         bins_g = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
-
         gbins = torch.zeros_like(bins)
-        graw = paam.Raw(params, SEED, first, n, stream=stream)  # handle whose buffers every step reuses
+        sweeper = paam.Sweeper()
 
         def gen_step():
-            graw.regenerate(params, SEED, first, n, stream=stream)
             with torch.cuda.stream(stream):
                 gbins.zero_()
-            sets.pack_analyze(graw, None, sched, gbins, stream=stream)
+            sweeper.run(params, SEED, first, n, sched, gbins, stream=stream)
             if dist is not None:
                 allreduce_bins(gbins, stream=stream)
             with torch.cuda.stream(stream):
@@ -306,9 +305,11 @@ def run_ours(args):
         gen_s = max_over_ranks(time.perf_counter() - t0, world)
         e2e_gen = {"value": world * n * args.steps / gen_s, "unit": "chain-sets/s", "ms_per_step": 1e3 * gen_s / args.steps,
                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
-                   "note": "host wall clock per step: paam_regenerate (device generation into a reused handle) + "
-                           "paam_pack_analyze + D2H of verdicts and bins"}
-        graw.free()
+                   "note": "host wall clock per step: paam_sweep (device generation of 256k-set chunks overlapped "
+                           "with pack + analyze of the previous chunk) + D2H of verdicts and bins"}
+        if sum(bins_g.tolist()[0::2]) != world * n:
+            raise RuntimeError("paam_sweep bin totals do not match the sets")
+        sweeper.free()
     sets.pack_analyze(raw, wcrt, sched, vbins, stream=stream)  # the handle again describes `raw` (DES leg)
     stream.synchronize()
 

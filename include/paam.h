@@ -165,6 +165,20 @@ int paam_generate(const paam_gen_params* params, uint64_t seed, uint64_t first_i
 int paam_regenerate(paam_raw* raw, const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
                     uint64_t comm_cost, uint32_t flags, paam_stream_t stream);
 int paam_raw_batch(const paam_raw* raw, paam_batch* out);
+
+/* paam_sweep -- §8(a) steps 1-6 as one device-resident sweep over sets [first_index, first_index + n)
+ * of the stream `seed`: chunks of `chunk` sets (paam_sweep_create) are generated, packed and analysed,
+ * the generation of chunk i+1 overlapping the pack + analysis of chunk i on two internal streams;
+ * the raw batches are laid out at the generator's per-set upper bounds, so nothing is read back to
+ * the host and the call never synchronises.  Outputs: out_sched [n] (device, may be NULL) and
+ * out_bins [n_bins*2] (device, ACCUMULATED, may be NULL); no WCRTs (flags as paam_batch.flags,
+ * PAAM_FLAG_VERDICT_ONLY allowed).  The same verdicts and bins as paam_generate + paam_pack_analyze.
+ * Errors: PAAM_EINVAL for bad parameters or a chunk whose capacity exceeds 32-bit offsets. */
+typedef struct paam_sweeper paam_sweeper;
+int paam_sweep_create(uint32_t chunk, paam_sweeper** out);
+int paam_sweep(paam_sweeper* sweeper, const paam_gen_params* params, uint64_t seed, uint64_t first_index, uint32_t n,
+               uint64_t comm_cost, uint32_t flags, uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream);
+void paam_sweep_free(paam_sweeper* sweeper);
 void paam_raw_free(paam_raw* raw);
 
 /* paam_pack -- §8(a) step 2.  Validates every set and derives the per-set record the analysis and

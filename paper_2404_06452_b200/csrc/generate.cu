@@ -351,9 +351,21 @@ using namespace paam;
 namespace paam {
 namespace {
 
+// Per-set upper bounds of the generator's sizes {chains, callbacks, segments, executors, accelerators}.
+void size_caps(const pg_params& p, uint64_t cap[5]) {
+  cap[0] = p.m_hi;
+  cap[1] = (uint64_t)p.m_hi * p.cbs_per_chain;
+  cap[2] = 3ull * p.m_hi * p.cbs_per_chain;
+  cap[3] = p.exec_mode == 0 ? p.m_hi : p.n_exec;
+  cap[4] = p.n_accel;
+}
+
 // Generate into `raw`, reusing its device buffers when the new batch fits (paam_regenerate).
+// cap_sets > 0: lay the arrays out for cap_sets sets at the generator's per-set upper bounds instead
+// of reading the totals back -- no host synchronisation (paam_sweep); the batch's totals are then
+// those capacities, which no kernel reads.
 int generate_into(paam_raw* raw, const pg_params& p, uint64_t seed, uint64_t first_index, uint32_t n,
-                  uint64_t comm_cost, uint32_t flags, cudaStream_t st) {
+                  uint64_t comm_cost, uint32_t flags, cudaStream_t st, uint32_t cap_sets = 0) {
   cudaError_t e;
   // pass 1: sizes, then offsets (scratch: cnt[5n], offs[5(n+1)], scan temporaries)
   const size_t nn = (size_t)n + 1;
@@ -374,20 +386,27 @@ int generate_into(paam_raw* raw, const pg_params& p, uint64_t seed, uint64_t fir
   }
   for (int k = 0; k < 5; k++) scan(cnt + (size_t)k * n, offs + (size_t)k * nn, n, tmp, st);
   uint32_t tot[5];
-  for (int k = 0; k < 5; k++)
-    cudaMemcpyAsync(&tot[k], offs + (size_t)k * nn + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_generate: sizes");
+  if (cap_sets) {
+    uint64_t cap[5];
+    size_caps(p, cap);
+    for (int k = 0; k < 5; k++) tot[k] = (uint32_t)(cap[k] * cap_sets);
+  } else {
+    for (int k = 0; k < 5; k++)
+      cudaMemcpyAsync(&tot[k], offs + (size_t)k * nn + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_generate: sizes");
+  }
 
   // one allocation for every array of the raw batch
   const uint32_t nch = tot[0], ncb = tot[1], nsg = tot[2], nex = tot[3], nac = tot[4];
+  const size_t nset = cap_sets ? (size_t)cap_sets + 1 : nn;
   struct Part { size_t elems, size; } parts[] = {
-      {nn, 4}, {nn, 4}, {nn, 4},                                  // set offsets
+      {nset, 4}, {nset, 4}, {nset, 4},                            // set offsets
       {nch, 8}, {nch, 8}, {nch, 4}, {nch, 1}, {(size_t)nch + 1, 4},  // chains
       {ncb, 2}, {(size_t)ncb + 1, 4},                              // callbacks
       {nsg, 1}, {nsg, 8}, {nsg, 1}, {nsg, 1},                      // segments
       {nex, 1}, {nex, 4}, {nex, 1},                                // executors
       {nac, 1}, {nac, 1}, {nac, 1}, {nac, 8}, {nac, 8},            // accelerators
-      {n, 4}};                                                     // set_bin
+      {nset, 4}};                                                  // set_bin
   constexpr int NP = sizeof(parts) / sizeof(parts[0]);
   size_t off[NP], bytes = 0;
   for (int i = 0; i < NP; i++) { off[i] = bytes; bytes += align256(parts[i].elems * parts[i].size + 1); }
@@ -496,4 +515,98 @@ extern "C" void paam_raw_free(paam_raw* raw) {
   if (raw->buf) cudaFree(raw->buf);
   if (raw->scr) cudaFree(raw->scr);
   std::free(raw);
+}
+
+// ---- paam_sweep: steps 1-6 over device-generated chunks, generation overlapped with analysis ------
+struct paam_sweeper {
+  uint32_t chunk;
+  paam_raw raw[2];          // capacity-laid-out raw batches (ping-pong)
+  paam::Record* rec[2];     // packed records of the chunk being analysed
+  unsigned int* tickets;    // analyze work counters, one per buffer
+  cudaStream_t sg, sa;      // generation / pack + analysis
+  cudaEvent_t start, gen_done[2], ana_done[2], join[2];
+  int device;
+};
+
+extern "C" int paam_sweep_create(uint32_t chunk, paam_sweeper** out) {
+  if (!out || chunk == 0) return fail(PAAM_EINVAL, "paam_sweep_create: NULL out or chunk == 0");
+  *out = nullptr;
+  paam_sweeper* h = (paam_sweeper*)std::calloc(1, sizeof(paam_sweeper));
+  if (!h) return fail(PAAM_ENOMEM, "paam_sweep_create: host allocation");
+  h->chunk = chunk;
+  cudaError_t e = cudaGetDevice(&h->device);
+  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+    h->raw[i].device = h->device;
+    e = cudaMalloc((void**)&h->rec[i], sizeof(paam::Record) * (size_t)chunk);
+  }
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->tickets, sizeof(unsigned int) * 2);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sg, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sa, cudaStreamNonBlocking);
+  cudaEvent_t* evs[7] = {&h->start, &h->gen_done[0], &h->gen_done[1], &h->ana_done[0], &h->ana_done[1], &h->join[0], &h->join[1]};
+  for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    paam_sweep_free(h);
+    return fail_cuda(e, "paam_sweep_create");
+  }
+  *out = h;
+  return PAAM_OK;
+}
+
+extern "C" int paam_sweep(paam_sweeper* h, const paam_gen_params* params, uint64_t seed, uint64_t first_index,
+                          uint32_t n, uint64_t comm_cost, uint32_t flags, uint8_t* out_sched, int64_t* out_bins,
+                          paam_stream_t stream) {
+  if (!h) return fail(PAAM_EINVAL, "paam_sweep: NULL handle");
+  if (flags & ~(PAAM_FLAG_BLOCKING_SOUND | PAAM_FLAG_WFD_UNITS | PAAM_FLAG_VERDICT_ONLY))
+    return fail(PAAM_EINVAL, "paam_sweep: unknown flag");
+  pg_params p;
+  if (int rc = check_gen_args(params, comm_cost, &p)) return rc;
+  {
+    uint64_t cap[5];
+    size_caps(p, cap);
+    for (int k = 0; k < 5; k++)
+      if (cap[k] * h->chunk >= (1ull << 32)) return fail(PAAM_EINVAL, "paam_sweep: chunk too large for 32-bit offsets");
+  }
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) return fail_cuda(e, "paam_sweep: cudaSetDevice");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEventRecord(h->start, st);
+  cudaStreamWaitEvent(h->sg, h->start, 0);
+  cudaStreamWaitEvent(h->sa, h->start, 0);
+  const uint32_t nchunks = (n + h->chunk - 1) / h->chunk;
+  for (uint32_t i = 0; i < nchunks; i++) {
+    const int bi = i & 1;
+    const uint32_t lo = i * h->chunk, cnt = n - lo < h->chunk ? n - lo : h->chunk;
+    if (i >= 2) cudaStreamWaitEvent(h->sg, h->ana_done[bi], 0);  // buffers of chunk i-2 consumed
+    if (int rc = generate_into(&h->raw[bi], p, seed, first_index + lo, cnt, comm_cost, flags, h->sg, h->chunk)) return rc;
+    cudaEventRecord(h->gen_done[bi], h->sg);
+    cudaStreamWaitEvent(h->sa, h->gen_done[bi], 0);
+    if (int rc = launch_pack(&h->raw[bi].b, h->rec[bi], nullptr, h->sa)) return rc;
+    if (int rc = launch_analyze(h->rec[bi], cnt, comm_cost, flags, p.n_bins, nullptr, out_sched ? out_sched + lo : nullptr,
+                                p.n_bins ? out_bins : nullptr, h->tickets + bi, h->sa))
+      return rc;
+    cudaEventRecord(h->ana_done[bi], h->sa);
+  }
+  cudaEventRecord(h->join[0], h->sg);
+  cudaEventRecord(h->join[1], h->sa);
+  cudaStreamWaitEvent(st, h->join[0], 0);
+  cudaStreamWaitEvent(st, h->join[1], 0);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "paam_sweep");
+}
+
+extern "C" void paam_sweep_free(paam_sweeper* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < 2; i++) {
+    if (h->raw[i].buf) cudaFree(h->raw[i].buf);
+    if (h->raw[i].scr) cudaFree(h->raw[i].scr);
+    if (h->rec[i]) cudaFree(h->rec[i]);
+  }
+  if (h->tickets) cudaFree(h->tickets);
+  if (h->sg) cudaStreamDestroy(h->sg);
+  if (h->sa) cudaStreamDestroy(h->sa);
+  cudaEvent_t evs[7] = {h->start, h->gen_done[0], h->gen_done[1], h->ana_done[0], h->ana_done[1], h->join[0], h->join[1]};
+  for (int i = 0; i < 7; i++) if (evs[i]) cudaEventDestroy(evs[i]);
+  std::free(h);
 }

@@ -79,6 +79,10 @@ def lib():
         L.paam_regenerate.argtypes = [_vp, ctypes.POINTER(PaamGenParams), ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _vp]
         L.paam_raw_batch.argtypes = [_vp, ctypes.POINTER(PaamBatch)]
+        L.paam_sweep_create.argtypes = [ctypes.c_uint32, ctypes.POINTER(_vp)]
+        L.paam_sweep.argtypes = [_vp, ctypes.POINTER(PaamGenParams), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                                 ctypes.c_uint64, ctypes.c_uint32, _vp, _vp, _vp]
+        L.paam_sweep_free.argtypes = [_vp]
         L.paam_raw_free.argtypes = [_vp]
         L.paam_raw_free.restype = None
         L.paam_pack.argtypes = [ctypes.POINTER(PaamBatch), ctypes.POINTER(_vp), _vp, _vp]
@@ -292,6 +296,33 @@ class Sets:
     def free(self):
         if self.h:
             lib().paam_free(self.h)
+            self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Sweeper:
+    """paam_sweep: generate -> pack -> analyse over device-generated chunks, generation overlapped with
+    analysis, no host synchronisation (§8(a) steps 1-6)."""
+
+    def __init__(self, chunk: int = 262_144):
+        self.h = _vp()
+        set_device_from_torch()
+        check(lib().paam_sweep_create(chunk, ctypes.byref(self.h)), "paam_sweep_create")
+
+    def run(self, params: PaamGenParams, seed: int, first: int, n: int, out_sched=None, out_bins=None,
+            comm_cost=100_000, flags=0, stream=None):
+        ptr = lambda t: None if t is None else t.data_ptr()
+        check(lib().paam_sweep(self.h, ctypes.byref(params), seed, first, n, comm_cost, flags, ptr(out_sched),
+                               ptr(out_bins), _stream_ptr(stream)), "paam_sweep")
+
+    def free(self):
+        if self.h:
+            lib().paam_sweep_free(self.h)
             self.h = _vp()
 
     def __del__(self):

@@ -86,3 +86,26 @@ def test_verdict_only_rejects_wcrt_output_and_admit_ignores_it():
     sets0.admit(dec)
     torch.cuda.synchronize()
     assert torch.equal(dec, dec_vo)
+
+
+@pytest.mark.parametrize("flags", [0, paam.PAAM_FLAG_BLOCKING_SOUND, VO])
+def test_sweep_matches_generate_pack_analyze(flags):
+    """paam_sweep (device-generated chunks, generation overlapped with analysis, capacity layout) gives
+    the verdicts and bins of paam_generate + paam_pack_analyze, over a ragged range of chunks."""
+    p = config3_params()
+    n, first = 300_001, 12_345
+    dev = torch.device("cuda")
+    sw = paam.Sweeper(chunk=65_536)
+    sched_s = torch.full((n,), 7, dtype=torch.uint8, device=dev)
+    bins_s = torch.zeros(2 * p.n_bins, dtype=torch.int64, device=dev)
+    sw.run(paam.PaamGenParams.from_buffer_copy(bytes(p)), 4, first, n, sched_s, bins_s, flags=flags)
+    sw.run(paam.PaamGenParams.from_buffer_copy(bytes(p)), 4, first, n, None, bins_s, flags=flags)  # reuse: bins x2
+    raw = paam.Raw(paam.PaamGenParams.from_buffer_copy(bytes(p)), 4, first, n, flags=flags)
+    sets = paam.Sets(raw)
+    sched = torch.full((n,), 9, dtype=torch.uint8, device=dev)
+    bins = torch.zeros(2 * p.n_bins, dtype=torch.int64, device=dev)
+    sets.pack_analyze(raw, None, sched, bins)
+    torch.cuda.synchronize()
+    assert torch.equal(sched_s, sched)
+    assert torch.equal(bins_s, 2 * bins)
+    sw.free()
