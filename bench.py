@@ -412,6 +412,9 @@ def run_ours(args):
                 "kernel": "analyze_kernel", "kernel_ms": ana_avg, "ops_per_set": work["mu_regrouped_per_set"] * OPS_PER_MU,
                 "peak_source": "derived: 148 SMs x 128 int32 lanes/clk (B300_MICROARCH alu+fma pipes) x 1.965 GHz",
                 "hbm_achieved_GBps": (rec_bytes * n) / (ana_avg / 1e3) / 1e9}
+    issue = ncu_issue_stats()
+    pack_roof["ncu_issue"] = issue.get("pack_kernel")
+    ana_roof["ncu_issue"] = issue.get("analyze_kernel")
     dominant = pack_roof if pack_avg >= ana_avg else ana_roof
     other = ana_roof if dominant is pack_roof else pack_roof
     roof = dict(dominant)
@@ -459,12 +462,23 @@ def work_per_set(gp, first, sample=4000):
 
 
 def measured_traffic_per_set():
-    """dram bytes per set of analyze_kernel from the committed ncu --set full capture, if present."""
+    """DRAM bytes per set of each kernel from the committed ncu --set full capture, if present."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         return {k: float(v["dram_bytes_per_set"]) for k, v in d.items() if not k.startswith("_")}
     except Exception:
         return None
+
+
+def ncu_issue_stats():
+    """Issue-slot utilisation and warp instructions per set of each kernel (same committed capture)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return {k: {"issue_active_pct": v.get("issue_active_pct"), "warp_inst_per_set": v.get("warp_inst_per_set"),
+                    "source": "profiles/traffic.json (ncu --set full, profiles/r01_ncu_full_v9_summary.txt)"}
+                for k, v in d.items() if not k.startswith("_")}
+    except Exception:
+        return {}
 
 
 def main():
