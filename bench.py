@@ -160,12 +160,20 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"config-3 recipe, seed {SEED}, {per_step} sets per step (bounded sample)",
-                      "sets_per_step": per_step},
+           "config": {"workload": workload_name(args.sets_per_gpu), "sets_per_gpu": args.sets_per_gpu,
+                      "global_sets": world * args.sets_per_gpu, "seed": SEED,
+                      "reference_sample": f"each step analyses {per_step} sets of that workload (bounded so the "
+                                          f"run ends within minutes); value is sets/s over the sampled sets"},
            "cpu_baseline": {"value": v, "unit": "chain-sets/s", "cores": nthreads, "kind": "oracle",
                             "sample": f"{per_step} sets per step x {args.steps} steps"},
            "e2e": {"value": v, "unit": "chain-sets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def workload_name(n: int) -> str:
+    """The bench workload (both arms): config-3 recipe, n sets per GPU, set-index shards."""
+    return (f"config-3 recipe (m 8-16 chains x 4 callbacks, GPU-like n=6 + TPU-like n=1, 9 utilisation bins), "
+            f"{n} sets/GPU, seed {SEED}, rank r owns [r*{n}, (r+1)*{n}) -- N=8 is config 4 (16M sets)")
 
 
 def batch_bytes(c) -> int:
@@ -426,10 +434,7 @@ def run_ours(args):
     out = {"metric": METRIC, "value": value, "unit": "chain-sets/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-           "config": {"workload": f"config-3 recipe (m 8-16 chains x 4 callbacks, GPU-like n=6 + TPU-like n=1, "
-                                  f"9 utilisation bins), {n} sets/GPU, seed {SEED}, rank r owns "
-                                  f"[r*{n}, (r+1)*{n}) -- N=8 is config 4 (16M sets)",
-                      "sets_per_gpu": n, "global_sets": world * n, "seed": SEED,
+           "config": {"workload": workload_name(n), "sets_per_gpu": n, "global_sets": world * n, "seed": SEED,
                       "l2": f"inputs larger than L2: {(in_bytes + rec_bytes * n) / 1e9:.1f} GB/GPU resident",
                       "parallelism": f"dp{world} (set-index shards, NCCL all-reduce of bin counts)"},
            "gpu_launches": int(launches), "clocks": clk, "roofline": roof, "roofline_other_kernel": other,
