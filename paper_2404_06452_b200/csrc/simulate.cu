@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
     Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr};
     uint32_t next_k = 0;  // lane = rank
+    uint64_t next_rel = (uint32_t)lane < nch ? S.cPhase[lane] : NONE64;  // release time of instance next_k (D2)
     uint32_t seq = 0;     // warp-uniform
     bool on_core = false; // lane = canonical executor
     uint32_t drops = 0, ovf = 0;
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               const uint32_t q = slot_of(tm);
               if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; }
             }
-            const uint64_t r = S.cPhase[c] + (uint64_t)next_k * S.cT[c];
+            const uint64_t r = next_rel;
             if (r == C.t && r < horizon) {
               if (S.cCls[c] == 1)
                 for (uint32_t dm = slots_eq(S.iState[c], I_READY) & slots_eq(S.iCb[c], 0); dm; dm &= dm - 1) {
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
                 C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
               }
               next_k++;
+              next_rel += S.cT[c];
              
             }
           }
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       // ===================== advance time =====================
       uint64_t nt = NONE64;
       if (is_chain) {
-        const uint64_t r = S.cPhase[lane] + (uint64_t)next_k * S.cT[lane];
+        const uint64_t r = next_rel;
         if (r < horizon) nt = r;
         for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
           nt = min(nt, S.iw[lane][slot_of(tm)].ready_at);
