@@ -34,6 +34,7 @@ struct __align__(16) WarpSmem {
   uint32_t Hs[MAXS];   // H*_c(R_c) of every solved sub-chain
   unsigned long long sum[MAXC];  // end-to-end accumulation per chain
   uint32_t uns[MAXC];
+  uint8_t gpos[MAXS + 1];  // first canonical sub-chain of each core group, then n_sub
 };
 
 constexpr uint32_t FULL = 0xffffffffu;
@@ -181,15 +182,17 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const uint32_t prev_core = __shfl_up_sync(FULL, my_core, 1);
       const uint32_t gstart = __ballot_sync(FULL, is_sub && (lane == 0 || my_core != prev_core));
       const uint32_t ngroups = __popc(gstart);
+      if ((gstart >> lane) & 1u) w.gpos[__popc(gstart & ((1u << lane) - 1u))] = (uint8_t)lane;
+      if (lane == 0) w.gpos[ngroups] = (uint8_t)nsub;
+      __syncwarp();
       const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
       bool miss = false;  // verdict-only: a CRITICAL sub-chain already exceeded its deadline
       for (uint32_t gb = 0; gb < ngroups && !miss; gb += 4) {
         const uint32_t grp = gb + gi;
         uint32_t g0 = 0, glen = 0;
         if (grp < ngroups) {
-          g0 = __fns(gstart, 0, grp + 1);
-          const uint32_t rest = gstart & ~((2u << g0) - 1u);
-          glen = (rest ? (uint32_t)__ffs(rest) - 1u : nsub) - g0;
+          g0 = w.gpos[grp];
+          glen = w.gpos[grp + 1] - g0;
         }
         const uint32_t maxlen = __reduce_max_sync(FULL, glen);
         for (uint32_t pos = 0; pos < maxlen; pos++) {
