@@ -77,6 +77,10 @@ struct Scratch {
 };
 
 
+// 2^16 / d + 1 for 1 <= d <= 32 (n of an accelerator, bucket group size g); warp-uniform index
+__constant__ uint32_t kInv16[33] = {0u, 65537u, 32769u, 21846u, 16385u, 13108u, 10923u, 9363u, 8193u, 7282u, 6554u, 5958u, 5462u, 5042u, 4682u, 4370u, 4097u, 3856u, 3641u, 3450u, 3277u, 3121u, 2979u, 2850u, 2731u, 2622u, 2521u, 2428u, 2341u, 2260u, 2185u, 2115u, 2049u};
+__device__ __forceinline__ uint32_t inv16(uint32_t d) { return kInv16[d]; }
+
 // saturating inclusive prefix sum over lanes (Hillis-Steele; min(a+b, SAT) is associative on [0, SAT])
 __device__ __forceinline__ uint32_t scan_sat_incl(uint32_t v, int lane) {
 #pragma unroll
@@ -421,8 +425,9 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     for (uint32_t a = 0; a < nac; a++) {
       const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
       const uint32_t ma = __popc(U), n = s.aN[a];
-      const uint32_t g = ma ? (ma + n - 1) / n : 1u;
-      const uint32_t ginv = (1u << 16) / g + 1u;  // (p * ginv) >> 16 == p / g for p < 64, g <= 32
+      // x / d == (x * (2^16 / d + 1)) >> 16 for x < 64, 1 <= d <= 32 (checked exhaustively): no divides
+      const uint32_t g = ma ? ((ma + n - 1) * inv16(n)) >> 16 : 1u;
+      const uint32_t ginv = inv16(g);
       const bool user = (U >> lane) & 1u;
       const uint32_t p = __popc(U & lt);  // position among users in rank order
       // users of a form aligned blocks of g consecutive positions, one block per bucket: the user at

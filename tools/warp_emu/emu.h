@@ -23,6 +23,7 @@
 #define __restrict__ __restrict
 #define __align__(n) alignas(n)
 #define __shared__ static
+#define __constant__
 
 struct dim3emu { unsigned x = 0, y = 0, z = 0; };
 inline thread_local dim3emu threadIdx, blockIdx;
