@@ -38,6 +38,19 @@ __global__ void gen_sizes_kernel(pg_params p, uint64_t seed, uint64_t first, uin
 }
 
 constexpr int GW = 4;  // warps per block of the fill kernel
+
+// floor(x / d), exactly, without the 64-bit integer divide routine when both operands are exact
+// doubles: the correctly rounded double quotient is within 1 of the true one, and one integer step
+// corrects it.
+__device__ __forceinline__ uint64_t udiv64(uint64_t x, uint64_t d) {
+  if (x < (1ull << 52) && d < (1ull << 52)) {
+    uint64_t q = (uint64_t)__ddiv_rn((double)x, (double)d);
+    if (q * d > x) q--;
+    else if ((q + 1) * d <= x) q++;
+    return q;
+  }
+  return x / d;
+}
 constexpr uint32_t FULL = 0xffffffffu;
 
 struct GenWarp {
@@ -67,6 +80,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
   GenWarp& w = smem[threadIdx.x >> 5];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t K = p.cbs_per_chain;
+  const uint32_t invK = 65536u / K + 1u;  // cb / K == (cb * invK) >> 16 for cb < 64, K <= 32 (exhaustive check)
   const uint32_t units[PG_MAX_ACCEL] = {p.units[0], p.units[1], p.units[2], p.units[3]};
   for (uint32_t i = blockIdx.x * GW + (threadIdx.x >> 5); i < n; i += gridDim.x * GW) {
     const uint64_t index = first + i;
@@ -103,7 +117,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
       T = t_us * 1000ull;
     }
     const uint64_t C = (share * T) >> 20;
-    const uint64_t base = C / K, rem = C % K;
+    const uint64_t base = udiv64(C, K), rem = C - base * K;
 
     // callbacks (lane = callback, passes of 32): budget, segments, accelerator and unit draws
     const uint32_t ncb = m * K;
@@ -111,7 +125,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
     for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
       const uint32_t cb = pass * 32 + lane;
       const bool iscb = cb < ncb;
-      const uint32_t c = iscb ? cb / K : 0u, j = iscb ? cb - c * K : 0u;
+      const uint32_t c = iscb ? (cb * invK) >> 16 : 0u, j = iscb ? cb - c * K : 0u;
       const uint64_t bc = __shfl_sync(FULL, base, c), rc = __shfl_sync(FULL, rem, c);
       const uint64_t budget = bc + (j < rc ? 1 : 0);
       uint32_t nseg = 0, acc = 0, unit = 0;
@@ -122,7 +136,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
           w0 = budget ? budget : 1;
           atomicAdd((unsigned long long*)&w.ccpu[c], (unsigned long long)w0);
         } else {
-          uint64_t A = budget * p.ratio_acc / (p.ratio_acc + p.ratio_cpu);
+          uint64_t A = udiv64(budget * p.ratio_acc, (uint32_t)(p.ratio_acc + p.ratio_cpu));
           uint64_t E = budget - A;
           uint64_t e1 = E / 2, e2 = E - E / 2;
           nseg = 3;
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
     const uint32_t n_be = (uint32_t)(((uint64_t)m * p.be_frac_q16) >> 16);
 
     // CPU utilisation and the worst-fit order (utilisation desc, index asc)
-    const uint64_t util = isc ? (w.ccpu[lane] << 20) / T : 0ull;
+    const uint64_t util = isc ? udiv64(w.ccpu[lane] << 20, T) : 0ull;
     {
       uint32_t rk = 0;
       for (uint32_t d = 0; d < m; d++) {
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(GW * 32) gen_fill_kernel(pg_params p, uint64_t
       o.chain_cb_off[ch0 + lane] = cb0 + lane * K;
     }
     for (uint32_t cb = lane; cb < ncb; cb += 32) {
-      const uint32_t c = cb / K, j = cb - c * K;
+      const uint32_t c = (cb * invK) >> 16, j = cb - c * K;
       uint32_t x;
       if (p.exec_mode == 0) x = c;
       else x = (w.split[c] && j >= (K + 1) / 2) ? w.second[c] : w.best[c];
