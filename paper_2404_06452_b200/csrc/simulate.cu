@@ -521,11 +521,22 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           if (__any_sync(FULL, oc != on_core)) chB = true;
           on_core = oc;
         }
-        // (7) unit dispatch (D8-D11)
-        for (uint32_t u = 0; u < n_unit; u++) {
+        // (7) unit dispatch (D8-D11).  Lane u decides whether unit u has anything to dispatch (queue
+        // occupancy, state); only those units are visited (dispatch on one unit changes no other's).
+        uint32_t umask;
+        {
+          bool cand = false;
+          if (is_unit) {
+            const uint32_t ust = S.unState[lane], q = S.uQ[lane];
+            cand = fifo ? (ust == U_IDLE && q > 0)
+                        : ((ust == U_IDLE && q > 0) || (ust == U_RUN && S.uN[lane] > 1 && q > 1));
+          }
+          umask = __ballot_sync(FULL, cand);
+        }
+        for (; umask; umask &= umask - 1) {
+          const uint32_t u = __ffs(umask) - 1;
           const uint32_t ust = S.unState[u];
           if (fifo) {  // FIFO_DIRECT: an idle unit starts the oldest request; never preempts
-            if (ust != U_IDLE || S.uQ[u] == 0) continue;
             uint32_t myseq = 0xffffffffu;
             int fslot = -1;
             if (is_chain)
@@ -549,8 +560,6 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             __syncwarp();
             continue;
           }
-          if (ust != U_IDLE && !(ust == U_RUN && S.uN[u] > 1)) continue;
-          if (S.uQ[u] <= (ust == U_RUN ? 1u : 0u)) continue;  // nothing queued besides the running request
           // best waiting request on u, excluding the running one: key = bucket | started | priority
           uint32_t key = 0;
           int bslot = -1;
