@@ -96,12 +96,22 @@ struct DesSmem {
   uint32_t cnt[MAXC];
 };
 
-__device__ __forceinline__ uint64_t fnv_record(uint64_t t, uint32_t kind, uint32_t chain, uint32_t cb, uint32_t seg,
-                                               uint32_t unit, uint32_t bk) {
+// FNV-1a-64 of a 32-byte event record (D17) in two parts: the state after the record's 8-byte time
+// (the same for every record of a timestamp, so computed once per timestamp), then the 24 other bytes.
+__device__ __forceinline__ uint64_t fnv_time(uint64_t t) {
   uint64_t h = 0xcbf29ce484222325ull;
-  const uint32_t w[8] = {(uint32_t)t, (uint32_t)(t >> 32), kind, chain, cb, seg, unit, bk};
 #pragma unroll
-  for (int i = 0; i < 8; i++)
+  for (int b = 0; b < 8; b++) {
+    h ^= (t >> (8 * b)) & 0xffu;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+__device__ __forceinline__ uint64_t fnv_rest(uint64_t h, uint32_t kind, uint32_t chain, uint32_t cb, uint32_t seg,
+                                             uint32_t unit, uint32_t bk) {
+  const uint32_t w[6] = {kind, chain, cb, seg, unit, bk};
+#pragma unroll
+  for (int i = 0; i < 6; i++)
 #pragma unroll
     for (int b = 0; b < 4; b++) {
       h ^= (w[i] >> (8 * b)) & 0xffu;
@@ -127,8 +137,9 @@ struct Ctx {
   uint64_t dig;  // this lane's partial digest
   bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
   bool want_dig; // the caller asked for digests (out_digest != NULL); otherwise events are not hashed
+  uint64_t th;   // FNV-1a state after the 8 bytes of t (kept current only when want_dig)
   __device__ void ev(uint32_t kind, uint32_t c, uint32_t cb, uint32_t seg, uint32_t unit, uint32_t bk) {
-    if (want_dig) dig += fnv_record(t, kind, S.cLocal[c], cb, seg, unit, bk);
+    if (want_dig) dig += fnv_rest(th, kind, S.cLocal[c], cb, seg, unit, bk);
   }
   // executor x has phase-A work due now (a zero-length eps leaves it due right after it starts)
   __device__ bool exec_due(uint32_t x) const {
@@ -347,7 +358,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     __syncwarp();
 
     const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
-    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr};
+    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr, fnv_time(0)};
     uint32_t next_k = 0;  // lane = rank
     uint64_t next_rel = (uint32_t)lane < nch ? S.cPhase[lane] : NONE64;  // release time of instance next_k (D2)
     uint32_t seq = 0;     // warp-uniform
@@ -657,6 +668,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       if (is_exec && on_core && (S.exPhase[lane] == P_CPU || S.exPhase[lane] == P_EPS_SPIN)) S.exRem[lane] -= dt;
       if (is_unit && S.unState[lane] == U_RUN) S.unRem[lane] -= dt;
       C.t = nt;
+      if (C.want_dig) C.th = fnv_time(nt);
       __syncwarp();
     }
 
