@@ -107,17 +107,25 @@ __device__ __forceinline__ uint64_t fnv_time(uint64_t t) {
   }
   return h;
 }
+// One 4-byte field.  Every field of a record is either FULL (a compile-time constant at its call
+// site) or below 256, whose three zero bytes only multiply: (h ^ v) * P^4 (mod 2^64), one product.
+__device__ __forceinline__ uint64_t fnv_field(uint64_t h, uint32_t v) {
+  constexpr uint64_t P = 0x100000001b3ull, P4 = 0x9ffaac085635bc91ull;  // P^4 mod 2^64
+  if (v == 0xffffffffu) {
+#pragma unroll
+    for (int b = 0; b < 4; b++) h = (h ^ 0xffu) * P;
+    return h;
+  }
+  return (h ^ v) * P4;  // v < 256 at every call site (kind, set-local chain / callback / segment, unit, bucket)
+}
 __device__ __forceinline__ uint64_t fnv_rest(uint64_t h, uint32_t kind, uint32_t chain, uint32_t cb, uint32_t seg,
                                              uint32_t unit, uint32_t bk) {
-  const uint32_t w[6] = {kind, chain, cb, seg, unit, bk};
-#pragma unroll
-  for (int i = 0; i < 6; i++)
-#pragma unroll
-    for (int b = 0; b < 4; b++) {
-      h ^= (w[i] >> (8 * b)) & 0xffu;
-      h *= 0x100000001b3ull;
-    }
-  return h;
+  h = fnv_field(h, kind);
+  h = fnv_field(h, chain);
+  h = fnv_field(h, cb);
+  h = fnv_field(h, seg);
+  h = fnv_field(h, unit);
+  return fnv_field(h, bk);
 }
 
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {

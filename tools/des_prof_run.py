@@ -10,5 +10,6 @@ raw = paam.Raw(pp, 3, 0, n); sets = paam.Sets(raw)
 dev = torch.device("cuda")
 w = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev); sets.analyze(w, None, None)
 resp = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
-sets.simulate(10_000_000_000, 3, resp, None, None, w, None)
+dig = torch.empty(n, dtype=torch.int64, device=dev) if os.environ.get("DES_DIGEST") else None
+sets.simulate(10_000_000_000, 3, resp, None, dig, w, None)
 torch.cuda.synchronize(); print("ok")
