@@ -15,6 +15,10 @@
 // Mapping: lane = chain (ranked), lane = callback (two passes of 32), lane = sub-chain; relations are
 // 32/64-bit masks built with ballot / match / warp reductions; the bucket LP-blocking maximum is a
 // segmented suffix-max scan over the users of each unit (buckets are aligned blocks in rank order).
+// Memory: sets are assigned to warps in contiguous blocks, so each set's CSR start offsets are the
+// previous set's end offsets (its dependent offset loads are software-pipelined one set ahead); a
+// set's segments are staged into shared memory with coalesced loads, into scratch that is dead until
+// the W / WFD phase, and no integer divide runs per set (bucket sizes come from a reciprocal table).
 #include "common.cuh"
 
 namespace paam {
