@@ -55,6 +55,36 @@ __device__ __forceinline__ bool gor8(bool p) {
   return v != 0;
 }
 
+// Lemma 2 (Eq.3) for accelerator segment i: the least fixed point of
+// G(h) = aBase2 + sum_{k<r} floor((h-1)/T_k) * W[k][u] from aBase2, or SAT (UNB) once an iterate
+// exceeds the cutoff (A4).  aBase2 already holds A* + LPB + 2 sum_{k<r} W[k][u] (the "+2" of every mu),
+// so the start is G's value for floor(.) = 0, <= the least fixed point (A3).  Products are 64-bit; a
+// product >= 2^32 (high word != 0) is far above every cutoff, and without one the 64-bit sum of <= 31
+// products cannot overflow.
+__device__ __forceinline__ uint32_t lemma2(const Record& r, uint32_t i) {
+  const uint32_t misc = r.aMisc[i];
+  const uint32_t rk = misc & 0xffu, u = (misc >> 8) & 0xffu;
+  const uint32_t base = r.aBase2[i], cut = r.cCut[rk];
+  uint32_t h = base;
+  while (h <= cut) {
+    const uint32_t h2 = (h - 1u) << 1;
+    uint64_t acc = base;
+    uint32_t hi = 0;
+#pragma unroll 2
+    for (uint32_t k = 0; k < rk; k++) {
+      const uint32_t q = __umulhi(h2, r.cM[k]) >> (r.cMisc[k] & 31u);
+      const uint64_t p = (uint64_t)q * r.W[k][u];
+      acc += p;
+      hi |= (uint32_t)(p >> 32);
+    }
+    if (hi || acc > cut) break;
+    const uint32_t g = (uint32_t)acc;
+    if (g == h) return h;
+    h = g;
+  }
+  return SAT;
+}
+
 #ifndef ANA_MINB
 #define ANA_MINB 4
 #endif
@@ -107,44 +137,24 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const uint32_t nch = r.n_chain, nsub = r.n_sub, nas = r.n_aseg;
 
       // ---- step 3: Lemma 2, one lane per accelerator segment ----------------------------------------
-      // aBase2 already holds A* + LPB + 2 sum_{k<r} W[k][u] (the "+2" of every mu), so
-      // G(h) = aBase2 + sum_{k<r} floor((h-1)/T_k) * W[k][u]; starting at G's value for
-      // floor(.) = 0 is <= the least fixed point, so the lfp is unchanged (A3).  Products are
-      // 64-bit; a product >= 2^32 (high word != 0) is far above every cutoff, and without one the
-      // 64-bit sum of <= 31 products cannot overflow.
+      // Only the sound blocking term (A10) needs every H up front.  Otherwise S_c enters Eq.5 only as
+      // min(S_c, C_c(R)) and C_c almost always wins, so step 4 starts from the lower bound
+      // S_lb = sum of the Lemma-2 start values and computes the exact S_c only for a sub-chain whose
+      // C_c at the converged R exceeds S_lb (see step 4).
       // Segments are in rank order (rank = number of HP chains = loop length), so the loop cost of a
       // round is set by its highest rank: the first round takes segments [0, nas-32) (short loops),
       // the second the last 32 (nas <= 64).
-      const uint32_t f = nas > 32 ? nas - 32 : 0;
-      for (uint32_t i = lane < f ? lane : f + lane; i < nas; i = (i < f) ? f + lane : nas) {
-        const uint32_t misc = r.aMisc[i];
-        const uint32_t rk = misc & 0xffu, u = (misc >> 8) & 0xffu;
-        const uint32_t base = r.aBase2[i], cut = r.cCut[rk];
-        uint32_t h = base, H = SAT;
-        while (h <= cut) {
-          const uint32_t h2 = (h - 1u) << 1;
-          uint64_t acc = base;
-          uint32_t hi = 0;
-#pragma unroll 2
-          for (uint32_t k = 0; k < rk; k++) {
-            const uint32_t q = __umulhi(h2, r.cM[k]) >> (r.cMisc[k] & 31u);
-            const uint64_t p = (uint64_t)q * r.W[k][u];
-            acc += p;
-            hi |= (uint32_t)(p >> 32);
-          }
-          if (hi || acc > cut) break;
-          const uint32_t g = (uint32_t)acc;
-          if (g == h) { H = h; break; }
-          h = g;
-        }
-        w.H[i] = H;
+      const bool lazy_s = !(flags & PAAM_FLAG_BLOCKING_SOUND);
+      if (!lazy_s) {
+        const uint32_t f = nas > 32 ? nas - 32 : 0;
+        for (uint32_t i = lane < f ? lane : f + lane; i < nas; i = (i < f) ? f + lane : nas) w.H[i] = lemma2(r, i);
       }
       __syncwarp();
       // per-segment sums S_c and the blocking term in use
       if (lane < nsub) {
         const uint32_t sg = r.sSeg[lane], a0 = sg & 0xffu, na = (sg >> 8) & 0xffu;
         uint32_t S = 0;
-        for (uint32_t i = a0; i < a0 + na; i++) S = sadd(S, w.H[i]);
+        for (uint32_t i = a0; i < a0 + na; i++) S = sadd(S, lazy_s ? r.aBase2[i] : w.H[i]);  // S_lb or S_c
         w.S[lane] = S;
         uint32_t B = r.sB[lane];
         if (flags & PAAM_FLAG_BLOCKING_SOUND) {  // A10: an LP callback also holds its accelerator wait
@@ -243,11 +253,14 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
           pois = gor8(pois);
           gsum8x2(wu_sum, x_sum);
           const uint32_t BE = act ? sadd(w.Bc[c], r.sE[c]) : 0u;
-          const uint32_t S = act ? w.S[c] : 0u, base3 = act ? r.sBase3[c] : 0u, eps = act ? r.sEps[c] : 0u;
+          uint32_t S = act ? w.S[c] : 0u;
+          const uint32_t base3 = act ? r.sBase3[c] : 0u, eps = act ? r.sEps[c] : 0u;
           const uint32_t cut = act ? r.cCut[rk] : 0u;
           uint32_t R = sadd(sadd(BE, sadd(min(S, sadd(base3, sadd(wu_sum, wu_sum))), eps)), sadd(x_sum, x_sum)), Hst = 0;
+          uint32_t C = 0;  // Lemma-3 term C_c(R) of the last iterate
           bool done = !act || pois;
           if (pois) R = SAT;
+          auto iterate = [&]() {
           while (__any_sync(FULL, !done)) {
             if (!done && R > cut) { R = SAT; done = true; }
             const uint32_t h2 = (R - 1u) << 1;
@@ -267,10 +280,31 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
             uint32_t bs = (hi || bb > SAT) ? SAT : (uint32_t)bb;
             gsum8x2(a, bs);
             if (!done) {
-              Hst = sadd(min(S, sadd(base3, a)), eps);
+              C = sadd(base3, a);
+              Hst = sadd(min(S, C), eps);
               const uint32_t F = sadd(sadd(BE, Hst), bs);
               if (F == R) done = true;
               else R = F;
+            }
+          }
+          };
+          iterate();
+          // With S_lb <= S_c, F_lb <= F pointwise, so lfp(F_lb) <= lfp(F): a deadline miss under S_lb is a
+          // miss, and a converged R with C_c(R) <= S_lb is also a fixed point of F (both mins pick C_c),
+          // hence lfp(F).  Otherwise the group computes the exact S_c (lane per segment) and iterates F on
+          // from R, a valid start below lfp(F).  need is uniform within a group.
+          if (lazy_s) {
+            const bool need = act && !pois && R != SAT && C > S;
+            if (__any_sync(FULL, need)) {
+              uint32_t Sx = 0, unused = 0;
+              if (need) {
+                const uint32_t sg = r.sSeg[c], a0 = sg & 0xffu, na = (sg >> 8) & 0xffu;
+                for (uint32_t i = a0 + gl; i < a0 + na; i += 8) Sx = sadd(Sx, lemma2(r, i));
+              }
+              gsum8x2(Sx, unused);
+              if (need) { S = Sx; done = false; }
+              else done = true;
+              iterate();
             }
           }
           if (act && gl == 0) {
