@@ -109,6 +109,9 @@ typedef void* paam_stream_t; /* a cudaStream_t (may be NULL = legacy default str
  *                                                        larger = higher), wait 0 SUSPEND / 1 SPIN
  *   accelerators [set_accel_off[i], ...)                : buckets n (>1 = preemptive GPU-like,
  *                                                        1 = TPU-like), units, server core, eps, kappa
+ * Offset arrays must be non-decreasing.  Within a set, a chain's callback range or a callback's
+ * segment range that leaves the set's own range is reported PAAM_SET_EDANGLING (never read out of
+ * range); a set whose ranges exceed the caps is PAAM_SET_ERANGE.
  */
 typedef struct {
   uint32_t n_sets;

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         cls = b.chain_class[c0 + lane];
         cbo = b.chain_cb_off[c0 + lane] - cb0;
         cbn = b.chain_cb_off[c0 + lane + 1] - cb0 - cbo;
-        edang |= (cbn == 0);
+        edang |= (cbn == 0) || (cbo > ncb) || (cbn > ncb - cbo);  // (malformed CSR: no out-of-range indexing)
         eshape |= (cls > 1);
         edl |= (D == 0 || (cls == 0 && D > T));
       }

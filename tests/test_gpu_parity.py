@@ -309,3 +309,30 @@ def test_pack_analyze_from_host_batch_pipelined(pinned):
     resp = torch.empty(hb.c.n_chains, dtype=torch.int64, device=dev)
     sets.simulate(10**9, 3, resp, n=64)
     torch.cuda.synchronize()
+
+
+def test_malformed_csr_ranges_are_rejected_per_set():
+    """A chain's callback range or a callback's segment range leaving its set's range is reported
+    EDANGLING for that set alone (the kernel never indexes out of range); the other sets are unchanged."""
+    rng = random.Random(21)
+    systems = [random_small_system(rng, max_chains=4) for _ in range(40)]
+    b = flatten(systems, comm_cost=1)
+    _, osch, ost, _ = O.analyze(b)
+    bad = dict(b)
+    bad["chain_cb_off"] = b["chain_cb_off"].copy()
+    bad["cb_seg_off"] = b["cb_seg_off"].copy()
+    i, j = 5, 17
+    c = int(b["set_chain_off"][i])                  # set i: its first chain claims callbacks of set i+1
+    bad["chain_cb_off"][c + 1] = b["chain_cb_off"][b["set_chain_off"][i + 1]] + 1
+    cb = int(b["chain_cb_off"][b["set_chain_off"][j]])  # set j: a callback whose segments run backwards
+    bad["cb_seg_off"][cb + 1] = b["cb_seg_off"][cb] - 1 if b["cb_seg_off"][cb] > 0 else b["cb_seg_off"][cb]
+    st = np.full(len(systems), -9, np.int32)
+    hb = paam.Batch.from_host(bad)
+    sets = paam.Sets(hb, st)
+    sched = torch.full((len(systems),), 7, dtype=torch.uint8, device="cuda")
+    sets.analyze(None, sched, None)
+    torch.cuda.synchronize()
+    assert st[i] != 0 and st[j] != 0
+    others = [k for k in range(len(systems)) if k not in (i, i + 1, j)]
+    assert np.array_equal(st[others], ost[others])
+    assert np.array_equal(sched.cpu().numpy()[others], osch[others])
