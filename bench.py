@@ -2,10 +2,17 @@
 """bench.py -- chain sets analysed per second (PAAM WCRT fixed points) on N B200s.
 
 One step = the whole hot path over this rank's batch of synthetic chain sets that is already
-resident in HBM: paam_repack (validate + derive, §8(a) step 2) -> paam_analyze (Lemma 2 / Eq.5 fixed
-points, end-to-end WCRT, verdict, bin counts; steps 3-6) -> (N > 1) one NCCL all-reduce of the bin
-counts.  Weak scaling: every rank owns SETS_PER_GPU consecutive set indices of the config-4 stream
-(seed 4), so N = 8 is exactly config 4 (16M sets) and N = 1 is the config-3 recipe on 2M sets.
+resident in HBM: paam_pack_analyze (validate + derive, §8(a) step 2, pipelined in two chunks with the
+Lemma 2 / Eq.5 fixed points, end-to-end WCRT, verdict and bin counts of steps 3-6) -> (N > 1) one NCCL
+all-reduce of the bin counts.  Weak scaling: every rank owns SETS_PER_GPU consecutive set indices of
+the config-4 stream (seed 4), so N = 8 is exactly config 4 (16M sets) and N = 1 is the config-3
+recipe on 2M sets.
+
+Extra legs in the same JSON line: per-kernel times from a sequential pass (roofline of the dominant
+kernel and of the other one), verdict_only (PAAM_FLAG_VERDICT_ONLY), e2e (the same metric from
+pinned host buffers through paam_pack_analyze, H2D / D2H inside the timed region),
+e2e_device_generate (paam_sweep: device generation included), des (config-5 leg: paam_simulate on
+100k sets, 10 s horizon, sim <= bound census, with and without digests), cpu_baseline (the oracle).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
