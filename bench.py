@@ -139,9 +139,15 @@ def cpu_baseline(params, first, budget_s=15.0, nthreads=None):
     t0 = time.perf_counter()
     O.analyze(sample, nthreads=nthreads)
     dt = time.perf_counter() - t0
+    n1 = max(500, min(n, int(n / nthreads / 4)))  # one thread, about a quarter of the budget
+    one = generate_host(params, SEED, first, n1)
+    t1 = time.perf_counter()
+    O.analyze(one, nthreads=1)
+    dt1 = time.perf_counter() - t1
     return {"value": n / dt, "unit": "chain-sets/s", "cores": nthreads, "kind": "oracle",
+            "value_1_thread": n1 / dt1,
             "sample": f"first {n} sets of this rank's range (config-3 recipe, seed {SEED}): {dt:.1f} s "
-                      f"of oracle analysis on {nthreads} threads"}
+                      f"of oracle analysis on {nthreads} threads; 1 thread: first {n1} sets, {dt1:.1f} s"}
 
 
 def run_reference(args):
