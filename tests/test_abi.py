@@ -54,6 +54,8 @@ def test_calls_fail_loudly_without_device():
     p = paam.PaamGenParams.from_buffer_copy(bytes(make_params()))
     with pytest.raises(paam.PaamError):
         paam.Raw(p, seed=1, first=0, n=4)
+    with pytest.raises(paam.PaamError):
+        paam.Sweeper(chunk=1024)
 
 
 def test_null_arguments_rejected():
@@ -62,12 +64,15 @@ def test_null_arguments_rejected():
     L = paam.lib()
     assert L.paam_pack(None, None, None, None) == -1
     assert L.paam_analyze(None, 0, None, None, None, None) == -1
+    assert L.paam_sweep(None, None, 0, 0, 0, 0, 0, None, None, None) == -1
+    assert L.paam_sweep_create(0, None) == -1
+    assert L.paam_regenerate(None, None, 0, 0, 0, 0, 0, None) == -1
 
 
 def test_binding_surface():
     """The thin binding exposes every entry point the tests and bench.py call (no GPU needed)."""
     from paper_2404_06452_b200 import paam
-    for cls, names in ((paam.Raw, ("regenerate", "free", "to_host")),
+    for cls, names in ((paam.Raw, ("regenerate", "free", "to_host")), (paam.Sweeper, ("run", "free")),
                        (paam.Sets, ("repack", "pack_analyze", "analyze", "admit", "simulate", "free")),
                        (paam.Batch, ("from_host", "from_host_to_device"))):
         for nm in names:
