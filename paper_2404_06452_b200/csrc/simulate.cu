@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           run_a = __any_sync(FULL, due_x);
         }
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
-        bool chB = false, dueB = false;  // dueB: B left phase-A work due now
+        bool needB = false, dueB = false;  // another phase-B pass could act / B left phase-A work due now
         uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
         if (is_chain) {
           const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
@@ -522,7 +522,6 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             }
           }
           __syncwarp();
-          chB = true;
         }
         // (6) core dispatch (D5): highest process priority runnable executor per core.  ready_x is
         // current: (5) recomputed it on every chain lane whose instance it started.
@@ -537,7 +536,10 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           const uint32_t R = __ballot_sync(FULL, run);
           const uint32_t cand = is_exec ? (R & S.xSameCore[lane]) : 0u;
           const bool oc = cand && (__ffs(cand) - 1 == lane);
-          if (__any_sync(FULL, oc != on_core)) chB = true;
+          // an executor that just got its core while idle with ready work is the only thing another
+          // phase-B pass could act on ((5) serves every wanting executor once per pass; (7) units are
+          // independent of each other)
+          needB = oc && !on_core && is_exec && S.exPhase[lane] == P_NONE;
           on_core = oc;
         }
         // (7) unit dispatch (D8-D11).  Lane u decides whether unit u has anything to dispatch (queue
@@ -575,7 +577,6 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               S.unRem[u] = S.gW[S.bSeg0[j] + seg];
               C.ev(EV_ACC_START, lane, I.cb, seg, u, 0u);
             }
-            chB = true;
             __syncwarp();
             continue;
           }
@@ -639,17 +640,15 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
                 S.unEnd[u] = C.t + S.uKap[u];
                 dueB |= S.uKap[u] == 0;
               }
-              chB = true;
             }
           } else {
-            chB = true;
           }
           __syncwarp();
         }
-        // phase A ended stable and B changed nothing: the timestamp is settled (a further A/B round
-        // would be a no-op)
-        const uint32_t vb = __reduce_or_sync(FULL, (chB ? 1u : 0u) | (dueB ? 2u : 0u));
-        if (!(vb & 1u)) break;
+        // the timestamp is settled unless B left phase-A work due now or gave an idle executor with
+        // ready work its core (every other further A/B round would be a no-op)
+        const uint32_t vb = __reduce_or_sync(FULL, (needB ? 1u : 0u) | (dueB ? 2u : 0u));
+        if (!vb) break;
         run_a = (vb & 2u) != 0;
       }
       // ===================== advance time =====================
