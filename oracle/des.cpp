@@ -105,7 +105,10 @@ struct Sim {
 
   void event(int kind, int chain, int cb, int seg, int unit, int bk) {
     unsigned char rec[32];
-    const uint32_t f[6] = {(uint32_t)kind, (uint32_t)chain, (uint32_t)cb, (uint32_t)seg, (uint32_t)unit, (uint32_t)bk};
+    // D17: a field that does not apply (-1) is recorded as 0xff; no real value reaches 255 (callback
+    // < 64, segment < 192, unit < 8, bucket < 32)
+    auto enc = [](int v) -> uint32_t { return v < 0 ? 0xffu : (uint32_t)v; };
+    const uint32_t f[6] = {enc(kind), enc(chain), enc(cb), enc(seg), enc(unit), enc(bk)};
     std::memcpy(rec, &t, 8);
     std::memcpy(rec + 8, f, 24);
     digest += fnv1a64(rec, 32);  // D17 (order-independent within the multiset of records)

@@ -107,16 +107,12 @@ __device__ __forceinline__ uint64_t fnv_time(uint64_t t) {
   }
   return h;
 }
-// One 4-byte field.  Every field of a record is either FULL (a compile-time constant at its call
-// site) or below 256, whose three zero bytes only multiply: (h ^ v) * P^4 (mod 2^64), one product.
+// One 4-byte field.  A field that does not apply (FULL at its call site) is recorded as 0xff (D17),
+// and every real field is below 255, so each field's three high bytes are zero and only multiply:
+// FNV-1a over the field's 4 bytes is (h ^ v) * P^4 (mod 2^64), one product.
 __device__ __forceinline__ uint64_t fnv_field(uint64_t h, uint32_t v) {
-  constexpr uint64_t P = 0x100000001b3ull, P4 = 0x9ffaac085635bc91ull;  // P^4 mod 2^64
-  if (v == 0xffffffffu) {
-#pragma unroll
-    for (int b = 0; b < 4; b++) h = (h ^ 0xffu) * P;
-    return h;
-  }
-  return (h ^ v) * P4;  // v < 256 at every call site (kind, set-local chain / callback / segment, unit, bucket)
+  constexpr uint64_t P4 = 0x9ffaac085635bc91ull;  // P^4 mod 2^64, P = 0x100000001b3
+  return (h ^ (v == 0xffffffffu ? 0xffu : v)) * P4;
 }
 __device__ __forceinline__ uint64_t fnv_rest(uint64_t h, uint32_t kind, uint32_t chain, uint32_t cb, uint32_t seg,
                                              uint32_t unit, uint32_t bk) {
