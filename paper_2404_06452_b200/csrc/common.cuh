@@ -104,7 +104,6 @@ struct __align__(16) Record {
   uint32_t n_out;       // chains of the set in the batch (== n_chain when valid)
   uint32_t pad_[3];
   // chains by rank (rank 0 = highest priority)
-  uint32_t cT[MAXC];     // period
   uint32_t cCut[MAXC];   // cutoff min(D, T) (A4, A12)
   uint32_t cD[MAXC];     // deadline (verdict)
   uint32_t cM[MAXC];     // mu magic multiplier for T

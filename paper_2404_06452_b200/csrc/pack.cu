@@ -539,7 +539,6 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       const uint32_t o = s.rCbo[k], nb = s.rNcb[k];
       const uint64_t rng = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) << o;
       const uint32_t nsub = __popcll(runstart & rng);
-      r->cT[k] = s.rT[k];
       r->cCut[k] = min(s.rD[k], s.rT[k]);
       r->cD[k] = s.rD[k];
       r->cM[k] = M;
