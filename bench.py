@@ -418,8 +418,8 @@ def run_ours(args):
     traffic = measured_traffic_per_set()
     # pack_kernel: algorithmic bytes = the raw batch it must read + the record fields it must write
     # (config 3: one sub-chain per chain, one accelerator segment per callback, 2 units):
-    # header 32 B + 4 B x (5 per chain + 2 W per chain + 9 per sub-chain + 4 per segment)
-    rec_used = 32 * n + 4 * (16 * raw.c.n_chains + 4 * raw.c.n_cbs)
+    # header 32 B + 4 B x (4 per chain + 2 W per chain + 9 per sub-chain + 4 per segment)
+    rec_used = 32 * n + 4 * (15 * raw.c.n_chains + 4 * raw.c.n_cbs)
     pack_bytes = in_bytes + rec_used
     pack_roof = {"bound": "hbm", "achieved": pack_bytes / (pack_avg / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                  "frac": pack_bytes / (pack_avg / 1e3) / 1e9 / hbm_peak,
