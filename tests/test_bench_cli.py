@@ -24,3 +24,17 @@ def test_reference_arm_json_line():
 def test_bench_module_compiles():
     import py_compile
     py_compile.compile(os.path.join(ROOT, "bench.py"), doraise=True)
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """Launched the way the driver launches N > 1 (torch.distributed.run, 127.0.0.1): rank 0 alone
+    prints the reference line; the other rank exits 0 without work."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29617", os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "2", "--warmup", "3", "--ref-sets-per-step", "1000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
