@@ -4,16 +4,18 @@
 //           H <- A* + LPB + sum_{HP chains k} mu(H, T_k) * W[unit][k]     (start: first two terms)
 //           to its least fixed point, or UNB (= SAT) once an iterate exceeds the cutoff (A4).
 //           W[u][k] regroups the hps sum per interfering chain and unit (all segments of chain k on
-//           unit u share T_k, so sum mu*A* = mu * sum A* exactly).
-//   step 4  Theorem 1 / Eq.5 per sub-chain in canonical order (A7).  One R-iteration
-//           is warp-wide: lane k evaluates mu(R, T_k) for chain k, lane h the hp / hpp term of
-//           sub-chain h (mu by shuffle from its chain's lane), two saturating butterfly reductions
-//           give the Lemma-3 interference (Eq.4, union form A1) and the CPU interference, and
+//           unit u share T_k, so sum mu*A* = mu * sum A* exactly).  Computed on demand: step 4 first
+//           uses the lower bound S_lb (sum of the start values) and asks for the exact S_c only where
+//           the min(S_c, C_c) could depend on it (see step 4); the sound blocking flag computes all.
+//   step 4  Theorem 1 / Eq.5 per sub-chain in canonical order (A7), the sub-chains of
+//           four cores at a time, one 8-lane group per core: lanes take the Lemma-3 chains and the
+//           hp / hpp sub-chains in turn, two saturating butterfly reductions per iterate give the
+//           Lemma-3 interference (Eq.4, union form A1) and the CPU interference, and
 //           H*_c(R) = min(S_c, C_c(R)) + sum eps (Eq.1).  Convergence / deadline miss are
-//           warp-uniform because every lane holds the same reduced value.
+//           group-uniform because every lane of a group holds the same reduced value.
 //   step 5  R* = sum of sub-chain R_c + comm per executor crossing (A9); verdict = every
 //           CRITICAL chain has R* <= D, voted with __all_sync.
-//   step 6  per-block shared-memory bin counts, flushed with one global atomic per bin per block.
+//   step 6  per-warp shared-memory bin counts, flushed with one global atomic per bin at warp exit.
 #include "common.cuh"
 
 namespace paam {
