@@ -10,11 +10,15 @@
 // Every timestamp is settled like this (D15): phase A = (1) unit phase ends and completions,
 // (2) executor CPU / eps completions with enqueues sequenced by (chain, instance) (D7),
 // (3) comm arrivals, (4) releases -- repeated until stable; phase B = (5) executor choice,
-// (6) core dispatch, (7) unit dispatch; A/B repeat until nothing changes.  Each sub-phase is
+// (6) core dispatch, (7) unit dispatch; A/B repeat until nothing changes.  A pass is repeated only
+// when something is provably left for it (zero-length work due now, an executor that just got its
+// core with ready work), so every skipped pass would have been a no-op.  Each sub-phase is
 // lane-parallel over the entities it touches (they touch disjoint state; shared statistics use
 // shared-memory atomics); "best" choices are warp reductions over rank-ordered lanes, so the
 // highest priority is the lowest set bit of a ballot.  Time then jumps to the warp-min next event.
-// The event digest is a sum of per-record FNV-1a-64 hashes (order independent), reduced at the end.
+// Instance slots are packed one byte per slot per chain (byte-compare scans).  The event digest is
+// a sum of per-record FNV-1a-64 hashes (order independent), reduced at the end, computed only when
+// requested.
 #include "../../gen/paam_gen.h"
 #include "common.cuh"
 
