@@ -103,12 +103,13 @@ struct DesSmem {
 // FNV-1a-64 of a 32-byte event record (D17) in two parts: the state after the record's 8-byte time
 // (the same for every record of a timestamp, so computed once per timestamp), then the 24 other bytes.
 __device__ __forceinline__ uint64_t fnv_time(uint64_t t) {
+  constexpr uint64_t P = 0x100000001b3ull, P3 = 0x08a97b0004e7feabull;  // P^3 mod 2^64
   uint64_t h = 0xcbf29ce484222325ull;
 #pragma unroll
-  for (int b = 0; b < 8; b++) {
-    h ^= (t >> (8 * b)) & 0xffu;
-    h *= 0x100000001b3ull;
-  }
+  for (int b = 0; b < 5; b++) h = (h ^ ((t >> (8 * b)) & 0xffu)) * P;
+  if ((t >> 40) == 0) return h * P3;  // three zero bytes only multiply (t < 2^40 ns = 18 min)
+#pragma unroll
+  for (int b = 5; b < 8; b++) h = (h ^ ((t >> (8 * b)) & 0xffu)) * P;
   return h;
 }
 // One 4-byte field.  A field that does not apply (FULL at its call site) is recorded as 0xff (D17),
