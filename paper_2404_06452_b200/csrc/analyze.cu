@@ -198,6 +198,20 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       if (lane == 0) w.gpos[ngroups] = (uint8_t)nsub;
       __syncwarp();
       const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
+      // Period magic constants of the interferers a group lane serves: chain k = gl + 8j (Lemma 3) and
+      // the chain of sub-chain k (hp/hpp).  They depend on k only, so they are loaded once per set.
+      uint32_t KM[4], KL[4], XM[4], XL[4];
+#pragma unroll
+      for (uint32_t j = 0; j < 4; j++) {
+        const uint32_t k = gl + 8 * j;
+        KM[j] = 1; KL[j] = 0; XM[j] = 1; XL[j] = 0;
+        if (k < nch) { KM[j] = r.cM[k]; KL[j] = r.cMisc[k] & 31u; }
+        if (k < nsub) {
+          const uint32_t hm = r.sMisc[k] & 0xffu;
+          XM[j] = r.cM[hm];
+          XL[j] = r.cMisc[hm] & 31u;
+        }
+      }
       bool miss = false;  // verdict-only: a CRITICAL sub-chain already exceeded its deadline
       for (uint32_t gb = 0; gb < ngroups && !miss; gb += 4) {
         const uint32_t grp = gb + gi;
@@ -217,11 +231,11 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
           const uint32_t hibit = cpu_m ? 32u - __clz(cpu_m) : 0u;
           const uint32_t jmax = (__reduce_max_sync(FULL, max(rk, hibit)) + 7u) >> 3;
           // per-lane interferers: Lemma-3 chains and hp/hpp sub-chains (A8 poison on dependencies)
-          uint32_t WU[4], XM[4], XL[4], KM[4], KL[4], X[4];
+          uint32_t WU[4], X[4];
           bool pois = false;
 #pragma unroll
           for (uint32_t j = 0; j < 4; j++) {
-            WU[j] = 0; X[j] = 0; KM[j] = 1; KL[j] = 0; XM[j] = 1; XL[j] = 0;
+            WU[j] = 0; X[j] = 0;
             if (j < jmax) {
               const uint32_t k = gl + 8 * j;
               if (k < rk) {
@@ -232,16 +246,11 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
                   wu = sadd(wu, r.W[k][u]);  // union of hps over the sub-chain's units (A1)
                 }
                 WU[j] = wu;
-                KM[j] = r.cM[k];
-                KL[j] = r.cMisc[k] & 31u;
               }
               if ((cpu_m >> k) & 1u) {
                 const uint32_t hE = r.sE[k], hHs = w.Hs[k];
-                const uint32_t hm = r.sMisc[k] & 0xffu;
                 X[j] = ((hpm >> k) & 1u) ? sadd(hE, hHs)
                                          : sadd(hE, ((spin_mask >> k) & 1u) ? hHs : r.sEps[k]);  // spin() P:1132
-                XM[j] = r.cM[hm];
-                XL[j] = r.cMisc[hm] & 31u;
                 if ((dep >> k) & 1u) pois |= (w.R[k] == SAT);
               }
             }
