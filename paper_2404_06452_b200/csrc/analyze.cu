@@ -248,9 +248,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
                 WU[j] = wu;
               }
               if ((cpu_m >> k) & 1u) {
-                const uint32_t hE = r.sE[k], hHs = w.Hs[k];
-                X[j] = ((hpm >> k) & 1u) ? sadd(hE, hHs)
-                                         : sadd(hE, ((spin_mask >> k) & 1u) ? hHs : r.sEps[k]);  // spin() P:1132
+                X[j] = sadd(r.sE[k], (((hpm | spin_mask) >> k) & 1u) ? w.Hs[k] : r.sEps[k]);  // spin() P:1132
                 if ((dep >> k) & 1u) pois |= (w.R[k] == SAT);
               }
             }
