@@ -128,6 +128,10 @@ inline unsigned __reduce_or_sync(unsigned m, unsigned v) {
   return (unsigned)emu::collect(m, v, [](uint64_t* s, unsigned mk) {
     uint32_t a = 0; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) a |= (uint32_t)s[i]; return (uint64_t)a; });
 }
+inline unsigned __reduce_and_sync(unsigned m, unsigned v) {
+  return (unsigned)emu::collect(m, v, [](uint64_t* s, unsigned mk) {
+    uint32_t a = 0xffffffffu; for (int i = 0; i < 32; i++) if ((mk >> i) & 1u) a &= (uint32_t)s[i]; return (uint64_t)a; });
+}
 inline unsigned __match_any_sync(unsigned m, unsigned long long v) {
   const int l = emu::lane();
   return (unsigned)emu::collect(m, v, [l](uint64_t* s, unsigned mk) {
