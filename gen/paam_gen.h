@@ -23,7 +23,7 @@
 #ifdef __CUDACC__
 #define PG_FN static __host__ __device__ __forceinline__
 #ifdef __CUDA_ARCH__
-#define PG_TABLE(i) PG_EXP2_Q30_DEV[i]
+#define PG_TABLE(i) __ldg(PG_EXP2_Q30_DEV + (i))
 #else
 #define PG_TABLE(i) PG_EXP2_Q30[i]
 #endif
