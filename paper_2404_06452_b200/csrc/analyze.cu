@@ -7,8 +7,9 @@
 //           unit u share T_k, so sum mu*A* = mu * sum A* exactly).  Computed on demand: step 4 first
 //           uses the lower bound S_lb (sum of the start values) and asks for the exact S_c only where
 //           the min(S_c, C_c) could depend on it (see step 4); the sound blocking flag computes all.
-//   step 4  Theorem 1 / Eq.5 per sub-chain in canonical order (A7), the sub-chains of
-//           four cores at a time, one 8-lane group per core: lanes take the Lemma-3 chains and the
+//   step 4  Theorem 1 / Eq.5 per sub-chain, in waves of up to four sub-chains whose
+//           dependencies (hp, spinning hpp: earlier in the canonical order, A7) are solved, first
+//           ready first, one 8-lane group per sub-chain: lanes take the Lemma-3 chains and the
 //           hp / hpp sub-chains in turn, two saturating butterfly reductions per iterate give the
 //           Lemma-3 interference (Eq.4, union form A1) and the CPU interference, and
 //           H*_c(R) = min(S_c, C_c(R)) + sum eps (Eq.1).  Convergence / deadline miss are
@@ -36,7 +37,7 @@ struct __align__(16) WarpSmem {
   uint32_t Hs[MAXS];   // H*_c(R_c) of every solved sub-chain
   unsigned long long sum[MAXC];  // end-to-end accumulation per chain
   uint32_t uns[MAXC];
-  uint8_t gpos[MAXS + 1];  // first canonical sub-chain of each core group, then n_sub
+  uint8_t gpos[4];          // the sub-chains of the current Eq.5 wave, one per lane group
 };
 
 constexpr uint32_t FULL = 0xffffffffu;
@@ -183,20 +184,13 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       __syncwarp();
 
       // ---- step 4: Eq.5, one core at a time per 8-lane group, four cores in parallel -------------------
-      // Dependencies (hp, hpp) only point to earlier sub-chains of the same core (A7), and the canonical
-      // order groups sub-chains by core, so lane group g (lanes 8g..8g+7) walks core group g's
-      // sub-chains in order while the other groups walk theirs.  Within a group, lane l handles the
+      // A sub-chain's Eq.5 reads the results of its hp sub-chains and spinning hpp sub-chains only
+      // (H*_h and R_h, A8); those precede it in the canonical order (A7).  The four 8-lane groups
+      // (lanes 8g..8g+7) solve four ready sub-chains at a time.  Within a group, lane l handles the
       // Lemma-3 chains k = l, l+8, ... (< rank) and the hp/hpp sub-chains h = l, l+8, ...; the two
       // interference sums are reduced over the group with three xor-shuffles each.
       const uint32_t gi = lane >> 3, gl = lane & 7;
       const bool is_sub = lane < nsub;
-      const uint32_t my_core = is_sub ? (r.sSeg[lane] >> 24) : 0x100u + lane;
-      const uint32_t prev_core = __shfl_up_sync(FULL, my_core, 1);
-      const uint32_t gstart = __ballot_sync(FULL, is_sub && (lane == 0 || my_core != prev_core));
-      const uint32_t ngroups = __popc(gstart);
-      if ((gstart >> lane) & 1u) w.gpos[__popc(gstart & ((1u << lane) - 1u))] = (uint8_t)lane;
-      if (lane == 0) w.gpos[ngroups] = (uint8_t)nsub;
-      __syncwarp();
       const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
       // Period magic constants of the interferers a group lane serves: chain k = gl + 8j (Lemma 3) and
       // the chain of sub-chain k (hp/hpp).  They depend on k only, so they are loaded once per set.
@@ -212,18 +206,8 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
           XL[j] = r.cMisc[hm] & 31u;
         }
       }
-      bool miss = false;  // verdict-only: a CRITICAL sub-chain already exceeded its deadline
-      for (uint32_t gb = 0; gb < ngroups && !miss; gb += 4) {
-        const uint32_t grp = gb + gi;
-        uint32_t g0 = 0, glen = 0;
-        if (grp < ngroups) {
-          g0 = w.gpos[grp];
-          glen = w.gpos[grp + 1] - g0;
-        }
-        const uint32_t maxlen = __reduce_max_sync(FULL, glen);
-        for (uint32_t pos = 0; pos < maxlen; pos++) {
-          const bool act = pos < glen;
-          const uint32_t c = act ? g0 + pos : 0u;
+      // solve(act, c): the group's sub-chain c (if act); returns the verdict-only early-exit vote
+      auto solve = [&](const bool act, const uint32_t c) -> bool {
           const uint32_t cmisc = act ? r.sMisc[c] : 0u;
           const uint32_t rk = cmisc & 0xffu, umask = (cmisc >> 8) & 0xffu;
           const uint32_t hpm = act ? r.sHp[c] : 0u, hppm = act ? r.sHpp[c] : 0u;
@@ -321,10 +305,32 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
             w.Hs[c] = (R == SAT) ? SAT : Hst;
           }
           __syncwarp();
-          if (flags & PAAM_FLAG_VERDICT_ONLY) {  // R_c > D_c of a CRITICAL chain => R* > D
-            miss = __any_sync(FULL, act && gl == 0 && R == SAT && ((r.cMisc[rk] >> 8) & 0xffu) == 0);
-            if (miss) break;
+          if (flags & PAAM_FLAG_VERDICT_ONLY)  // R_c > D_c of a CRITICAL chain => R* > D
+            return __any_sync(FULL, act && gl == 0 && R == SAT && ((r.cMisc[rk] >> 8) & 0xffu) == 0);
+          return false;
+      };
+      bool miss = false;  // verdict-only: a CRITICAL sub-chain already exceeded its deadline
+      // Waves: a sub-chain is ready once every sub-chain it depends on (hp, spinning hpp) is solved;
+      // each wave solves the first four ready sub-chains in canonical order, one per group.  The first
+      // unsolved sub-chain is always ready (its dependencies precede it, A7).
+      {
+        const uint32_t my_dep = is_sub ? (r.sHp[lane] | (r.sHpp[lane] & spin_mask)) : 0u;
+        uint32_t todo = nsub >= 32 ? FULL : (1u << nsub) - 1u;
+        while (todo && !miss) {
+          const uint32_t ready = __ballot_sync(FULL, ((todo >> lane) & 1u) && (my_dep & todo) == 0u);
+          if ((ready >> lane) & 1u) {
+            const uint32_t rnk = __popc(ready & ((1u << lane) - 1u));
+            if (rnk < 4) w.gpos[rnk] = (uint8_t)lane;
           }
+          __syncwarp();
+          const bool act = gi < (uint32_t)__popc(ready);
+          const uint32_t c = act ? w.gpos[gi] : 0u;
+          uint32_t rest = ready;
+#pragma unroll
+          for (int q = 0; q < 4; q++) rest &= rest - 1u;
+          todo &= ~(ready & ~rest);
+          __syncwarp();
+          miss = solve(act, c);
         }
       }
       __syncwarp();
