@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       }
       __syncwarp();
 
-      // ---- step 4: Eq.5, one core at a time per 8-lane group, four cores in parallel -------------------
+      // ---- step 4: Eq.5, waves of up to four ready sub-chains, one 8-lane group each -------------------
       // A sub-chain's Eq.5 reads the results of its hp sub-chains and spinning hpp sub-chains only
       // (H*_h and R_h, A8); those precede it in the canonical order (A7).  The four 8-lane groups
       // (lanes 8g..8g+7) solve four ready sub-chains at a time.  Within a group, lane l handles the
@@ -317,18 +317,14 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
         const uint32_t my_dep = is_sub ? (r.sHp[lane] | (r.sHpp[lane] & spin_mask)) : 0u;
         uint32_t todo = nsub >= 32 ? FULL : (1u << nsub) - 1u;
         while (todo && !miss) {
-          const uint32_t ready = __ballot_sync(FULL, ((todo >> lane) & 1u) && (my_dep & todo) == 0u);
-          if ((ready >> lane) & 1u) {
-            const uint32_t rnk = __popc(ready & ((1u << lane) - 1u));
-            if (rnk < 4) w.gpos[rnk] = (uint8_t)lane;
-          }
+          const bool rdy = ((todo >> lane) & 1u) && (my_dep & todo) == 0u;
+          const uint32_t ready = __ballot_sync(FULL, rdy);
+          const uint32_t rnk = __popc(ready & ((1u << lane) - 1u));
+          if (rdy && rnk < 4) w.gpos[rnk] = (uint8_t)lane;
+          todo &= ~__ballot_sync(FULL, rdy && rnk < 4);
           __syncwarp();
           const bool act = gi < (uint32_t)__popc(ready);
           const uint32_t c = act ? w.gpos[gi] : 0u;
-          uint32_t rest = ready;
-#pragma unroll
-          for (int q = 0; q < 4; q++) rest &= rest - 1u;
-          todo &= ~(ready & ~rest);
           __syncwarp();
           miss = solve(act, c);
         }
