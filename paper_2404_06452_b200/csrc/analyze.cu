@@ -23,9 +23,15 @@ namespace paam {
 
 namespace {
 
-constexpr int AW = 8;          // warps per block
+#ifndef ANA_AW
+#define ANA_AW 8
+#endif
+#ifndef ANA_TICK
+#define ANA_TICK 2
+#endif
+constexpr int AW = ANA_AW;     // warps per block
 constexpr int WARP_BINS = 32;  // bins counted per warp in shared memory (more: direct global atomics)
-constexpr uint32_t TICK = 2;   // sets per work ticket
+constexpr uint32_t TICK = ANA_TICK;  // sets per work ticket
 constexpr uint64_t UNS = PAAM_UNSCHED;
 
 struct __align__(16) WarpSmem {
