@@ -127,12 +127,17 @@ def test_edge_cases():
     assert gpu_host_path(b)[2].tolist() == [1, 0]
 
 
-@pytest.mark.parametrize("cfg,cpu_only", [("config2", 0.0), ("config2", 0.25), ("config3", 0.0), ("modeB_split", 0.0)])
+@pytest.mark.parametrize("cfg,cpu_only", [("config2", 0.0), ("config2", 0.25), ("config3", 0.0), ("modeB_split", 0.0),
+                                          ("deep_deps", 0.0), ("many_cores", 0.0)])
 def test_generated_workloads_full(cfg, cpu_only):
     if cfg == "config2":
         p, seed, n = config2_params(cpu_only_frac=cpu_only), 2, 10_000
     elif cfg == "config3":
         p, seed, n = config3_params(), 3, 20_000
+    elif cfg == "deep_deps":  # one core, shared spinning executors: every sub-chain waits for the previous ones
+        p, seed, n = make_params(exec_mode=1, n_cores=1, n_exec=4, xexec_frac=0.5, spin_frac=1.0), 13, 10_000
+    elif cfg == "many_cores":  # 16 cores, up to 32 chains: more ready sub-chains than one Eq.5 wave takes
+        p, seed, n = make_params(m_lo=20, m_hi=32, cbs_per_chain=2, n_cores=16, n_exec=16), 14, 10_000
     else:
         p, seed, n = make_params(exec_mode=1, n_exec=4, xexec_frac=0.5, cpu_only_frac=0.2, spin_frac=0.5), 6, 20_000
     b = generate_host(p, seed, 0, n)
