@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const uint32_t gi = lane >> 3, gl = lane & 7;
       const bool is_sub = lane < nsub;
       const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
+      const bool two_units = r.n_unit <= 2;  // set-uniform
       // Period magic constants of the interferers a group lane serves: chain k = gl + 8j (Lemma 3) and
       // the chain of sub-chain k (hp/hpp).  They depend on k only, so they are loaded once per set.
       uint32_t KM[4], KL[4], XM[4], XL[4];
@@ -229,12 +230,13 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
             if (j < jmax) {
               const uint32_t k = gl + 8 * j;
               if (k < rk) {
-                uint32_t um = umask, wu = 0;
-                while (um) {
-                  const uint32_t u = __ffs(um) - 1;
-                  um &= um - 1;
-                  wu = sadd(wu, r.W[k][u]);  // union of hps over the sub-chain's units (A1)
-                }
+                uint32_t wu = 0;
+                if (two_units) {  // units 0 and 1 only: one 8-byte row load, two selects
+                  const uint2 w01 = *reinterpret_cast<const uint2*>(&r.W[k][0]);
+                  wu = sadd((umask & 1u) ? w01.x : 0u, (umask & 2u) ? w01.y : 0u);
+                } else
+                for (uint32_t um = umask; um; um &= um - 1)
+                  wu = sadd(wu, r.W[k][__ffs(um) - 1]);  // union of hps over the sub-chain's units (A1)
                 WU[j] = wu;
               }
               if ((cpu_m >> k) & 1u) {
