@@ -412,11 +412,11 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           }
           __syncwarp();
           // (2) executors: CPU / eps completions; enqueues sequenced by (chain, instance) (D7)
-          bool enq = false;
+          bool enq = false, adv = false;
           uint32_t enq_key = 0xffffffffu;
           if (is_exec) {
             const uint32_t x = lane, ph = S.exPhase[x];
-            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); }
+            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); adv = true; }
             else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
               S.exPhase[x] = P_WAIT;
               enq = true;
@@ -424,7 +424,9 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
              
             }
           }
-          const bool due_x = is_exec && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
+          // (2) served every executor that was due, and advance_segment(x) changes executor x only, so
+          // only an executor (2) advanced can be due again (its next segment may be zero-length)
+          const bool due_x = adv && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
           const uint32_t enq_mask = __ballot_sync(FULL, enq);
           if (enq_mask) {
             uint32_t pos = 0;
