@@ -70,6 +70,17 @@ def test_random_small_systems_des(seed):
     check(b, 400, seed)
 
 
+def test_random_small_systems_des_zero_comm():
+    """comm = 0 with eps / kappa often 0: zero-length transits, eps phases and switches, so settle
+    passes repeat at one timestamp (the pass-repeat rules of simulate.cu)."""
+    rng = random.Random(977)
+    systems = [random_small_system(rng, max_chains=6, tmax=60) for _ in range(600)]
+    b = flatten(systems, comm_cost=0)
+    _, _, st, _ = O.analyze(b)
+    assert (st == 0).all()
+    check(b, 400, 4)
+
+
 @pytest.mark.parametrize("cfg", ["config3", "config2_cpuonly", "modeB_split"])
 def test_generated_des(cfg):
     if cfg == "config3":
