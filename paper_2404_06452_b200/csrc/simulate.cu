@@ -129,11 +129,6 @@ __device__ __forceinline__ uint64_t fnv_rest(uint64_t h, uint32_t kind, uint32_t
   return fnv_field(h, bk);
 }
 
-__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-  const uint32_t hi = __reduce_min_sync(FULL, (uint32_t)(v >> 32));
-  const uint32_t lo = __reduce_min_sync(FULL, (uint32_t)(v >> 32) == hi ? (uint32_t)v : 0xffffffffu);
-  return ((uint64_t)hi << 32) | lo;
-}
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -655,28 +650,34 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         run_a = (vb & 2u) != 0;
       }
       // ===================== advance time =====================
-      uint64_t nt = NONE64;
+      // Every pending event lies less than 2^31 ns ahead (a period, eps, kappa, comm or remaining
+      // work, each < 2^31 - 1 ns), so the next event is found as a 32-bit distance from t.
+      uint32_t nd = 0xffffffffu;  // none
+      bool run_x = false, run_u = false;  // executor / unit whose remaining work shrinks with time
       if (is_chain) {
         const uint64_t r = next_rel;
-        if (r < horizon) nt = r;
+        if (r < horizon) nd = (uint32_t)(r - C.t);
         for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
-          nt = min(nt, S.iw[lane][slot_of(tm)].ready_at);
+          nd = min(nd, (uint32_t)(S.iw[lane][slot_of(tm)].ready_at - C.t));
       }
       if (is_exec) {
         const uint32_t ph = S.exPhase[lane];
-        if ((ph == P_CPU || ph == P_EPS_SPIN) && on_core) nt = min(nt, C.t + S.exRem[lane]);
-        if (ph == P_EPS_SUSP) nt = min(nt, S.exTimer[lane]);
+        run_x = (ph == P_CPU || ph == P_EPS_SPIN) && on_core;
+        if (run_x) nd = min(nd, S.exRem[lane]);
+        if (ph == P_EPS_SUSP) nd = min(nd, (uint32_t)(S.exTimer[lane] - C.t));
       }
       if (is_unit) {
-        if (S.unState[lane] == U_RUN) nt = min(nt, C.t + S.unRem[lane]);
-        if (S.unState[lane] == U_SWOUT || S.unState[lane] == U_SWIN) nt = min(nt, S.unEnd[lane]);
+        const uint32_t us = S.unState[lane];
+        run_u = us == U_RUN;
+        if (run_u) nd = min(nd, S.unRem[lane]);
+        if (us == U_SWOUT || us == U_SWIN) nd = min(nd, (uint32_t)(S.unEnd[lane] - C.t));
       }
-      nt = warp_min_u64(nt);
-      if (nt == NONE64) break;
+      nd = __reduce_min_sync(FULL, nd);
+      if (nd == 0xffffffffu) break;
       if (++steps > STEP_CAP) { aborted = true; break; }
-      const uint32_t dt = (uint32_t)min(nt - C.t, (uint64_t)0xffffffffu);
-      if (is_exec && on_core && (S.exPhase[lane] == P_CPU || S.exPhase[lane] == P_EPS_SPIN)) S.exRem[lane] -= dt;
-      if (is_unit && S.unState[lane] == U_RUN) S.unRem[lane] -= dt;
+      const uint64_t nt = C.t + nd;
+      if (run_x) S.exRem[lane] -= nd;
+      if (run_u) S.unRem[lane] -= nd;
       C.t = nt;
       if (C.want_dig) C.th = fnv_time(nt);
       __syncwarp();
