@@ -493,7 +493,7 @@ def ncu_issue_stats():
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         return {k: {"issue_active_pct": v.get("issue_active_pct"), "warp_inst_per_set": v.get("warp_inst_per_set"),
-                    "source": "profiles/traffic.json (ncu --set full, profiles/r01_ncu_full_v15_summary.txt)"}
+                    "source": v.get("source", "profiles/traffic.json (ncu --set full, profiles/r01_ncu_full_v15_summary.txt)")}
                 for k, v in d.items() if not k.startswith("_")}
     except Exception:
         return {}

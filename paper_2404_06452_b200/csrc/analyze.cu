@@ -115,26 +115,67 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
 
   // Dynamic work distribution: warps take TICK consecutive sets per atomic ticket, so the per-set
   // cost variance does not leave warps (and their block's resources) idle at the end.
-  uint32_t set = 0, left = 0;
-  for (;;) {
-    if (left == 0) {
-      uint32_t t = 0;
-      if (lane == 0) t = atomicAdd(ticket, TICK);
-      set = __shfl_sync(FULL, t, 0);
-      if (set >= n) break;
-      left = min((uint32_t)TICK, n - set);
-    } else {
-      set++;
-    }
-    left--;
-    // ---- stage the record in shared memory (16-byte vector loads, coalesced) ---------------------
+  // The next set's header word (its counts) is loaded one set ahead, so staging can skip the
+  // record vectors past the live entries without a round trip in front of the set's loads.
+  const uint32_t* hdr_base = reinterpret_cast<const uint32_t*>(recs);
+  constexpr uint32_t HDR_STRIDE = sizeof(Record) / 4;
+  uint32_t set, left;  // left: sets of the current ticket after `set`
+  {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(ticket, TICK);
+    set = __shfl_sync(FULL, t, 0);
+    left = set < n ? min((uint32_t)TICK, n - set) - 1 : 0;
+  }
+  uint32_t hdr = set < n ? __ldg(hdr_base + (size_t)set * HDR_STRIDE) : 0u;
+  while (set < n) {
+    // ---- stage the record's live vectors in shared memory (16-byte vector loads, coalesced) -------
+    // The header's counts decide, per array, how many leading 16-byte vectors are live (pack writes
+    // nothing past them, and nothing below reads past them).  Config-3 sets use about 55% of the record.
     {
       const uint4* src = reinterpret_cast<const uint4*>(recs + set);
       uint4* dst = reinterpret_cast<uint4*>(&r);
       constexpr int NV = sizeof(Record) / 16;
-#pragma unroll 4
-      for (int i = lane; i < NV; i += 32) dst[i] = __ldg(src + i);
+      constexpr int V_CH = offsetof(Record, cCut) / 16, V_W = offsetof(Record, W) / 16;
+      constexpr int V_SUB = offsetof(Record, sE) / 16, V_SEG = offsetof(Record, aBase2) / 16;
+      static_assert(V_CH == 2 && V_W - V_CH == 4 * MAXC / 4 && V_SEG - V_SUB == 9 * MAXS / 4 &&
+                        NV - V_SEG == 4 * MAXA / 4 && MAXU == 8,
+                    "live-vector map assumes the Record layout in common.cuh");
+      const uint32_t nc = hdr & 0xffu, vc = (nc + 3) >> 2, vs = (((hdr >> 8) & 0xffu) + 3) >> 2;
+      const uint32_t va = (((hdr >> 16) & 0xffu) + 3) >> 2;
+      // Predicated loads in groups of four, all issued before their stores (one round trip per group).
+      constexpr int NK = (NV + 31) / 32;
+#pragma unroll
+      for (int k0 = 0; k0 < NK; k0 += 4) {
+        uint4 v[4];
+        uint32_t livem = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int i = lane + 32 * (k0 + k);
+          const bool live = i < V_CH    ? true
+                            : i < V_W   ? (uint32_t)((i - V_CH) & (MAXC / 4 - 1)) < vc
+                            : i < V_SUB ? (uint32_t)((i - V_W) >> 1) < nc  // W row k = 2 vectors
+                            : i < V_SEG ? (uint32_t)((i - V_SUB) & (MAXS / 4 - 1)) < vs
+                            : i < NV    ? (uint32_t)((i - V_SEG) & (MAXA / 4 - 1)) < va
+                                        : false;
+          livem |= (uint32_t)live << k;
+          v[k] = live ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (livem >> k & 1u) dst[lane + 32 * (k0 + k)] = v[k];
+      }
     }
+    uint32_t nset, nleft;
+    if (left) {
+      nset = set + 1;
+      nleft = left - 1;
+    } else {
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(ticket, TICK);
+      nset = __shfl_sync(FULL, t, 0);
+      nleft = nset < n ? min((uint32_t)TICK, n - nset) - 1 : 0;
+    }
+    const uint32_t nhdr = nset < n ? __ldg(hdr_base + (size_t)nset * HDR_STRIDE) : 0u;
     __syncwarp();
     const int32_t status = r.status;
     uint32_t sched = 0;
@@ -378,6 +419,9 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       }
     }
     __syncwarp();
+    set = nset;
+    left = nleft;
+    hdr = nhdr;
   }
   if (warp_bins) {
     __syncwarp();
