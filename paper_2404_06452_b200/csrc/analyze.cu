@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
                             : i < NV    ? (uint32_t)((i - V_SEG) & (MAXA / 4 - 1)) < va
                                         : false;
           livem |= (uint32_t)live << k;
-          v[k] = live ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+          v[k] = live ? __ldg(src + i) : uint4{0u, 0u, 0u, 0u};
         }
 #pragma unroll
         for (int k = 0; k < 4; k++)
