@@ -247,3 +247,47 @@ def test_wfd_unit_assignment():
     # without the flag the input units (all 0) are used: everyone blocks everyone below
     d = O.detail(flatten([_wfd_system([20, 20, 20, 20])], comm_cost=0, flags=0))
     assert d["aseg_LPB"] == [20, 20, 20, 0]
+
+
+def spin_system(wait):
+    """hpp interferer with an accelerator segment (golden 'spin_hpp')."""
+    s = System()
+    a = s.accel(buckets=1, server_core=0, eps=1 * MS)
+    xh = s.executor(core=1, prio=2, wait=wait)
+    xc = s.executor(core=1, prio=1, wait=SUSPEND)
+    s.chain(T=100 * MS, prio=2, cbs=[cb(xh, cpu(2 * MS), acc(a, 10 * MS))])
+    s.chain(T=100 * MS, prio=1, cbs=[cb(xc, cpu(5 * MS))])
+    return s
+
+
+@pytest.mark.parametrize("wait,key", [(SPIN, "R_c_spin"), (SUSPEND, "R_c_suspend")])
+def test_spin_of_hpp_interferer(wait, key):
+    g = GOLD["spin_hpp"]
+    b, (wcrt, sched, status, _) = run([spin_system(wait)])
+    d = O.detail(b)
+    assert status[0] == 0
+    assert d["sub_R"][0] == g["R_h"] and d["sub_Hstar"][0] == g["Hstar_h"]
+    assert d["sub_R"][1] == g[key]
+    assert wcrt.tolist() == [g["R_h"], g[key]]
+
+
+def lemma3_union_system():
+    """Two segments of one sub-chain on one unit sharing one HP interferer (golden 'lemma3_union')."""
+    s = System()
+    a = s.accel(buckets=1, server_core=0)
+    xh = s.executor(core=2)
+    xc = s.executor(core=1)
+    s.chain(T=50 * MS, prio=2, cbs=[cb(xh, acc(a, 4 * MS))])
+    s.chain(T=200 * MS, prio=1, cbs=[cb(xc, acc(a, 3 * MS), cpu(1 * MS), acc(a, 3 * MS))])
+    return s
+
+
+def test_lemma3_union_counts_each_hp_segment_once():
+    g = GOLD["lemma3_union"]
+    b, (wcrt, sched, status, _) = run([lemma3_union_system()])
+    d = O.detail(b)
+    assert status[0] == 0
+    assert d["sub_S"][1] == g["S_c"]
+    assert d["sub_C"][1] == g["C_c"] and d["sub_Hstar"][1] == g["Hstar_c"]
+    assert d["sub_R"][1] == g["R_c"] and wcrt[1] == g["R_c"]
+    assert g["R_c"] != g["R_c_if_summed_per_segment"]
