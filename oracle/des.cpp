@@ -13,8 +13,9 @@
 //               P:370), preemption of a lower bucket by a higher one costing kappa to switch out
 //               and kappa to switch back in (R4);                              D6-D11
 //   chains      periodic releases, successors released on completion, comm delay across
-//               executors, BE overrun drops (D14), response = last callback done -
-//               release (D16).
+//               executors, overrun (D14): a CRITICAL chain queues every new
+//               instance (an unbounded per-chain backlog), a BE chain drops its older pending,
+//               not-started instance; response = last callback done - release (D16).
 // Digest (D17): parity unpinned -- the record layout and hash are this implementation's definition
 // (the paper defines none); only determinism and GPU/oracle agreement are tested.
 // Same-timestamp order (D15): (A) every change due now -- unit phase ends / completions, eps and CPU
@@ -29,9 +30,7 @@ using namespace oracle_model;
 
 namespace {
 
-const int QCAP = 4;  // live instances per chain; a release beyond it is skipped and counted (D14b)
-
-enum EvKind {
+enum EvKind {  // EV_OVERFLOW is reserved (never recorded: the backlog is unbounded, D14)
   EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_ENQUEUE, EV_ACC_START,
   EV_ACC_PREEMPT, EV_ACC_RESUME, EV_ACC_DONE, EV_CB_DONE, EV_CHAIN_DONE
 };
@@ -80,13 +79,13 @@ struct Sim {
   std::vector<int> unit_base;
   u64 horizon, t = 0;
   std::vector<u64> phase, next_k;
-  std::vector<std::vector<Instance>> inst;  // [chain][QCAP]
+  std::vector<std::vector<Instance>> inst;  // [chain][slot]: the chain's backlog, grown on demand (D14)
   std::vector<ExecState> ex;
   std::vector<UnitState> units;
   std::vector<int> core_owner;              // by core id (0..255), -1 none
   u64 seq = 0, digest = 0;
   // statistics per chain (D16)
-  std::vector<u64> max_resp, count, sum_resp, misses, drops, overflows;
+  std::vector<u64> max_resp, count, sum_resp, misses, drops, peak_live;
 
   Sim(const System& sys, u64 hz, const std::vector<u64>& ph) : s(sys), horizon(hz), phase(ph) {
     bucket = bucket_map(s);
@@ -96,11 +95,11 @@ struct Sim {
       for (int u = 0; u < s.accels[a].units; u++) { UnitState us; us.acc = a; units.push_back(us); }
     const size_t m = s.chains.size();
     next_k.assign(m, 0);
-    inst.assign(m, std::vector<Instance>(QCAP));
+    inst.assign(m, std::vector<Instance>());
     ex.assign(s.execs.size(), ExecState());
     core_owner.assign(256, -1);
     max_resp.assign(m, 0); count.assign(m, 0); sum_resp.assign(m, 0); misses.assign(m, 0);
-    drops.assign(m, 0); overflows.assign(m, 0);
+    drops.assign(m, 0); peak_live.assign(m, 0);
   }
 
   void event(int kind, int chain, int cb, int seg, int unit, int bk) {
@@ -149,7 +148,7 @@ struct Sim {
   void start_job(int x) {  // D4
     int bc = -1, bs = -1;
     for (int c = 0; c < (int)s.chains.size(); c++)
-      for (int k = 0; k < QCAP; k++) {
+      for (int k = 0; k < (int)inst[c].size(); k++) {
         const Instance& I = inst[c][k];
         if (!I.live || I.state != 0 || cbk(c, I.cb).exec != x) continue;
         if (bc < 0) { bc = c; bs = k; continue; }
@@ -274,16 +273,18 @@ struct Sim {
               drops[c]++;
               event(EV_DROP, c, -1, -1, -1, -1);
             }
+        // D14: the new instance always queues; a free slot is reused, else the backlog grows
         int slot = -1;
-        for (int k = 0; k < QCAP; k++) if (!inst[c][k].live) { slot = k; break; }
-        if (slot < 0) {
-          overflows[c]++;
-          event(EV_OVERFLOW, c, -1, -1, -1, -1);
-        } else {
-          Instance& I = inst[c][slot];
-          I.live = true; I.release = t; I.k = next_k[c]; I.cb = 0; I.state = 0;
-          event(EV_RELEASE, c, -1, -1, -1, -1);
+        u64 live = 0;
+        for (int k = 0; k < (int)inst[c].size(); k++) {
+          if (inst[c][k].live) live++;
+          else if (slot < 0) slot = k;
         }
+        if (slot < 0) { slot = (int)inst[c].size(); inst[c].push_back(Instance()); }
+        Instance& I = inst[c][slot];
+        I.live = true; I.release = t; I.k = next_k[c]; I.cb = 0; I.state = 0;
+        peak_live[c] = std::max(peak_live[c], live + 1);
+        event(EV_RELEASE, c, -1, -1, -1, -1);
         next_k[c]++;
         changed = true;
       }
@@ -422,7 +423,7 @@ extern "C" int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, ui
       if (out_misc) {
         out_misc[3 * (c0 + c) + 0] = sim.misses[c];
         out_misc[3 * (c0 + c) + 1] = sim.drops[c];
-        out_misc[3 * (c0 + c) + 2] = sim.overflows[c];
+        out_misc[3 * (c0 + c) + 2] = sim.peak_live[c];
       }
       if (set_sched && s.chains[c].cls == 0 && sim.max_resp[c] > bound[c0 + c]) viol[th]++;
     }

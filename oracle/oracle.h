@@ -79,7 +79,8 @@ int32_t oracle_generate_analyze(const void* params, uint64_t seed, uint64_t firs
                                 uint64_t* counters, int nthreads);
 
 /* Discrete-event simulation (des.cpp, DESIGN.md App. A): per chain max / count of observed end-to-end
- * responses, misc[3] = {deadline misses, BE drops, overflowed releases}; per set an order-independent
+ * responses, misc[3] = {deadline misses (D16), BE drops (D14), peak backlog = the most live
+ * instances the chain ever had at once (D14: CRITICAL chains queue every release)}; per set an order-independent
  * FNV-1a-64 digest of the event records; violations of `bound` counted for CRITICAL chains of sets
  * whose every CRITICAL chain has bound <= D (the analysis' schedulable sets).  phases_or_null: explicit release phases per chain (brute force), else pg_phase(). */
 int32_t oracle_simulate_batch(const or_batch* b, uint64_t horizon, uint64_t seed, uint64_t first_index,

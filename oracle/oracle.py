@@ -125,7 +125,7 @@ def generate_analyze(params: GenParams, seed: int, first: int, n: int, comm_cost
 
 def simulate(batch: dict, horizon: int, seed: int = 0, first_index: int = 0, phases=None, bound=None,
              nthreads: int = 1, fifo: bool = False) -> dict:
-    """Oracle DES.  Returns dict(resp, count, misses, drops, overflows per chain; digest per set;
+    """Oracle DES.  Returns dict(resp, count, misses, drops, peak_live per chain; digest per set;
     violations)."""
     b = make_batch(batch)
     nch = int(batch["set_chain_off"][-1])
@@ -141,5 +141,5 @@ def simulate(batch: dict, horizon: int, seed: int = 0, first_index: int = 0, pha
                                      _ptr(misc), _ptr(dig), _ptr(bd), _ptr(viol), nthreads)
     assert rc == 0
     misc = misc[:3 * nch].reshape(-1, 3) if nch else np.zeros((0, 3), np.uint64)
-    return dict(resp=resp[:nch], count=cnt[:nch], misses=misc[:, 0], drops=misc[:, 1], overflows=misc[:, 2],
+    return dict(resp=resp[:nch], count=cnt[:nch], misses=misc[:, 0], drops=misc[:, 1], peak_live=misc[:, 2],
                 digest=dig[:n], violations=int(viol[0]))

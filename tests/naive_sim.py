@@ -7,8 +7,6 @@ sets pins the oracle's time-advance, timers, preemption and tie-breaking code.
 """
 import math
 
-QCAP = 4
-
 
 def buckets_of(s):
     out = {}
@@ -36,7 +34,7 @@ def simulate(s, horizon, phases, comm):
     units = [dict(q=[], state="idle", cur=None, end=0) for _ in unit_acc]
     owner = {}
     seq = [0]
-    stats = [dict(mx=0, n=0) for _ in range(m)]
+    stats = [dict(mx=0, n=0, miss=0, drop=0, peak=0) for _ in range(m)]
 
     def exec_of(c, j):
         return s.chains[c].cbs[j].exec
@@ -75,6 +73,7 @@ def simulate(s, horizon, phases, comm):
             r = t - I["release"]
             stats[c]["mx"] = max(stats[c]["mx"], r)
             stats[c]["n"] += 1
+            stats[c]["miss"] += r > s.chains[c].D
             insts[c].remove(I)
         e["job"], e["phase"] = None, "none"
 
@@ -138,9 +137,11 @@ def simulate(s, horizon, phases, comm):
                     if r != t or r >= horizon:
                         continue
                     if s.chains[c].cls == 1:
-                        insts[c] = [I for I in insts[c] if not (I["state"] == "ready" and I["cb"] == 0)]
-                    if len(insts[c]) < QCAP:
-                        insts[c].append(dict(release=t, k=nxt[c], cb=0, state="ready", ready_at=0))
+                        kept = [I for I in insts[c] if not (I["state"] == "ready" and I["cb"] == 0)]
+                        stats[c]["drop"] += len(insts[c]) - len(kept)
+                        insts[c] = kept
+                    insts[c].append(dict(release=t, k=nxt[c], cb=0, state="ready", ready_at=0))  # D14: queue
+                    stats[c]["peak"] = max(stats[c]["peak"], len(insts[c]))
                     nxt[c] += 1
                     ch = True
                 if not ch:
@@ -190,4 +191,4 @@ def simulate(s, horizon, phases, comm):
         for U in units:
             if U["state"] == "run":
                 U["cur"]["rem"] -= 1
-    return [st["mx"] for st in stats], [st["n"] for st in stats]
+    return {k: [st[k] for st in stats] for k in ("mx", "n", "miss", "drop", "peak")}

@@ -66,6 +66,7 @@ def tiny_system(rng):
 
 def test_naive_tick_simulator_agrees():
     rng = random.Random(2024)
+    backlog = drops = misses = 0
     for trial in range(150):
         s = tiny_system(rng)
         comm = rng.choice([0, 1, 2])
@@ -76,9 +77,16 @@ def test_naive_tick_simulator_agrees():
         if st[0] != 0:
             continue
         r = O.simulate(b, horizon, phases=np.array(phases, np.uint64))
-        mx, n = naive(s, horizon, phases, comm)
-        assert r["resp"].tolist() == mx, (trial, phases)
-        assert r["count"].tolist() == n, trial
+        nv = naive(s, horizon, phases, comm)
+        assert r["resp"].tolist() == nv["mx"], (trial, phases)
+        assert r["count"].tolist() == nv["n"] and r["misses"].tolist() == nv["miss"], trial
+        assert r["drops"].tolist() == nv["drop"] and r["peak_live"].tolist() == nv["peak"], trial
+        backlog += max(nv["peak"], default=0) > 4
+        drops += sum(nv["drop"])
+        misses += sum(nv["miss"])
+    # the random tiny sets exercise every statistic: backlogs beyond four instances (D14 queueing),
+    # BE drops and deadline misses
+    assert backlog > 0 and drops > 0 and misses > 0, (backlog, drops, misses)
 
 
 def same_executor_lp_callback(s):
