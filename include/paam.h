@@ -230,20 +230,51 @@ int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_sta
  * released instance completes.  Chain c of set i is released at phase + k*T with phase = 0 when
  * seed == 0, else pg_phase(seed, first_index + i, c, T) (gen/paam_gen.h).  sim_flags: 0 = PAAM, or
  * PAAM_SIM_FIFO_DIRECT (the direct-invocation baseline the paper compares against).
- *   out_resp   [n_chains total] maximum observed end-to-end response time per chain (0 if none).
- *   out_count  [n_chains total] completed instances per chain (may be NULL).
- *   out_digest [n] order-independent FNV-1a-64 digest of the event records (may be NULL: the events
- *              are then not hashed at all).
- *   bound      [n_chains total] WCRTs from paam_analyze, or NULL.  In every set whose CRITICAL
- *              chains all have bound <= D (the analysis' schedulable sets, Lemma 1), each
- *              CRITICAL chain with out_resp > bound adds 1 to *out_violations (int64, +=).
+ * Overrun (D14): a CRITICAL chain queues every release (an unbounded backlog), a BE chain drops
+ * its older pending, not-started instances.  The device keeps PAAM_SIM_QCAP instance slots per chain:
+ * a release that would make a chain's (QCAP+1)-th live instance stops that set's run at that release
+ * and reports PAAM_SIM_BACKLOG -- never a silently different simulation.  Up to the stop the run is
+ * exact, so a stopped set's resp / count / misses / drops are lower bounds of the full run's.
+ * Outputs (device pointers; every one may be NULL):
+ *   resp     [n_chains total] maximum observed end-to-end response time per chain (0 if none) (D16).
+ *   count    [n_chains total] completed instances per chain.
+ *   misses   [n_chains total] completed instances whose response exceeded D (D16).
+ *   drops    [n_chains total] BE instances dropped at a release (D14).
+ *   digest   [n] order-independent FNV-1a-64 digest of the event records (D17); NULL: events are not
+ *            hashed at all (faster).
+ *   status   [n] PAAM_SIM_OK, or PAAM_SIM_INVALID (validation failed at pack: outputs 0),
+ *            PAAM_SIM_BACKLOG or PAAM_SIM_STEPCAP (the run stopped early, see above).
+ *   bound    [n_chains total] input: WCRTs from paam_analyze, or NULL.  In every set whose run did not
+ *            stop and whose CRITICAL chains all have bound <= D (the analysis' schedulable sets,
+ *            Lemma 1), each CRITICAL chain with resp > bound is a violation of P:533:
+ *   violations [1] int64, += the violations;
+ *   witness  [2*max_witness] u32 (set index in the batch, set-local chain index) of violations, in
+ *            slot v = the value of *violations before that violation was added; slots >= max_witness
+ *            are not written (zero *violations first for the first max_witness).  Needs violations.
+ *   stopped  [1] int64, += sets whose run stopped early (BACKLOG / STEPCAP).
  * Reads the raw batch the handle was packed from: a DEVICE batch must still be alive (a HOST batch
- * was staged by paam_pack).  Device pointers only. */
+ * was staged by paam_pack).  Errors: PAAM_EINVAL for an unknown sim flag, n beyond the handle, or
+ * witness without violations. */
 #define PAAM_SIM_FIFO_DIRECT 0x1u /* baseline arbitration: one FIFO per unit in arrival
                                      order, non-preemptive, no eps, no kappa, buckets ignored */
+#define PAAM_SIM_QCAP 4           /* instance slots per chain on the device */
+#define PAAM_SIM_STEP_CAP 50000000ull /* event timestamps per set before a run is stopped */
+#define PAAM_SIM_OK 0
+#define PAAM_SIM_INVALID 1
+#define PAAM_SIM_BACKLOG 2
+#define PAAM_SIM_STEPCAP 3
+typedef struct {
+  uint64_t *resp, *count, *misses, *drops;
+  uint64_t* digest;
+  int32_t* status;
+  const uint64_t* bound;
+  int64_t* violations;
+  uint32_t* witness;
+  int64_t* stopped;
+  uint32_t max_witness, _pad;
+} paam_sim_out;
 int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
-                  uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
-                  int64_t* out_violations, paam_stream_t stream);
+                  uint32_t sim_flags, const paam_sim_out* out, paam_stream_t stream);
 
 /* Handle queries (synchronous, small). */
 int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins);

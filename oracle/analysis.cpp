@@ -342,12 +342,20 @@ extern "C" int32_t oracle_analyze_batch(const or_batch* b, uint64_t* out_wcrt, u
   std::vector<int64_t> bins_local((size_t)(nthreads > 0 ? nthreads : 1) * b->n_bins * 2, 0);
   parallel_for(n, nthreads, [&](uint32_t i, int t) {
     System s = read_set(b, i);
+    // a utilisation bin outside [0, n_bins) is a size-range error of the set (reading V):
+    // the set is rejected and counted in no bin
+    const bool bad_bin = b->set_bin && b->n_bins && b->set_bin[i] >= b->n_bins;
     SetResult r = analyze_system(s);
+    if (bad_bin) {
+      r.status = OR_ERANGE;
+      r.sched = 0;
+      r.wcrt.assign(s.chains.size(), OR_UNSCHED);
+    }
     if (out_wcrt)
       for (size_t c = 0; c < r.wcrt.size(); c++) out_wcrt[b->set_chain_off[i] + c] = r.wcrt[c];
     if (out_sched) out_sched[i] = (uint8_t)r.sched;
     if (out_status) out_status[i] = r.status;
-    if (b->set_bin && b->n_bins) {
+    if (b->set_bin && b->n_bins && !bad_bin) {
       const uint32_t bin = b->set_bin[i];
       bins_local[((size_t)t * b->n_bins + bin) * 2] += 1;
       bins_local[((size_t)t * b->n_bins + bin) * 2 + 1] += r.sched;

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
   verdict_done:
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
-      if (out_bins) {
+      if (out_bins && r.bin < n_bins) {  // (pack stores bin = ~0 for an out-of-range bin: ERANGE)
         if (warp_bins) {
           wbins[2 * r.bin]++;
           if (sched) wbins[2 * r.bin + 1]++;

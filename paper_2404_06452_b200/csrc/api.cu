@@ -234,14 +234,17 @@ extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decisi
 }
 
 extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
-                             uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest, const uint64_t* bound,
-                             int64_t* out_violations, paam_stream_t stream) {
+                             uint32_t sim_flags, const paam_sim_out* out, paam_stream_t stream) {
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_simulate: n exceeds the packed sets");
   if (sim_flags & ~(uint32_t)PAAM_SIM_FIFO_DIRECT) return fail(PAAM_EINVAL, "paam_simulate: unknown sim flag");
+  paam_sim_out o{};
+  if (out) o = *out;
+  if (o.witness && !o.violations) return fail(PAAM_EINVAL, "paam_simulate: witness needs violations");
+  if (!o.witness) o.max_witness = 0;
   if (int rc = use_device(sets)) return rc;
-  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
-                         bound, out_violations, const_cast<paam_sets*>(sets)->tickets + 18, (cudaStream_t)stream);
+  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, &o,
+                         const_cast<paam_sets*>(sets)->tickets + 18, (cudaStream_t)stream);
 }
 
 extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
@@ -283,6 +286,23 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   size_t foff[32];
   int32_t* status_dev = out_status;
   if (host) {
+    // The chunk copies below read the host CSR offsets at chunk boundaries: they must be monotone and
+    // within the declared totals (include/paam.h), else a copy range would be wrong or out of bounds.
+    const paam_batch& hb = *batch;
+    uint32_t pc = 0, pb = 0, ps = 0, px = 0, pa = 0;
+    for (int i = 0; i <= K; i++) {
+      const uint32_t s = (uint32_t)((uint64_t)n * i / K);
+      const uint32_t c = hb.set_chain_off[s], x = hb.set_exec_off[s], a = hb.set_accel_off[s];
+      if (c < pc || x < px || a < pa || c > hb.n_chains || x > hb.n_execs || a > hb.n_accels)
+        return fail(PAAM_EINVAL, "paam_pack_analyze: host set offsets not monotone or beyond the batch totals");
+      const uint32_t bcb = hb.chain_cb_off[c];
+      if (bcb < pb || bcb > hb.n_cbs)
+        return fail(PAAM_EINVAL, "paam_pack_analyze: host chain_cb_off not monotone or beyond n_cbs");
+      const uint32_t sg = hb.cb_seg_off[bcb];
+      if (sg < ps || sg > hb.n_segs)
+        return fail(PAAM_EINVAL, "paam_pack_analyze: host cb_seg_off not monotone or beyond n_segs");
+      pc = c; px = x; pa = a; pb = bcb; ps = sg;
+    }
     size_t bytes = 0;
     for (int i = 0; i < nf; i++) { foff[i] = bytes; bytes += align256(f[i].elems * f[i].size); }
     if ((rc = ensure_stage(sets, bytes))) return rc;

@@ -143,8 +143,7 @@ int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
                    cudaStream_t st, int32_t* out_fail = nullptr);
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
-                    const uint64_t* bound, int64_t* out_viol, unsigned int* ticket, cudaStream_t st);
+                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st);
 #endif
 
 }  // namespace paam

@@ -164,7 +164,10 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     bool st2 = !more, st3 = !more;
     int st = PAAM_SET_OK;
 
-    if (nch > MAXC || ncb > MAXCB || nseg > MAXSEG || nex > MAXX || nac > 4) st = PAAM_SET_ERANGE;
+    const uint32_t bin = b.set_bin ? b.set_bin[set] : 0u;
+    // size caps; a utilisation bin outside [0, n_bins) is a range error too (it is counted in no bin)
+    if (nch > MAXC || ncb > MAXCB || nseg > MAXSEG || nex > MAXX || nac > 4 || (b.set_bin && bin >= b.n_bins))
+      st = PAAM_SET_ERANGE;
     uint32_t n_aseg = 0, n_sub = 0, n_unit = 0;
     uint64_t runstart = 0;  // bit j: callback j starts a sub-chain
     uint64_t cstart = 0;    // bit j: callback j is the first of its chain
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     if (lane == 0) {
       r->status = st;
       r->chain_base = c0;
-      r->bin = b.set_bin ? b.set_bin[set] : 0u;
+      r->bin = (b.set_bin && bin >= b.n_bins) ? 0xffffffffu : bin;  // analyze skips an out-of-range bin
       r->n_out = nch;
       if (status_out) status_out[set] = st;
       if (st != PAAM_SET_OK) { r->n_chain = 0; r->n_sub = 0; r->n_aseg = 0; r->n_unit = 0; }

@@ -4,7 +4,10 @@
 // (PiCAS executors P:135-136, fixed-priority cores P:136, PAAM server rules R1-R4 P:366-373,
 // eps / kappa overheads P:374, bucket FIFO on equal priority P:320).  Lane ownership:
 //   lane k  = chain of rank k (k = 0 highest priority): its <= QCAP live instances, release
-//             schedule, statistics;
+//             schedule, statistics.  D14 queues every release of a chain (an unbounded backlog,
+//             S:311); a release that finds all QCAP slots live stops the set's run and reports
+//             PAAM_SIM_BACKLOG (everything up to that release is exact, so the outputs are lower
+//             bounds of the full run's);
 //   lane x  = executor x in canonical order (core asc, process priority desc): job, phase, work;
 //   lane u  = accelerator unit u: state (idle / run / switch-out / switch-in), current request.
 // Every timestamp is settled like this (D15): phase A = (1) unit phase ends and completions,
@@ -29,11 +32,11 @@ namespace paam {
 namespace {
 
 constexpr int SW = 4;      // warps per block
-constexpr int QCAP = 4;    // live instances per chain (D14b)
+constexpr int QCAP = PAAM_SIM_QCAP;  // instance slots per chain; one more live instance stops the run
 constexpr int MAXG = 192;  // segments per set
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint64_t NONE64 = ~0ull;
-constexpr uint64_t STEP_CAP = 50000000ull;  // safety valve: a set exceeding it reports digest ~0
+constexpr uint64_t STEP_CAP = PAAM_SIM_STEP_CAP;  // safety valve: a run past it stops (PAAM_SIM_STEPCAP)
 
 enum { EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_ENQUEUE, EV_ACC_START,
        EV_ACC_PREEMPT, EV_ACC_RESUME, EV_ACC_DONE, EV_CB_DONE, EV_CHAIN_DONE };
@@ -97,7 +100,7 @@ struct DesSmem {
   uint8_t unState[MAXU], unChain[MAXU], unSlot[MAXU];
   uint32_t uQ[MAXU];  // requests queued on the unit (waiting, started or not; the running one included)
   unsigned long long maxResp[MAXC];
-  uint32_t cnt[MAXC];
+  uint32_t cnt[MAXC], miss[MAXC];
 };
 
 // FNV-1a-64 of a 32-byte event record (D17) in two parts: the state after the record's 8-byte time
@@ -182,6 +185,7 @@ struct Ctx {
       const uint64_t resp = t - (S.cPhase[c] + (uint64_t)I.k * S.cT[c]);  // D16
       atomicMax(&S.maxResp[c], (unsigned long long)resp);
       atomicAdd(&S.cnt[c], 1u);
+      if (resp > S.cD[c]) atomicAdd(&S.miss[c], 1u);  // D16: deadline miss
       ev(EV_CHAIN_DONE, c, FULL, FULL, FULL, FULL);
       I.state = I_FREE;
     }
@@ -195,11 +199,12 @@ struct Ctx {
 #endif
 __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
                                                            uint64_t horizon, uint64_t seed, uint64_t first_index,
-                                                           uint32_t sim_flags, uint64_t* __restrict__ out_resp, uint64_t* __restrict__ out_count,
-                                                           uint64_t* __restrict__ out_digest,
-                                                           const uint64_t* __restrict__ bound,
-                                                           int64_t* __restrict__ out_viol,
+                                                           uint32_t sim_flags, paam_sim_out o,
                                                            unsigned int* __restrict__ ticket) {
+  uint64_t* __restrict__ out_resp = o.resp;
+  uint64_t* __restrict__ out_count = o.count;
+  uint64_t* __restrict__ out_digest = o.digest;
+  const uint64_t* __restrict__ bound = o.bound;
   __shared__ DesSmem smem[SW];
   const uint32_t lane = threadIdx.x & 31;
   DesSmem& S = smem[threadIdx.x >> 5];
@@ -218,8 +223,11 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       for (uint32_t i = lane; i < nch; i += 32) {
         if (out_resp) out_resp[c0 + i] = 0;
         if (out_count) out_count[c0 + i] = 0;
+        if (o.misses) o.misses[c0 + i] = 0;
+        if (o.drops) o.drops[c0 + i] = 0;
       }
       if (lane == 0 && out_digest) out_digest[set] = 0;
+      if (lane == 0 && o.status) o.status[set] = PAAM_SIM_INVALID;
       continue;
     }
     const uint32_t x0 = b.set_exec_off[set], nex = b.set_exec_off[set + 1] - x0;
@@ -355,6 +363,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       S.iWUnit[lane] = rep4(NOQ);
       S.maxResp[lane] = 0;
       S.cnt[lane] = 0;
+      S.miss[lane] = 0;
       S.exPhase[lane] = P_NONE;
       S.exChain[lane] = 0xff;
     }
@@ -367,9 +376,10 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     uint64_t next_rel = (uint32_t)lane < nch ? S.cPhase[lane] : NONE64;  // release time of instance next_k (D2)
     uint32_t seq = 0;     // warp-uniform
     bool on_core = false; // lane = canonical executor
-    uint32_t drops = 0, ovf = 0;
+    uint32_t drops = 0;
     uint64_t steps = 0;
-    bool aborted = false;
+    int32_t stop = PAAM_SIM_OK;  // warp-uniform: why the run stopped early (PAAM_SIM_BACKLOG / _STEPCAP)
+    bool backlog = false;         // lane = chain: a release found every instance slot live
     const bool is_chain = lane < nch, is_exec = lane < nex, is_unit = lane < n_unit;
 
     for (;;) {
@@ -462,8 +472,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               const uint32_t fm = slots_eq(S.iState[c], I_FREE);
               const int slot = fm ? (int)slot_of(fm) : -1;
               if (slot < 0) {
-                ovf++;
-                C.ev(EV_OVERFLOW, c, FULL, FULL, FULL, FULL);
+                backlog = true;  // D14: the new instance would be the chain's (QCAP+1)-th live one
               } else {
                 InstRef I = S.ref(c, slot);
                 I.state = I_READY; I.k = next_k; I.cb = 0; I.wunit = NOQ;
@@ -475,7 +484,9 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             }
           }
           __syncwarp();
-          run_a = __any_sync(FULL, due_x);
+          // a backlog stop is checked only when the cheap vote fires (it almost never does)
+          run_a = __any_sync(FULL, due_x || backlog);
+          if (run_a && __any_sync(FULL, backlog)) { stop = PAAM_SIM_BACKLOG; goto sim_done; }
         }
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
         bool needB = false, dueB = false;  // another phase-B pass could act / B left phase-A work due now
@@ -674,7 +685,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       }
       nd = __reduce_min_sync(FULL, nd);
       if (nd == 0xffffffffu) break;
-      if (++steps > STEP_CAP) { aborted = true; break; }
+      if (++steps > STEP_CAP) { stop = PAAM_SIM_STEPCAP; break; }
       const uint64_t nt = C.t + nd;
       if (run_x) S.exRem[lane] -= nd;
       if (run_u) S.unRem[lane] -= nd;
@@ -683,26 +694,44 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       __syncwarp();
     }
 
+  sim_done:
     // ---- outputs ---------------------------------------------------------------------------------------
+    // A stopped run's statistics cover the exact prefix up to the stop (lower bounds of the full run's);
+    // its chains are not checked against the bound (census[stopped] counts it instead).
     const uint64_t digest = warp_sum_u64(C.dig);
-    bool viol = false, set_sched = bound != nullptr;
+    bool viol = false, set_sched = bound != nullptr && stop == PAAM_SIM_OK;
+    uint64_t bd = 0;
     if (is_chain) {
       const uint32_t local = S.cLocal[lane];
       if (out_resp) out_resp[c0 + local] = S.maxResp[lane];
       if (out_count) out_count[c0 + local] = S.cnt[lane];
+      if (o.misses) o.misses[c0 + local] = S.miss[lane];
+      if (o.drops) o.drops[c0 + local] = drops;
       if (bound) {
-        const uint64_t bd = bound[c0 + local];
+        bd = bound[c0 + local];
         if (S.cCls[lane] == 0 && (bd == PAAM_UNSCHED || bd > S.cD[lane])) set_sched = false;
         viol = S.cCls[lane] == 0 && S.maxResp[lane] > bd;
       }
     }
     set_sched = __all_sync(FULL, set_sched || !is_chain);
-    const uint32_t nv = __popc(__ballot_sync(FULL, viol && set_sched));
-    if (lane == 0) {
-      if (out_digest) out_digest[set] = aborted ? ~0ull : digest;
-      if (out_viol && nv) atomicAdd((unsigned long long*)out_viol, (unsigned long long)nv);
+    const uint32_t vm = __ballot_sync(FULL, viol && set_sched);
+    if (vm && o.violations) {  // sim > bound: count, and record the first max_witness witnesses
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd((unsigned long long*)o.violations, (unsigned long long)__popc(vm));
+      base = __shfl_sync(FULL, base, 0);
+      if ((vm >> lane) & 1u) {
+        const unsigned long long w = base + __popc(vm & lanemask_lt());
+        if (o.witness && w < o.max_witness) {
+          o.witness[2 * w] = set;
+          o.witness[2 * w + 1] = S.cLocal[lane];
+        }
+      }
     }
-    (void)drops; (void)ovf;
+    if (lane == 0) {
+      if (out_digest) out_digest[set] = digest;
+      if (o.status) o.status[set] = stop;
+      if (o.stopped && stop != PAAM_SIM_OK) atomicAdd((unsigned long long*)o.stopped, 1ull);
+    }
     __syncwarp();
   }
 }
@@ -711,8 +740,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
 
 #ifndef PAAM_WARP_EMU
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, uint64_t* out_resp, uint64_t* out_count, uint64_t* out_digest,
-                    const uint64_t* bound, int64_t* out_viol, unsigned int* ticket, cudaStream_t st) {
+                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st) {
   if (n == 0) return PAAM_OK;
   cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   int dev = 0, sms = 148, per_sm = 1;
@@ -723,8 +751,7 @@ int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t
   const uint32_t need = (n + SW - 1) / SW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, out_resp, out_count, out_digest,
-                                           bound, out_viol, ticket);
+  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, *out, ticket);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "simulate_kernel launch");

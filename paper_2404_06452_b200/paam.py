@@ -59,6 +59,16 @@ class PaamGenParams(ctypes.Structure):
     ]
 
 
+class PaamSimOut(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_void_p) for k in ("resp", "count", "misses", "drops", "digest", "status", "bound",
+                                              "violations", "witness", "stopped")] + \
+               [("max_witness", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
+
+
+PAAM_SIM_OK, PAAM_SIM_INVALID, PAAM_SIM_BACKLOG, PAAM_SIM_STEPCAP = 0, 1, 2, 3
+PAAM_SIM_QCAP = 4
+
+
 class PaamError(RuntimeError):
     pass
 
@@ -91,7 +101,7 @@ def lib():
         L.paam_admit.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp]
         L.paam_pack_analyze.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
-                                    ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp]
+                                    ctypes.c_uint32, ctypes.POINTER(PaamSimOut), _vp]
         L.paam_sets_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_uint32)]
         L.paam_free.argtypes = [_vp]
@@ -255,14 +265,19 @@ class Sets:
                                              else out_status.data_ptr())
         set_device_from_torch()
         check(lib().paam_pack(ctypes.byref(c), ctypes.byref(self.h), st, _stream_ptr(stream)), "paam_pack")
-        self.n_sets = c.n_sets
-        self.n_chains = c.n_chains
-        self.n_bins = c.n_bins if c.set_bin else 0
+        self._refresh()
+
+    def _refresh(self):
+        """n_sets / n_chains / n_bins of the batch last packed into the handle (paam_sets_info)."""
+        a, b, c = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        check(lib().paam_sets_info(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "paam_sets_info")
+        self.n_sets, self.n_chains, self.n_bins = a.value, b.value, c.value
 
     def repack(self, batch, out_status=None, stream=None):
         st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
                                              else out_status.data_ptr())
         check(lib().paam_repack(ctypes.byref(batch.c), self.h, st, _stream_ptr(stream)), "paam_repack")
+        self._refresh()
 
     def admit(self, out_decision, out_wcrt=None, n=None, stream=None):
         """Batched admission decisions (paam_admit): -1 accept, >= 0 first failing chain, <= -2 invalid."""
@@ -278,6 +293,7 @@ class Sets:
                                              else out_status.data_ptr())
         check(lib().paam_pack_analyze(ctypes.byref(batch.c), self.h, st, ptr(out_wcrt), ptr(out_sched),
                                       ptr(out_bins), _stream_ptr(stream)), "paam_pack_analyze")
+        self._refresh()
 
     def analyze(self, out_wcrt=None, out_sched=None, out_bins=None, n=None, stream=None):
         """Device tensors (torch) or None; returns nothing (asynchronous on `stream`)."""
@@ -285,13 +301,21 @@ class Sets:
         check(lib().paam_analyze(self.h, self.n_sets if n is None else n, ptr(out_wcrt), ptr(out_sched),
                                  ptr(out_bins), _stream_ptr(stream)), "paam_analyze")
 
-    def simulate(self, horizon, seed, out_resp, out_count=None, out_digest=None, bound=None, out_violations=None,
-                 first_index=0, n=None, stream=None, fifo=False):
+    def simulate(self, horizon, seed, out_resp=None, out_count=None, out_digest=None, bound=None, out_violations=None,
+                 first_index=0, n=None, stream=None, fifo=False, out_misses=None, out_drops=None, out_status=None,
+                 out_witness=None, out_stopped=None):
+        """paam_simulate (device tensors or None).  out_witness: int32 tensor [2*K] of (set, chain) pairs
+        of sim > bound, filled first come (needs out_violations)."""
         ptr = lambda t: None if t is None else t.data_ptr()
+        o = PaamSimOut()
+        for k, t in (("resp", out_resp), ("count", out_count), ("misses", out_misses), ("drops", out_drops),
+                     ("digest", out_digest), ("status", out_status), ("bound", bound), ("violations", out_violations),
+                     ("witness", out_witness), ("stopped", out_stopped)):
+            setattr(o, k, ptr(t))
+        o.max_witness = 0 if out_witness is None else out_witness.numel() // 2
         check(lib().paam_simulate(self.h, self.n_sets if n is None else n, horizon, seed, first_index,
-                                  PAAM_SIM_FIFO_DIRECT if fifo else 0, ptr(out_resp),
-                                  ptr(out_count), ptr(out_digest), ptr(bound), ptr(out_violations),
-                                  _stream_ptr(stream)), "paam_simulate")
+                                  PAAM_SIM_FIFO_DIRECT if fifo else 0, ctypes.byref(o), _stream_ptr(stream)),
+              "paam_simulate")
 
     def free(self):
         if self.h:

@@ -341,3 +341,35 @@ def test_malformed_csr_ranges_are_rejected_per_set():
     others = [k for k in range(len(systems)) if k not in (i, i + 1, j)]
     assert np.array_equal(st[others], ost[others])
     assert np.array_equal(sched.cpu().numpy()[others], osch[others])
+
+
+@pytest.mark.parametrize("n_bins", [9, 40])
+def test_out_of_range_bin_is_rejected_not_counted(n_bins):
+    """A set whose utilisation bin is >= n_bins is PAAM_SET_ERANGE and counted in no bin, for the
+    per-warp shared-memory counters (n_bins <= 32) and the direct global atomics (n_bins > 32)."""
+    rng = random.Random(5 + n_bins)
+    systems = [random_small_system(rng, max_chains=5) for _ in range(300)]
+    for i, s in enumerate(systems):
+        s.bin = i % n_bins
+    b = flatten(systems, comm_cost=1, n_bins=n_bins)
+    b["set_bin"] = b["set_bin"].copy()
+    b["set_bin"][[3, 77, 150]] = [n_bins, n_bins + 5, 0xFFFFFFFF]
+    ow, osch, ost, ob = O.analyze(b, nthreads=NPROC)
+    assert (ost[[3, 77, 150]] == 1).all() and ob.sum() == 2 * 0 + ob.sum()  # oracle rejects them too
+    assert ob[0::2].sum() == len(systems) - 3
+    assert_same(b, gpu_host_path(b))
+    assert_same(b, gpu_device_path(b))
+
+
+def test_host_pipeline_rejects_non_monotone_offsets():
+    """paam_pack_analyze with a host batch reads CSR offsets at chunk boundaries; offsets that are not
+    monotone or exceed the totals fail the call with PAAM_EINVAL instead of copying wrong ranges."""
+    p = config3_params()
+    h = generate_host(p, 4, 0, 8192)
+    bad = dict(h)
+    bad["set_chain_off"] = h["set_chain_off"].copy()
+    bad["set_chain_off"][4096] = bad["set_chain_off"][-1] + 10
+    hb = paam.Batch.from_host(h)
+    sets = paam.Sets(hb)
+    with pytest.raises(paam.PaamError, match="invalid argument"):
+        sets.pack_analyze(paam.Batch.from_host(bad), None, None, None)

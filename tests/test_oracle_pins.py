@@ -291,3 +291,13 @@ def test_lemma3_union_counts_each_hp_segment_once():
     assert d["sub_C"][1] == g["C_c"] and d["sub_Hstar"][1] == g["Hstar_c"]
     assert d["sub_R"][1] == g["R_c"] and wcrt[1] == g["R_c"]
     assert g["R_c"] != g["R_c_if_summed_per_segment"]
+
+
+def test_out_of_range_bin_is_a_range_error():
+    """A utilisation bin outside [0, n_bins) rejects the set (ERANGE, reading V) and counts it nowhere."""
+    s = two_chain_accel_system()
+    b = flatten([s, s, s], comm_cost=0, n_bins=2)
+    b["set_bin"] = np.array([0, 2, 1], np.uint32)
+    _, sched, status, bins = O.analyze(b)
+    assert status.tolist() == [0, 1, 0] and sched.tolist() == [1, 0, 1]
+    assert bins.tolist() == [1, 1, 1, 1]

@@ -18,7 +18,7 @@ L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.envi
 vp = ctypes.c_void_p
 L.emu_pack.argtypes = [vp, vp, vp]
 L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
-L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp, vp, vp, vp, vp]
+L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp]
 L.emu_record_bytes.restype = ctypes.c_uint32
 
 
@@ -42,13 +42,20 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
                   None, sv.ctypes.data, bv.ctypes.data if hb.c.set_bin else None)
     out.update(sched_v=sv[:n], bins_v=bv[:2 * hb.c.n_bins])
     if horizon is not None:
-        resp = np.zeros(nch, np.uint64)
-        cnt = np.zeros(nch, np.uint64)
+        from paper_2404_06452_b200.paam import PaamSimOut
+        a = {k: np.zeros(nch, np.uint64) for k in ("resp", "count", "misses", "drops")}
         dig = np.zeros(max(n, 1), np.uint64)
         viol = np.zeros(1, np.int64)
-        L.emu_simulate(ctypes.addressof(hb.c), rec.ctypes.data, n, horizon, seed, first, 1 if fifo else 0, resp.ctypes.data,
-                       cnt.ctypes.data, dig.ctypes.data, None if fifo else w.ctypes.data, viol.ctypes.data)
-        out.update(resp=resp[:hb.c.n_chains], count=cnt[:hb.c.n_chains], digest=dig[:n], violations=int(viol[0]))
+        status = np.full(max(n, 1), -1, np.int32)
+        o = PaamSimOut()
+        for k, v in a.items():
+            setattr(o, k, v.ctypes.data)
+        o.digest, o.status, o.violations = dig.ctypes.data, status.ctypes.data, viol.ctypes.data
+        o.bound = None if fifo else w.ctypes.data
+        L.emu_simulate(ctypes.addressof(hb.c), rec.ctypes.data, n, horizon, seed, first, 1 if fifo else 0,
+                       ctypes.addressof(o))
+        out.update({k: v[:hb.c.n_chains] for k, v in a.items()})
+        out.update(digest=dig[:n], violations=int(viol[0]), sim_status=status[:n])
     return out
 
 
@@ -63,8 +70,21 @@ def compare(batch, horizon=None, seed=0, first=0, label="", fifo=False):
         msg.append(f"  status o={ost[:8]} e={e['status'][:8]} wcrt bad idx {bad} o={ow[bad]} e={e['wcrt'][bad]}")
     if horizon is not None:
         o = O.simulate(batch, horizon, seed=seed, first_index=first, bound=None if fifo else e["wcrt"], nthreads=8, fifo=fifo)
-        ok2 = (np.array_equal(o["resp"], e["resp"]) and np.array_equal(o["count"], e["count"])
-               and np.array_equal(o["digest"], e["digest"]) and o["violations"] == e["violations"])
+        # sets whose oracle backlog exceeds the device's 4 slots are stopped (PAAM_SIM_BACKLOG = 2) and
+        # excluded; every other set must agree exactly (and then the violation counts agree as well
+        # unless a stopped set had violations in the oracle's full run)
+        off = batch["set_chain_off"].astype(np.int64)
+        m = np.diff(off)
+        nz = m > 0
+        over = np.zeros(len(m), bool)
+        if nz.any():
+            pk = np.maximum.reduceat(o["peak_live"], (np.cumsum(m) - m)[nz])
+            over[nz] = pk > 4
+        full = ~np.repeat(over, m)
+        ok2 = np.array_equal(e["sim_status"] == 2, over) and not (e["sim_status"] == 3).any()
+        for k in ("resp", "count", "misses", "drops"):
+            ok2 = ok2 and np.array_equal(o[k][full], e[k][full])
+        ok2 = ok2 and np.array_equal(o["digest"][~over], e["digest"][~over])
         msg.append(f"  des {'OK' if ok2 else 'MISMATCH'}")
         if not ok2:
             msg.append(f"  resp o={o['resp'][:8]} e={e['resp'][:8]}\n  count o={o['count'][:8]} e={e['count'][:8]}"

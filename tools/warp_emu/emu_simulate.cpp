@@ -1,12 +1,11 @@
 #include "../../paper_2404_06452_b200/csrc/simulate.cu"
 extern "C" void emu_simulate(const paam_batch* b, const paam::Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                             uint64_t first, uint32_t simf, uint64_t* resp, uint64_t* cnt, uint64_t* dig, const uint64_t* bound,
-                             int64_t* viol) {
+                             uint64_t first, uint32_t simf, const paam_sim_out* out) {
   gridDim.x = 1;
   static unsigned int ticket;
   ticket = 0;
   emu::launch_block(0, paam::SW * 32, [&]() {
-    paam::simulate_kernel(*b, rec, n, horizon, seed, first, simf, resp, cnt, dig, bound, viol, &ticket);
+    paam::simulate_kernel(*b, rec, n, horizon, seed, first, simf, *out, &ticket);
   });
 }
 extern "C" unsigned emu_record_bytes() { return sizeof(paam::Record); }
