@@ -7,13 +7,15 @@
 //           unit u share T_k, so sum mu*A* = mu * sum A* exactly).  Computed on demand: step 4 first
 //           uses the lower bound S_lb (sum of the start values) and asks for the exact S_c only where
 //           the min(S_c, C_c) could depend on it (see step 4); the sound blocking flag computes all.
-//   step 4  Theorem 1 / Eq.5 per sub-chain, in waves of up to four sub-chains whose
-//           dependencies (hp, spinning hpp: earlier in the canonical order, A7) are solved, first
-//           ready first, one 8-lane group per sub-chain: lanes take the Lemma-3 chains and the
-//           hp / hpp sub-chains in turn, two saturating butterfly reductions per iterate give the
-//           Lemma-3 interference (Eq.4, union form A1) and the CPU interference, and
-//           H*_c(R) = min(S_c, C_c(R)) + sum eps (Eq.1).  Convergence / deadline miss are
-//           group-uniform because every lane of a group holds the same reduced value.
+//   step 4  Theorem 1 / Eq.5: every sub-chain of the set at once, one lane each.  The
+//           sub-chains depend on each other only through H*_h of their hp / spinning hpp sub-chains
+//           (acyclic, A7), so the joint least fixed point of the whole system is the sequential one; it
+//           is reached by Jacobi iteration from below (every lane evaluates F at its current R with the
+//           H*_h of the previous iterate; stop when no R and no H* changes).  mu(R, T) = 2 +
+//           floor((R-1)/T) (Eq.2 for R >= 1), and the floor term is non-zero only for periods T < R:
+//           an iterate adds the mu = 2 part from pack (sA2, and 2 X_h) and walks the set's chains in
+//           period order only up to the first T >= R.  H*_c(R) = min(S_c, C_c(R)) + sum eps (Eq.1,
+//           P:1092), C_c = Lemma 3 in union form (Eq.4, A1).
 //   step 5  R* = sum of sub-chain R_c + comm per executor crossing (A9); verdict = every
 //           CRITICAL chain has R* <= D, voted with __all_sync.
 //   step 6  per-warp shared-memory bin counts, flushed with one global atomic per bin at warp exit.
@@ -37,33 +39,15 @@ constexpr uint64_t UNS = PAAM_UNSCHED;
 struct __align__(16) WarpSmem {
   Record rec;
   uint32_t H[MAXA];    // Lemma-2 value per accelerator segment (SAT = UNB)
-  uint32_t S[MAXS];    // per-segment bound summed over the sub-chain
-  uint32_t Bc[MAXS];   // blocking term in use (as written, or the sound variant)
   uint32_t R[MAXS];    // converged R_c (SAT = UNSCHED)
-  uint32_t Hs[MAXS];   // H*_c(R_c) of every solved sub-chain
+  uint32_t Hs[MAXS];   // H*_c at the sub-chain's current iterate (SAT once it is UNSCHED)
+  uint8_t posOf[MAXC]; // period position of chain rank k
+  uint8_t sPos[MAXS];  // period position of sub-chain h's chain
   unsigned long long sum[MAXC];  // end-to-end accumulation per chain
   uint32_t uns[MAXC];
-  uint8_t gpos[4];          // the sub-chains of the current Eq.5 wave, one per lane group
 };
 
 constexpr uint32_t FULL = 0xffffffffu;
-// 8-lane group reductions (xor within aligned groups of 8)
-__device__ __forceinline__ void gsum8x2(uint32_t& a, uint32_t& b) {
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) {
-    const uint32_t xa = __shfl_xor_sync(FULL, a, o), xb = __shfl_xor_sync(FULL, b, o);
-    a = sadd(a, xa);
-    b = sadd(b, xb);
-  }
-}
-__device__ __forceinline__ bool gor8(bool p) {
-  uint32_t v = p;
-  v |= __shfl_xor_sync(FULL, v, 4);
-  v |= __shfl_xor_sync(FULL, v, 2);
-  v |= __shfl_xor_sync(FULL, v, 1);
-  return v != 0;
-}
-
 // Lemma 2 (Eq.3) for accelerator segment i: the least fixed point of
 // G(h) = aBase2 + sum_{k<r} floor((h-1)/T_k) * W[k][u] from aBase2, or SAT (UNB) once an iterate
 // exceeds the cutoff (A4).  aBase2 already holds A* + LPB + 2 sum_{k<r} W[k][u] (the "+2" of every mu),
@@ -94,6 +78,76 @@ __device__ __forceinline__ uint32_t lemma2(const Record& r, uint32_t i) {
   return SAT;
 }
 
+// One Eq.5 evaluation F_c(R) (Theorem 1) for R >= 1, with mu(R, T) = 2 + floor((R-1)/T)
+// (Eq.2): the mu = 2 parts come precomputed (A2 = base3 + 2 sum WU for Lemma 3, xs2 = 2 sum X_h of the
+// static interferers), and the floor parts are added only for periods T < R -- for the Lemma-3 chains
+// by walking their period positions (lmask) in ascending period order up to the first T >= R.
+// C = C_c(R) (Eq.4, union form A1), nH = H*_c(R) = min(S, C) + eps (Eq.1), F = B + E + H* +
+// the hp / hpp interference (SAT = above the cutoff: UNSCHED, A4; then H* = SAT poisons dependants, A8).
+// WIDE: every period >= 64 ns, so q * W < 2^56 and the u64 sums of <= 64 products cannot overflow;
+// otherwise every product's high word is checked.
+template <bool WIDE>
+__device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uint32_t R, uint32_t lmask, uint32_t wsel,
+                                         uint32_t umask, uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut,
+                                         uint32_t xm, uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F,
+                                         uint32_t& nH, uint32_t& C) {
+  const uint32_t h2 = (R - 1u) << 1;
+  uint64_t acc = 0;
+  uint32_t hi = 0;
+  for (uint32_t m = lmask; m;) {
+    const uint32_t i = __ffs(m) - 1;
+    const uint4 p = r.pTab[i];  // {T, M, rank | L << 8, W[rank][0] + W[rank][1]}
+    if (p.x >= R) break;        // this and every later period: floor((R-1)/T) = 0
+    m &= m - 1;
+    const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
+    uint32_t wu = p.w;
+    if (wsel) {  // not both of units 0 and 1: one unit (wsel = unit + 1), or the general unit union
+      const uint32_t k = p.z & 0xffu;
+      if (wsel <= MAXU) {
+        wu = r.W[k][wsel - 1];
+      } else {
+        wu = 0;
+        for (uint32_t um = umask; um; um &= um - 1) wu = sadd(wu, r.W[k][__ffs(um) - 1]);
+      }
+    }
+    if (WIDE) {
+      acc += (uint64_t)q * wu;
+    } else {
+      const uint64_t pr = (uint64_t)q * wu;
+      acc += pr;
+      hi |= (uint32_t)(pr >> 32);
+    }
+  }
+  acc += A2;
+  C = (hi || acc > SAT) ? SAT : (uint32_t)acc;  // C_c(R), Eq.4
+  nH = sadd(min(S, C), eps);                     // H*_c(R), Eq.1
+  uint64_t xs = xs2;  // CPU interference (hp, hpp): the mu = 2 part of the static interferers
+  for (uint32_t m = depm; m; m &= m - 1) {  // X_h = E_h + H*_h at h's current iterate (hp, spinning hpp)
+    const uint32_t h = __ffs(m) - 1;
+    const uint32_t X = sadd(r.sE[h], w.Hs[h]);
+    const uint4 p = r.pTab[w.sPos[h]];
+    const uint32_t q = p.x < R ? (__umulhi(h2, p.y) >> (p.z >> 8)) : 0u;
+    const uint64_t pr = (uint64_t)(q + 2u) * X;
+    xs += pr;
+    if (!WIDE) hi |= (uint32_t)(pr >> 32);
+  }
+  if (R > xTmin) {  // the floor terms of suspending hpp interferers with T_h < R: X_h = E_h + eps_h
+    for (uint32_t m = xm & ~depm; m; m &= m - 1) {
+      const uint32_t h = __ffs(m) - 1;
+      const uint4 p = r.pTab[w.sPos[h]];
+      if (p.x < R) {
+        const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
+        const uint64_t pr = (uint64_t)q * sadd(r.sE[h], r.sEps[h]);
+        xs += pr;
+        if (!WIDE) hi |= (uint32_t)(pr >> 32);
+      }
+    }
+  }
+  const uint64_t f = (uint64_t)BE + nH + xs;
+  F = (hi || f > cut) ? SAT : (uint32_t)f;  // above the cutoff: UNSCHED (A4)
+  if (F == SAT) nH = SAT;                   // dependants become UNSCHED as well (A8)
+}
+
 #ifndef ANA_MINB
 #define ANA_MINB 4
 #endif
@@ -112,6 +166,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
   const bool warp_bins = out_bins && n_bins <= WARP_BINS;  // per-warp counters, flushed at warp exit
   if (warp_bins) for (uint32_t i = lane; i < 2 * n_bins; i += 32) wbins[i] = 0;
   Record& r = w.rec;
+  const bool sound = (flags & PAAM_FLAG_BLOCKING_SOUND) != 0;  // aEps / aCbE / sLp are read only then
 
   // Dynamic work distribution: warps take TICK consecutive sets per atomic ticket, so the per-set
   // cost variance does not leave warps (and their block's resources) idle at the end.
@@ -135,10 +190,13 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const uint4* src = reinterpret_cast<const uint4*>(recs + set);
       uint4* dst = reinterpret_cast<uint4*>(&r);
       constexpr int NV = sizeof(Record) / 16;
-      constexpr int V_CH = offsetof(Record, cCut) / 16, V_W = offsetof(Record, W) / 16;
+      constexpr int V_CH = offsetof(Record, cCut) / 16, V_P = offsetof(Record, pTab) / 16;
+      constexpr int V_W = offsetof(Record, W) / 16;
       constexpr int V_SUB = offsetof(Record, sE) / 16, V_SEG = offsetof(Record, aBase2) / 16;
-      static_assert(V_CH == 2 && V_W - V_CH == 4 * MAXC / 4 && V_SEG - V_SUB == 9 * MAXS / 4 &&
-                        NV - V_SEG == 4 * MAXA / 4 && MAXU == 8,
+      constexpr int V_SND = offsetof(Record, aEps) / 16;  // aEps, aCbE: sound blocking only
+      static_assert(V_CH == 2 && V_P - V_CH == 4 * MAXC / 4 && V_W - V_P == MAXC && V_SEG - V_SUB == 10 * MAXS / 4 &&
+                        V_SND - V_SEG == 2 * MAXA / 4 && NV - V_SEG == 4 * MAXA / 4 && MAXU == 8 && MAXC == 32 &&
+                        MAXS == 32,
                     "live-vector map assumes the Record layout in common.cuh");
       const uint32_t nc = hdr & 0xffu, vc = (nc + 3) >> 2, vs = (((hdr >> 8) & 0xffu) + 3) >> 2;
       const uint32_t va = (((hdr >> 16) & 0xffu) + 3) >> 2;
@@ -152,10 +210,11 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
         for (int k = 0; k < 4; k++) {
           const int i = lane + 32 * (k0 + k);
           const bool live = i < V_CH    ? true
-                            : i < V_W   ? (uint32_t)((i - V_CH) & (MAXC / 4 - 1)) < vc
+                            : i < V_P   ? (uint32_t)((i - V_CH) & (MAXC / 4 - 1)) < vc
+                            : i < V_W   ? (uint32_t)(i - V_P) < nc  // one period-table entry per vector
                             : i < V_SUB ? (uint32_t)((i - V_W) >> 1) < nc  // W row k = 2 vectors
                             : i < V_SEG ? (uint32_t)((i - V_SUB) & (MAXS / 4 - 1)) < vs
-                            : i < NV    ? (uint32_t)((i - V_SEG) & (MAXA / 4 - 1)) < va
+                            : i < NV    ? (uint32_t)((i - V_SEG) & (MAXA / 4 - 1)) < va && (i < V_SND || sound)
                                         : false;
           livem |= (uint32_t)live << k;
           v[k] = live ? __ldg(src + i) : uint4{0u, 0u, 0u, 0u};
@@ -189,8 +248,8 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       // ---- step 3: Lemma 2, one lane per accelerator segment ----------------------------------------
       // Only the sound blocking term (A10) needs every H up front.  Otherwise S_c enters Eq.5 only as
       // min(S_c, C_c(R)) and C_c almost always wins, so step 4 starts from the lower bound
-      // S_lb = sum of the Lemma-2 start values and computes the exact S_c only for a sub-chain whose
-      // C_c at the converged R exceeds S_lb (see step 4).
+      // S_lb = sum of the Lemma-2 start values (pack's sSlb) and computes the exact S_c only for a
+      // sub-chain whose C_c at the converged R exceeds S_lb (see step 4).
       // Segments are in rank order (rank = number of HP chains = loop length), so the loop cost of a
       // round is set by its highest rank: the first round takes segments [0, nas-32) (short loops),
       // the second the last 32 (nas <= 64).
@@ -200,14 +259,24 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
         for (uint32_t i = lane < f ? lane : f + lane; i < nas; i = (i < f) ? f + lane : nas) w.H[i] = lemma2(r, i);
       }
       __syncwarp();
-      // per-segment sums S_c and the blocking term in use
-      if (lane < nsub) {
-        const uint32_t sg = r.sSeg[lane], a0 = sg & 0xffu, na = (sg >> 8) & 0xffu;
-        uint32_t S = 0;
-        for (uint32_t i = a0; i < a0 + na; i++) S = sadd(S, lazy_s ? r.aBase2[i] : w.H[i]);  // S_lb or S_c
-        w.S[lane] = S;
+      // ---- per sub-chain constants (lane = sub-chain in canonical order) -----------------------------
+      const bool act = lane < (int)nsub;
+      uint32_t rk = 0, umask = 0, cut = 0, BE = 0, A2 = 0, S = 0, eps = 0, hpm = 0, hppm = 0;
+      if (act) {
+        const uint32_t misc = r.sMisc[lane];
+        rk = misc & 0xffu;
+        umask = (misc >> 8) & 0xffu;
+        cut = r.cCut[rk];
+        A2 = r.sA2[lane];
+        eps = r.sEps[lane];
+        hpm = r.sHp[lane];
+        hppm = r.sHpp[lane];
         uint32_t B = r.sB[lane];
-        if (flags & PAAM_FLAG_BLOCKING_SOUND) {  // A10: an LP callback also holds its accelerator wait
+        if (lazy_s) {
+          S = r.sSlb[lane];
+        } else {  // exact S_c, and A10: an LP callback also holds its accelerator wait
+          const uint32_t sg = r.sSeg[lane], a0 = sg & 0xffu, na = (sg >> 8) & 0xffu;
+          for (uint32_t i = a0; i < a0 + na; i++) S = sadd(S, w.H[i]);
           uint32_t lp = r.sLp[lane];
           while (lp) {
             const uint32_t l = __ffs(lp) - 1;
@@ -226,166 +295,104 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
             if (cur_cb != 0xffffffffu) B = max(B, v);
           }
         }
-        w.Bc[lane] = B;
+        BE = sadd(B, r.sE[lane]);
+      }
+      const uint32_t spin_mask = __ballot_sync(FULL, act && ((r.sMisc[lane] >> 16) & 1u));
+      const uint32_t depm = hpm | (hppm & spin_mask);  // X_h = E_h + H*_h (hp, spinning hpp: P:1132)
+      const uint32_t xm = hpm | hppm;                   // every CPU interferer (Eq.5 sums)
+      const bool critical = act && ((r.cMisc[rk] >> 8) & 0xffu) == 0;
+      const bool wide = (r.hflags & REC_WIDE_OK) != 0u;  // set-uniform: unchecked 64-bit mu sums
+      bool sexact = !lazy_s;
+      // period positions of the chains (pTab is in ascending period order)
+      if (lane < (int)nch) w.posOf[r.pTab[lane].z & 0xffu] = (uint8_t)lane;
+      __syncwarp();
+      // lmask: period positions of the chains of rank < rk (Lemma-3 interferers, Eq.4), an exclusive
+      // OR-scan over ranks of 1 << position
+      uint32_t pb = lane < (int)nch ? (1u << w.posOf[lane]) : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, pb, o);
+        if (lane >= o) pb |= y;
+      }
+      uint32_t pex = __shfl_up_sync(FULL, pb, 1);
+      if (lane == 0) pex = 0;
+      const uint32_t lm_rk = __shfl_sync(FULL, pex, rk);  // every lane shuffles (rk = 0 when inactive)
+      const uint32_t lmask = act ? lm_rk : 0u;
+      const uint32_t n_unit = r.n_unit;
+      // Lemma-3 weight of chain k for this sub-chain: W[k][0] + W[k][1] (pTab.w) when it uses exactly
+      // units 0 and 1 of a <= 2-unit set (wsel = 0), W[k][u] for a single unit u (wsel = u + 1), else
+      // the union over its units (wsel = MAXU + 1)
+      const uint32_t wsel = (n_unit <= 2 && umask == (1u << n_unit) - 1u) ? 0u
+                            : __popc(umask) == 1 ? (uint32_t)__ffs(umask) : (uint32_t)MAXU + 1u;
+      // CPU interference of the suspending hpp interferers with every mu = 2 (2 (E_h + eps_h):
+      // spin() = delta eps), and their smallest period; the dependencies (hp, spinning hpp)
+      // are added per iterate
+      uint32_t xs2 = 0, xTmin = 0xffffffffu;
+      if (act) {
+        w.sPos[lane] = w.posOf[rk];
+        for (uint32_t m = xm & ~depm; m; m &= m - 1) {
+          const uint32_t h = __ffs(m) - 1;
+          xs2 = sadd(xs2, sadd(r.sE[h], r.sEps[h]));
+          xTmin = min(xTmin, r.pTab[w.posOf[r.sMisc[h] & 0xffu]].x);
+        }
+        xs2 = sadd(xs2, xs2);
       }
       __syncwarp();
 
-      // ---- step 4: Eq.5, waves of up to four ready sub-chains, one 8-lane group each -------------------
-      // A sub-chain's Eq.5 reads the results of its hp sub-chains and spinning hpp sub-chains only
-      // (H*_h and R_h, A8); those precede it in the canonical order (A7).  The four 8-lane groups
-      // (lanes 8g..8g+7) solve four ready sub-chains at a time.  Within a group, lane l handles the
-      // Lemma-3 chains k = l, l+8, ... (< rank) and the hp/hpp sub-chains h = l, l+8, ...; the two
-      // interference sums are reduced over the group with three xor-shuffles each.
-      const uint32_t gi = lane >> 3, gl = lane & 7;
-      const bool is_sub = lane < nsub;
-      const uint32_t spin_mask = __ballot_sync(FULL, is_sub && ((r.sMisc[lane] >> 16) & 1u));
-      const bool two_units = r.n_unit <= 2;  // set-uniform
-      // Period magic constants of the interferers a group lane serves: chain k = gl + 8j (Lemma 3) and
-      // the chain of sub-chain k (hp/hpp).  They depend on k only, so they are loaded once per set.
-      uint32_t KM[4], KL[4], XM[4], XL[4];
-#pragma unroll
-      for (uint32_t j = 0; j < 4; j++) {
-        const uint32_t k = gl + 8 * j;
-        KM[j] = 1; KL[j] = 0; XM[j] = 1; XL[j] = 0;
-        if (k < nch) { KM[j] = r.cM[k]; KL[j] = r.cMisc[k] & 31u; }
-        if (k < nsub) {
-          const uint32_t hm = r.sMisc[k] & 0xffu;
-          XM[j] = r.cM[hm];
-          XL[j] = r.cMisc[hm] & 31u;
+      // ---- step 4: Eq.5 for all sub-chains at once (Jacobi from below) -------------------------------
+      // Start: R = 1 <= lfp (E_c + H*_c >= 1), with H*_h at R = 1 for the dependants.
+      uint32_t R = act ? 1u : SAT, Hst = act ? sadd(min(S, A2), eps) : SAT, C = A2;
+      if (act) w.Hs[lane] = Hst;
+      __syncwarp();
+      bool dirty = act;  // must be evaluated this iterate (own R or a dependency's H* changed)
+      bool miss = false;
+      for (;;) {
+        uint32_t F = R, nH = Hst;
+        if (dirty) {
+          if (wide) eval_eq5<true>(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
+          else eval_eq5<false>(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
+        }
+        const bool chg = dirty && (F != R || nH != Hst);
+        const uint32_t cm = __ballot_sync(FULL, chg);
+        if (!cm) {
+          // fixed point with the current S values; a lazy S_lb is exact enough unless C_c(R) > S_lb
+          const bool need = act && !sexact && R != SAT && C > S;
+          const uint32_t needm = __ballot_sync(FULL, need);
+          if (!needm) break;
+          for (uint32_t i = lane; i < nas; i += 32)  // lane per segment of the sub-chains that need it
+            if ((needm >> ((r.aMisc[i] >> 16) & 0xffu)) & 1u) w.H[i] = lemma2(r, i);
+          __syncwarp();
+          if (need) {
+            const uint32_t sg = r.sSeg[lane], a0 = sg & 0xffu, na = (sg >> 8) & 0xffu;
+            uint32_t Sx = 0;
+            for (uint32_t i = a0; i < a0 + na; i++) Sx = sadd(Sx, w.H[i]);
+            S = Sx;
+            sexact = true;
+          }
+          dirty = need;  // S only grew: F continues from the current R (still <= the new lfp)
+          continue;
+        }
+        __syncwarp();  // every lane has read the H* of the previous iterate
+        if (chg) {
+          R = F;
+          Hst = nH;
+          w.Hs[lane] = nH;
+        }
+        __syncwarp();
+        dirty = act && R != SAT && (chg || (depm & cm) != 0u);
+        if (flags & PAAM_FLAG_VERDICT_ONLY) {  // R_c > D_c of a CRITICAL chain => R* > D
+          if (__any_sync(FULL, critical && R == SAT)) { miss = true; break; }
         }
       }
-      // solve(act, c): the group's sub-chain c (if act); returns the verdict-only early-exit vote
-      auto solve = [&](const bool act, const uint32_t c) -> bool {
-          const uint32_t cmisc = act ? r.sMisc[c] : 0u;
-          const uint32_t rk = cmisc & 0xffu, umask = (cmisc >> 8) & 0xffu;
-          const uint32_t hpm = act ? r.sHp[c] : 0u, hppm = act ? r.sHpp[c] : 0u;
-          const uint32_t cpu_m = hpm | hppm, dep = hpm | (hppm & spin_mask);
-          const uint32_t hibit = cpu_m ? 32u - __clz(cpu_m) : 0u;
-          const uint32_t jmax = (__reduce_max_sync(FULL, max(rk, hibit)) + 7u) >> 3;
-          // per-lane interferers: Lemma-3 chains and hp/hpp sub-chains (A8 poison on dependencies)
-          uint32_t WU[4], X[4];
-          bool pois = false;
-#pragma unroll
-          for (uint32_t j = 0; j < 4; j++) {
-            WU[j] = 0; X[j] = 0;
-            if (j < jmax) {
-              const uint32_t k = gl + 8 * j;
-              if (k < rk) {
-                uint32_t wu = 0;
-                if (two_units) {  // units 0 and 1 only: one 8-byte row load, two selects
-                  const uint2 w01 = *reinterpret_cast<const uint2*>(&r.W[k][0]);
-                  wu = sadd((umask & 1u) ? w01.x : 0u, (umask & 2u) ? w01.y : 0u);
-                } else
-                for (uint32_t um = umask; um; um &= um - 1)
-                  wu = sadd(wu, r.W[k][__ffs(um) - 1]);  // union of hps over the sub-chain's units (A1)
-                WU[j] = wu;
-              }
-              if ((cpu_m >> k) & 1u) {
-                X[j] = sadd(r.sE[k], (((hpm | spin_mask) >> k) & 1u) ? w.Hs[k] : r.sEps[k]);  // spin() P:1132
-                if ((dep >> k) & 1u) pois |= (w.R[k] == SAT);
-              }
-            }
-          }
-          // Start value (A3): R >= 1 on every iterate, so every mu >= 2 and
-          // F(R) >= B + E + min(S, base3 + 2 sum WU) + eps + 2 sum X for all R >= 1; that value is
-          // therefore <= the least fixed point and one iteration closer to it than the paper's start.
-          uint32_t wu_sum = 0, x_sum = 0;
-#pragma unroll
-          for (uint32_t j = 0; j < 4; j++) { wu_sum = sadd(wu_sum, WU[j]); x_sum = sadd(x_sum, X[j]); }
-          pois = gor8(pois);
-          gsum8x2(wu_sum, x_sum);
-          const uint32_t BE = act ? sadd(w.Bc[c], r.sE[c]) : 0u;
-          uint32_t S = act ? w.S[c] : 0u;
-          const uint32_t base3 = act ? r.sBase3[c] : 0u, eps = act ? r.sEps[c] : 0u;
-          const uint32_t cut = act ? r.cCut[rk] : 0u;
-          uint32_t R = sadd(sadd(BE, sadd(min(S, sadd(base3, sadd(wu_sum, wu_sum))), eps)), sadd(x_sum, x_sum)), Hst = 0;
-          uint32_t C = 0;  // Lemma-3 term C_c(R) of the last iterate
-          bool done = !act || pois;
-          if (pois) R = SAT;
-          auto iterate = [&]() {
-          while (__any_sync(FULL, !done)) {
-            if (!done && R > cut) { R = SAT; done = true; }
-            const uint32_t h2 = (R - 1u) << 1;
-            uint64_t aa = 0, bb = 0;
-            uint32_t hi = 0;
-#pragma unroll
-            for (uint32_t j = 0; j < 4; j++) {
-              if (j < jmax) {
-                const uint64_t pa = (uint64_t)((__umulhi(h2, KM[j]) >> KL[j]) + 2u) * WU[j];
-                const uint64_t pb = (uint64_t)((__umulhi(h2, XM[j]) >> XL[j]) + 2u) * X[j];
-                aa += pa;
-                bb += pb;
-                hi |= (uint32_t)(pa >> 32) | (uint32_t)(pb >> 32);
-              }
-            }
-            uint32_t a = (hi || aa > SAT) ? SAT : (uint32_t)aa;
-            uint32_t bs = (hi || bb > SAT) ? SAT : (uint32_t)bb;
-            gsum8x2(a, bs);
-            if (!done) {
-              C = sadd(base3, a);
-              Hst = sadd(min(S, C), eps);
-              const uint32_t F = sadd(sadd(BE, Hst), bs);
-              if (F == R) done = true;
-              else R = F;
-            }
-          }
-          };
-          iterate();
-          // With S_lb <= S_c, F_lb <= F pointwise, so lfp(F_lb) <= lfp(F): a deadline miss under S_lb is a
-          // miss, and a converged R with C_c(R) <= S_lb is also a fixed point of F (both mins pick C_c),
-          // hence lfp(F).  Otherwise the group computes the exact S_c (lane per segment) and iterates F on
-          // from R, a valid start below lfp(F).  need is uniform within a group.
-          if (lazy_s) {
-            const bool need = act && !pois && R != SAT && C > S;
-            if (__any_sync(FULL, need)) {
-              uint32_t Sx = 0, unused = 0;
-              if (need) {
-                const uint32_t sg = r.sSeg[c], a0 = sg & 0xffu, na = (sg >> 8) & 0xffu;
-                for (uint32_t i = a0 + gl; i < a0 + na; i += 8) Sx = sadd(Sx, lemma2(r, i));
-              }
-              gsum8x2(Sx, unused);
-              if (need) { S = Sx; done = false; }
-              else done = true;
-              iterate();
-            }
-          }
-          if (act && gl == 0) {
-            w.R[c] = R;
-            w.Hs[c] = (R == SAT) ? SAT : Hst;
-          }
-          __syncwarp();
-          if (flags & PAAM_FLAG_VERDICT_ONLY)  // R_c > D_c of a CRITICAL chain => R* > D
-            return __any_sync(FULL, act && gl == 0 && R == SAT && ((r.cMisc[rk] >> 8) & 0xffu) == 0);
-          return false;
-      };
-      bool miss = false;  // verdict-only: a CRITICAL sub-chain already exceeded its deadline
-      // Waves: a sub-chain is ready once every sub-chain it depends on (hp, spinning hpp) is solved;
-      // each wave solves the first four ready sub-chains in canonical order, one per group.  The first
-      // unsolved sub-chain is always ready (its dependencies precede it, A7).
-      {
-        const uint32_t my_dep = is_sub ? (r.sHp[lane] | (r.sHpp[lane] & spin_mask)) : 0u;
-        uint32_t todo = nsub >= 32 ? FULL : (1u << nsub) - 1u;
-        while (todo && !miss) {
-          const bool rdy = ((todo >> lane) & 1u) && (my_dep & todo) == 0u;
-          const uint32_t ready = __ballot_sync(FULL, rdy);
-          const uint32_t rnk = __popc(ready & ((1u << lane) - 1u));
-          if (rdy && rnk < 4) w.gpos[rnk] = (uint8_t)lane;
-          todo &= ~__ballot_sync(FULL, rdy && rnk < 4);
-          __syncwarp();
-          const bool act = gi < (uint32_t)__popc(ready);
-          const uint32_t c = act ? w.gpos[gi] : 0u;
-          __syncwarp();
-          miss = solve(act, c);
-        }
-      }
+      if (act) w.R[lane] = R;
       __syncwarp();
 
       // ---- step 5: end to end and verdict ---------------------------------------------------------
       if (miss) goto verdict_done;  // verdict-only early exit: sched stays 0 (out_wcrt is NULL here)
       if (lane < nch) { w.sum[lane] = 0; w.uns[lane] = 0; }
       __syncwarp();
-      if (is_sub) {
-        const uint32_t rk = r.sMisc[lane] & 0xffu, Rh = w.R[lane];
+      if (act) {
+        const uint32_t Rh = w.R[lane];
         if (Rh == SAT) w.uns[rk] = 1;
         else atomicAdd(&w.sum[rk], (unsigned long long)Rh);
       }

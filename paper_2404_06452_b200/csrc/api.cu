@@ -23,6 +23,8 @@ struct paam_sets {
   cudaEvent_t ev[17], evc[8];  // evc: chunk copies done
   unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18
   int device;             // the CUDA device the handle lives on (made current by every call)
+  bool rec_valid;         // rec holds the records of `dev` (false after the fused paam_pack_analyze, which writes
+                          // none: the next paam_analyze / paam_admit / paam_simulate packs them first)
 };
 
 namespace paam {
@@ -111,6 +113,15 @@ int ensure_streams(paam_sets* sets) {
   return PAAM_OK;
 }
 
+// Materialise the records of the handle's batch if the last call was the fused paam_pack_analyze.
+int ensure_records(const paam_sets* cs, cudaStream_t st) {
+  paam_sets* sets = const_cast<paam_sets*>(cs);
+  if (sets->rec_valid) return PAAM_OK;
+  if (int rc = launch_pack(&sets->dev, sets->rec, nullptr, st)) return rc;
+  sets->rec_valid = true;
+  return PAAM_OK;
+}
+
 int check_batch(const paam_batch* b) {
   if (!b) return fail(PAAM_EINVAL, "NULL batch");
   if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
@@ -178,6 +189,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
   sets->n_bins = batch->set_bin ? batch->n_bins : 0;
   sets->comm = batch->comm_cost;
   sets->flags = batch->flags;
+  sets->rec_valid = true;
   return PAAM_OK;
 }
 
@@ -220,6 +232,7 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
   if ((sets->flags & PAAM_FLAG_VERDICT_ONLY) && out_wcrt)
     return fail(PAAM_EINVAL, "paam_analyze: PAAM_FLAG_VERDICT_ONLY writes no WCRTs (out_wcrt must be NULL)");
   if (int rc = use_device(sets)) return rc;
+  if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
   return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
                         sets->n_bins ? out_bins : nullptr, sets->tickets + 16, (cudaStream_t)stream);
 }
@@ -229,6 +242,7 @@ extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decisi
   if (!sets || !out_decision) return fail(PAAM_EINVAL, "paam_admit: NULL argument");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_admit: n exceeds the packed sets");
   if (int rc = use_device(sets)) return rc;
+  if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
   return launch_analyze(sets->rec, n, sets->comm, sets->flags & ~PAAM_FLAG_VERDICT_ONLY, 0, out_wcrt, nullptr, nullptr,
                         const_cast<paam_sets*>(sets)->tickets + 17, (cudaStream_t)stream, out_decision);
 }
@@ -243,6 +257,7 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
   if (o.witness && !o.violations) return fail(PAAM_EINVAL, "paam_simulate: witness needs violations");
   if (!o.witness) o.max_witness = 0;
   if (int rc = use_device(sets)) return rc;
+  if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
   return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, &o,
                          const_cast<paam_sets*>(sets)->tickets + 18, (cudaStream_t)stream);
 }
@@ -257,42 +272,35 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
     return fail(PAAM_EINVAL, "paam_pack_analyze: PAAM_FLAG_VERDICT_ONLY writes no WCRTs (out_wcrt must be NULL)");
   if ((rc = use_device(sets))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (batch->n_sets < 4096) {  // small batch: sequential
-    rc = paam_repack(batch, sets, out_status, stream);
-    if (rc) return rc;
-    return paam_analyze(sets, batch->n_sets, out_wcrt, out_sched, out_bins, stream);
-  }
   cudaError_t e;
-  if ((rc = ensure_streams(sets))) return rc;
   const bool host = batch->mem == PAAM_MEM_HOST;
-  // Device batch: chunks of pack (side[0]) overlap analyze of the previous chunk (side[1]).  Host
-  // batch: in addition, each chunk's slice of every array is copied H2D on side[2] while the previous
-  // chunk is packed and analysed (copy engines alongside the SMs).
-  static const int KD = [] {  // chunks, device batch (PAAM_PIPELINE_CHUNKS overrides, for tuning)
-    const char* e = std::getenv("PAAM_PIPELINE_CHUNKS");
-    const int k = e ? std::atoi(e) : 2;  // measured best on B200 at 2M sets: 2 (K = 1, 4, 8 slower)
-    return k < 1 ? 1 : (k > 8 ? 8 : k);
-  }();
-  static const int KH = [] {  // chunks, host batch (PAAM_H2D_CHUNKS overrides, for tuning)
-    const char* e = std::getenv("PAAM_H2D_CHUNKS");
-    const int k = e ? std::atoi(e) : 4;
-    return k < 1 ? 1 : (k > 8 ? 8 : k);
-  }();
-  const int K = host ? KH : KD;
   const uint32_t n = batch->n_sets;
-  paam_batch d = *batch;  // the batch the kernels read (host: pointers into the staging buffer)
-  Field f[32];
-  const int nf = batch_fields(&d, f);
-  size_t foff[32];
+  const int64_t* bins = batch->set_bin ? out_bins : nullptr;
+  paam_batch d = *batch;  // the batch the kernel reads (host: pointers into the staging buffer)
   int32_t* status_dev = out_status;
-  if (host) {
-    // The chunk copies below read the host CSR offsets at chunk boundaries: they must be monotone and
-    // within the declared totals (include/paam.h), else a copy range would be wrong or out of bounds.
+  if (!host) {
+    // steps 2-6 in one kernel (fused.cu): the derived records stay on chip
+    if ((rc = launch_fused(&d, status_dev, out_wcrt, out_sched, const_cast<int64_t*>(bins), st))) return rc;
+  } else {
+    // Host batch: K chunks; chunk i's slice of every array is copied H2D on side[2] while the kernel of
+    // chunk i-1 runs on side[0] (copy engines alongside the SMs).
+    static const int KH = [] {  // chunks (PAAM_H2D_CHUNKS overrides, for tuning)
+      const char* ev = std::getenv("PAAM_H2D_CHUNKS");
+      const int k = ev ? std::atoi(ev) : 4;
+      return k < 1 ? 1 : (k > 8 ? 8 : k);
+    }();
+    const int K = n < 4096 ? 1 : KH;
+    if ((rc = ensure_streams(sets))) return rc;
+    Field f[32];
+    const int nf = batch_fields(&d, f);
+    size_t foff[32];
+    // The chunk copies read the host CSR offsets at chunk boundaries: they must be monotone and within
+    // the declared totals (include/paam.h), else a copy range would be wrong or out of bounds.
     const paam_batch& hb = *batch;
     uint32_t pc = 0, pb = 0, ps = 0, px = 0, pa = 0;
     for (int i = 0; i <= K; i++) {
-      const uint32_t s = (uint32_t)((uint64_t)n * i / K);
-      const uint32_t c = hb.set_chain_off[s], x = hb.set_exec_off[s], a = hb.set_accel_off[s];
+      const uint32_t sidx = (uint32_t)((uint64_t)n * i / K);
+      const uint32_t c = hb.set_chain_off[sidx], x = hb.set_exec_off[sidx], a = hb.set_accel_off[sidx];
       if (c < pc || x < px || a < pa || c > hb.n_chains || x > hb.n_execs || a > hb.n_accels)
         return fail(PAAM_EINVAL, "paam_pack_analyze: host set offsets not monotone or beyond the batch totals");
       const uint32_t bcb = hb.chain_cb_off[c];
@@ -311,13 +319,11 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
       if ((rc = ensure_dstatus(sets, n))) return rc;
       status_dev = sets->dstatus;
     }
-  }
-  cudaEventRecord(sets->ev[16], st);
-  for (int i = 0; i < 3; i++) cudaStreamWaitEvent(sets->side[i], sets->ev[16], 0);
-  for (int i = 0; i < K; i++) {
-    const uint32_t lo = (uint32_t)((uint64_t)n * i / K), hi = (uint32_t)((uint64_t)n * (i + 1) / K);
-    if (host) {  // element ranges of this chunk in every array (host CSR offsets), in batch_fields order
-      const paam_batch& hb = *batch;
+    cudaEventRecord(sets->ev[16], st);
+    for (int i = 0; i < 3; i++) cudaStreamWaitEvent(sets->side[i], sets->ev[16], 0);
+    for (int i = 0; i < K; i++) {
+      const uint32_t lo = (uint32_t)((uint64_t)n * i / K), hi = (uint32_t)((uint64_t)n * (i + 1) / K);
+      // element ranges of this chunk in every array (host CSR offsets), in batch_fields order
       const size_t cl = hb.set_chain_off[lo], ch = hb.set_chain_off[hi];
       const size_t xl = hb.set_exec_off[lo], xh = hb.set_exec_off[hi];
       const size_t al = hb.set_accel_off[lo], ah = hb.set_accel_off[hi];
@@ -342,32 +348,25 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
       }
       cudaEventRecord(sets->evc[i], sets->side[2]);
       cudaStreamWaitEvent(sets->side[0], sets->evc[i], 0);
+      paam_batch view = d;  // CSR offsets stay global: a chunk is a shifted window of set offsets
+      view.n_sets = hi - lo;
+      view.set_chain_off += lo;
+      view.set_exec_off += lo;
+      view.set_accel_off += lo;
+      if (view.set_bin) view.set_bin += lo;
+      if ((rc = launch_fused(&view, status_dev ? status_dev + lo : nullptr, out_wcrt, out_sched ? out_sched + lo : nullptr,
+                             const_cast<int64_t*>(bins), sets->side[0])))
+        return rc;
     }
-    paam_batch view = d;  // CSR offsets stay global: a chunk is a shifted window of set offsets
-    view.n_sets = hi - lo;
-    view.set_chain_off += lo;
-    view.set_exec_off += lo;
-    view.set_accel_off += lo;
-    if (view.set_bin) view.set_bin += lo;
-    rc = launch_pack(&view, sets->rec + lo, status_dev ? status_dev + lo : nullptr, sets->side[0]);
-    if (rc) return rc;
-    cudaEventRecord(sets->ev[i], sets->side[0]);
-    cudaStreamWaitEvent(sets->side[1], sets->ev[i], 0);
-    rc = launch_analyze(sets->rec + lo, hi - lo, batch->comm_cost, batch->flags, batch->set_bin ? batch->n_bins : 0,
-                        out_wcrt, out_sched ? out_sched + lo : nullptr, batch->set_bin ? out_bins : nullptr,
-                        sets->tickets + i, sets->side[1]);
-    if (rc) return rc;
-  }
-  cudaEventRecord(sets->ev[8], sets->side[1]);
-  cudaEventRecord(sets->ev[9], sets->side[0]);
-  cudaEventRecord(sets->ev[10], sets->side[2]);
-  cudaStreamWaitEvent(st, sets->ev[8], 0);
-  cudaStreamWaitEvent(st, sets->ev[9], 0);
-  cudaStreamWaitEvent(st, sets->ev[10], 0);
-  if (host && out_status) {  // host status, as paam_repack: copied back, the call synchronises
-    if ((e = cudaMemcpyAsync(out_status, status_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-      return fail_cuda(e, "paam_pack_analyze: status D2H");
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_pack_analyze: synchronize");
+    cudaEventRecord(sets->ev[9], sets->side[0]);
+    cudaEventRecord(sets->ev[10], sets->side[2]);
+    cudaStreamWaitEvent(st, sets->ev[9], 0);
+    cudaStreamWaitEvent(st, sets->ev[10], 0);
+    if (out_status) {  // host status, as paam_repack: copied back, the call synchronises
+      if ((e = cudaMemcpyAsync(out_status, status_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return fail_cuda(e, "paam_pack_analyze: status D2H");
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(e, "paam_pack_analyze: synchronize");
+    }
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "paam_pack_analyze");
   sets->dev = d;
@@ -376,6 +375,7 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   sets->n_bins = batch->set_bin ? batch->n_bins : 0;
   sets->comm = batch->comm_cost;
   sets->flags = batch->flags;
+  sets->rec_valid = false;  // the fused kernel wrote no records
   return PAAM_OK;
 }
 

@@ -94,6 +94,7 @@ constexpr int MAXA = 64;   // accelerator segments
 constexpr int MAXU = 8;    // accelerator units (all accelerators of the set)
 constexpr int MAXX = 32;   // executors
 constexpr int MAXCB = 64;  // callbacks
+constexpr uint32_t REC_WIDE_OK = 1u;  // Record::hflags
 
 struct __align__(16) Record {
   // header
@@ -102,12 +103,17 @@ struct __align__(16) Record {
   uint32_t chain_base;  // global index of the set's first chain (out_wcrt position)
   uint32_t bin;         // utilisation bin (0 when the batch has none)
   uint32_t n_out;       // chains of the set in the batch (== n_chain when valid)
-  uint32_t pad_[3];
+  uint32_t hflags;      // REC_WIDE_OK: every period >= 64 ns (unchecked 64-bit mu sums cannot overflow)
+  uint32_t pad_[2];
   // chains by rank (rank 0 = highest priority)
   uint32_t cCut[MAXC];   // cutoff min(D, T) (A4, A12)
   uint32_t cD[MAXC];     // deadline (verdict)
   uint32_t cM[MAXC];     // mu magic multiplier for T
   uint32_t cMisc[MAXC];  // L (5 bits) | class << 8 | local index << 16 | n_sub << 24
+  // the chains in period order (ascending T, ties by rank): mu(R, T) = 2 + floor((R-1)/T), and the
+  // floor is non-zero only for T < R, so an Eq.5 iterate walks this list up to the first T >= R.
+  // One 16-byte entry: {T, mu magic multiplier M, rank | L << 8, W[rank][0] + W[rank][1] (saturated)}
+  uint4 pTab[MAXC];
   // W[k][u]: sum of A* of chain rank k's segments on unit u (exact regrouping of Eq.3/Eq.4 sums);
   // rank-major so that lanes reading different units of one chain hit different banks
   uint32_t W[MAXC][MAXU];
@@ -115,17 +121,19 @@ struct __align__(16) Record {
   uint32_t sE[MAXS];      // calligraphic E_c
   uint32_t sB[MAXS];      // B_c as written
   uint32_t sEps[MAXS];    // sum of eps over the sub-chain's segments (delta_c * eps, A11)
-  uint32_t sBase3[MAXS];  // sum over segments of (A* + LPB): first term of Eq.4
   uint32_t sHp[MAXS];     // bit h: h in hp(c)
   uint32_t sHpp[MAXS];    // bit h: h in hpp(c)
-  uint32_t sLp[MAXS];     // bit h: h in lp(c)
+  uint32_t sLp[MAXS];     // bit h: h in lp(c) (PAAM_FLAG_BLOCKING_SOUND only)
   uint32_t sMisc[MAXS];   // rank | unitmask << 8 | spin << 16 | chain-position << 24
   uint32_t sSeg[MAXS];    // first accelerator segment | count << 8 | exec << 16 | core << 24
+  uint32_t sA2[MAXS];     // Eq.4 with every mu = 2: base3 + 2 sum_{k<rank} sum_{u in units} W[k][u]
+  uint32_t sSlb[MAXS];    // sum of the Lemma-2 start values aBase2 of the sub-chain's segments (<= S_c)
   // accelerator segments in chain-rank order (a sub-chain's segments are contiguous)
   uint32_t aBase2[MAXA];  // A* + LPB + 2 sum_{k<r} W[k][u]: Eq.3 with mu = floor((h-1)/T) + 2 split off
-  uint32_t aEps[MAXA];    // eps of the segment's accelerator
-  uint32_t aCbE[MAXA];    // E_j of the segment's callback (PAAM_FLAG_BLOCKING_SOUND)
   uint32_t aMisc[MAXA];   // rank | unit << 8 | sub << 16 | callback << 24
+  // written and read only under PAAM_FLAG_BLOCKING_SOUND (the sound B_c of reading A10)
+  uint32_t aEps[MAXA];    // eps of the segment's accelerator
+  uint32_t aCbE[MAXA];    // E_j of the segment's callback
 };
 static_assert(sizeof(Record) % 16 == 0, "record must be 16-byte aligned");
 static_assert(offsetof(Record, W) % 16 == 0, "W rows are copied as 16-byte vectors");
@@ -142,6 +150,9 @@ int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
                    cudaStream_t st, int32_t* out_fail = nullptr);
+// §8(a) steps 2-6 in one kernel (fused.cu): no record is written
+int launch_fused(const paam_batch* b, int32_t* status, uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins,
+                 cudaStream_t st);
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
                     uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st);
 #endif

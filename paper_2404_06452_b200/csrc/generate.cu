@@ -549,10 +549,7 @@ extern "C" int paam_sweep_create(uint32_t chunk, paam_sweeper** out) {
   if (!h) return fail(PAAM_ENOMEM, "paam_sweep_create: host allocation");
   h->chunk = chunk;
   cudaError_t e = cudaGetDevice(&h->device);
-  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
-    h->raw[i].device = h->device;
-    e = cudaMalloc((void**)&h->rec[i], sizeof(paam::Record) * (size_t)chunk);
-  }
+  for (int i = 0; i < 2; i++) h->raw[i].device = h->device;
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->tickets, sizeof(unsigned int) * 2);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sg, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sa, cudaStreamNonBlocking);
@@ -594,9 +591,8 @@ extern "C" int paam_sweep(paam_sweeper* h, const paam_gen_params* params, uint64
     if (int rc = generate_into(&h->raw[bi], p, seed, first_index + lo, cnt, comm_cost, flags, h->sg, h->chunk)) return rc;
     cudaEventRecord(h->gen_done[bi], h->sg);
     cudaStreamWaitEvent(h->sa, h->gen_done[bi], 0);
-    if (int rc = launch_pack(&h->raw[bi].b, h->rec[bi], nullptr, h->sa)) return rc;
-    if (int rc = launch_analyze(h->rec[bi], cnt, comm_cost, flags, p.n_bins, nullptr, out_sched ? out_sched + lo : nullptr,
-                                p.n_bins ? out_bins : nullptr, h->tickets + bi, h->sa))
+    if (int rc = launch_fused(&h->raw[bi].b, nullptr, nullptr, out_sched ? out_sched + lo : nullptr,
+                              p.n_bins ? out_bins : nullptr, h->sa))  // steps 2-6, records on chip
       return rc;
     cudaEventRecord(h->ana_done[bi], h->sa);
   }

@@ -70,7 +70,7 @@ struct Scratch {
       };
     };
     struct {  // the set's segments, staged by coalesced loads; dead before WFD / W are written
-      uint64_t gW[MAXSEG];
+      uint32_t gW[MAXSEG];  // WCET, saturated at SAT (a WCET >= LIM fails validation)
       uint8_t gKind[MAXSEG], gAcc[MAXSEG], gUnit[MAXSEG];
     };
   };
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   Scratch& s = smem[threadIdx.x >> 5];
+  const bool sound = (b.flags & PAAM_FLAG_BLOCKING_SOUND) != 0;  // record fields of the sound B_c (A10)
   // Blocked assignment: warp w owns the contiguous sets [lo, hi).  Consecutive sets are adjacent in
   // every CSR array, so the next set's start offsets are this set's end offsets: after the first set
   // no dependent offset loads remain, and the next set's lines are often already in L2.
@@ -222,19 +223,30 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       cstart = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(cstart_bit >> 32)) << 32) |
                               __reduce_or_sync(FULL, (uint32_t)cstart_bit);
       __syncwarp();
-      // ---- segments: staged with coalesced loads (one round trip for the whole set) ------------------
+      // ---- segments: staged with coalesced loads (one round trip for the whole set), lane per segment,
+      // with the per-segment validation (time range, kind, WCET > 0, declared accelerator and unit);
+      // the set's callbacks cover [sg0, sg1) exactly unless a callback range is malformed (EDANGLING)
 #ifndef PAAM_WARP_EMU
 #pragma unroll kStageUnroll
 #endif
       for (uint32_t i = lane; i < nseg; i += 32) {
-        s.gW[i] = b.seg_wcet[sg0 + i];
-        s.gKind[i] = b.seg_kind[sg0 + i];
-        s.gAcc[i] = b.seg_accel[sg0 + i];
-        s.gUnit[i] = b.seg_unit[sg0 + i];
+        const uint64_t w = b.seg_wcet[sg0 + i];
+        const uint32_t kind = b.seg_kind[sg0 + i], a = b.seg_accel[sg0 + i], u = b.seg_unit[sg0 + i];
+        erange |= (w >= LIM);
+        eshape |= (kind > 1) || (w == 0);
+        if (kind == 1) {
+          if (a >= nac) eaccel = true;
+          else edang |= (u >= s.aUnits[a]);
+        }
+        s.gW[i] = (uint32_t)min(w, (uint64_t)SAT);
+        s.gKind[i] = (uint8_t)kind;
+        s.gAcc[i] = (uint8_t)a;
+        s.gUnit[i] = (uint8_t)u;
       }
       __syncwarp();
       // ---- callbacks: two passes of 32 lanes; each lane walks its segments ----------------------
       uint32_t prev_exec = 0xffffffffu;
+      bool malformed = false;  // a callback's segment range leaves the set's: EDANGLING before segment checks
       for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
         const uint32_t j = pass * 32 + lane;
         uint32_t exec = 0xffffffffu, E = 0, na = 0, fa = 0, fu = 0, fw = 0;  // fa/fu/fw: first ACCEL segment
@@ -242,22 +254,18 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
           exec = b.cb_exec[cb0 + j];
           uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
           edang |= (se == so) || (exec >= nex);
-          if (so < sg0 || se < so || se > sg1) { edang = true; so = se = sg0; }  // malformed CSR: no staged reads
+          if (so < sg0 || se < so || se > sg1) { malformed = true; so = se = sg0; }  // no staged reads
           uint32_t prev_kind = 0xffffffffu;
 #pragma unroll kSegUnroll
           for (uint32_t k = so - sg0; k < se - sg0; k++) {
-            const uint32_t kind = s.gKind[k];
-            const uint64_t w = s.gW[k];
-            erange |= (w >= LIM);
-            eshape |= (kind > 1) || (w == 0) || (kind == prev_kind);
+            const uint32_t kind = s.gKind[k], w = s.gW[k];
+            eshape |= (kind == prev_kind);  // CPU / ACCEL segments alternate
             prev_kind = kind;
-            if (kind == 0) E = sadd(E, (uint32_t)w);  // w < LIM in a valid set: E stays exact
-            if (kind == 1) {
-              const uint32_t a = s.gAcc[k], u = s.gUnit[k];
-              if (na == 0) { fa = a; fu = u; fw = (uint32_t)w; }
+            if (kind == 0) {
+              E = sadd(E, w);
+            } else {
+              if (na == 0) { fa = s.gAcc[k]; fu = s.gUnit[k]; fw = w; }
               na++;
-              if (a >= nac) eaccel = true;
-              else edang |= (u >= s.aUnits[a]);
             }
           }
           s.bExec[j] = (uint8_t)min(exec, 255u);
@@ -312,8 +320,10 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         }
       }
       erange |= (n_aseg > MAXA) || (n_unit > MAXU);
-      // first failing class, in the documented order
-      if (__any_sync(FULL, erange)) st = PAAM_SET_ERANGE;
+      // first failing class, in the documented order (a malformed callback range is a dangling
+      // reference: it is reported before the checks of the segments the callbacks no longer cover)
+      if (__any_sync(FULL, malformed)) st = PAAM_SET_EDANGLING;
+      else if (__any_sync(FULL, erange)) st = PAAM_SET_ERANGE;
       else if (__any_sync(FULL, edang)) st = PAAM_SET_EDANGLING;
       else if (__any_sync(FULL, eaccel)) st = PAAM_SET_EACCEL;
       else if (__any_sync(FULL, eshape)) st = PAAM_SET_ESHAPE;
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         } else {
           const uint32_t so = b.cb_seg_off[cb0 + j] - sg0, se = b.cb_seg_off[cb0 + j + 1] - sg0;
           for (uint32_t k = so; k < se; k++)  // the staged segments are intact until WFD / W
-            if (s.gKind[k] == 1) put(s.gAcc[k], s.gUnit[k], (uint32_t)min(s.gW[k], (uint64_t)SAT));
+            if (s.gKind[k] == 1) put(s.gAcc[k], s.gUnit[k], s.gW[k]);
         }
       }
     }
@@ -500,13 +510,17 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       const uint32_t qa = s.rA0[s_rank] + (s.bA0[s_j0] - s.cA0[c]);
       const uint32_t qn = s.bA0[s_j0 + s_nj] - s.bA0[s_j0];
       const uint32_t E = s_E;
-      uint32_t eps = 0, base3 = 0, umask = 0;
+      uint32_t eps = 0, base3 = 0, umask = 0, slb = 0;
       for (uint32_t q = qa; q < qa + qn; q++) {
         const uint32_t u = s.qUnit[q];
         eps = sadd(eps, s.aEps[s.qAcc[q]]);
-        base3 = sadd(base3, sadd(s.qAstar[q], s.maxA[u][s_rank]));
+        const uint32_t b = sadd(s.qAstar[q], s.maxA[u][s_rank]);
+        base3 = sadd(base3, b);
+        slb = sadd(slb, sadd(b, s.pre2[u][s_rank]));  // aBase2 of the segment (Lemma-2 start value)
         umask |= 1u << u;
       }
+      uint32_t a2 = base3;  // Eq.4 with every mu = 2 (the union of hps over the sub-chain's units, A1)
+      for (uint32_t um = umask; um; um &= um - 1) a2 = sadd(a2, s.pre2[__ffs(um) - 1][s_rank]);
       uint32_t hp = 0, lp = 0, hpp = 0, B = 0;
       uint32_t m = same_exec & ~(1u << lane);
       while (m) {
@@ -527,18 +541,20 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       r->sE[k] = E;
       r->sB[k] = B;
       r->sEps[k] = eps;
-      r->sBase3[k] = base3;
       r->sHp[k] = hp;
       r->sHpp[k] = hpp;
-      r->sLp[k] = lp;
+      if (sound) r->sLp[k] = lp;
       r->sMisc[k] = s_rank | (umask << 8) | ((uint32_t)(s.xWait[s_exec] == 1) << 16) | (pos << 24);
       r->sSeg[k] = qa | (qn << 8) | (s_exec << 16) | ((uint32_t)s.xCore[s_exec] << 24);
+      r->sA2[k] = a2;
+      r->sSlb[k] = slb;
     }
     // ---- chains by rank ---------------------------------------------------------------------------------
+    const uint32_t Tk = is_chain ? s.rT[lane] : 0xffffffffu;
+    uint32_t M = 0, L = 0;
     if (is_chain) {
       const uint32_t k = lane;
-      uint32_t M, L;
-      make_magic(s.rT[k], &M, &L);
+      make_magic(Tk, &M, &L);
       const uint32_t o = s.rCbo[k], nb = s.rNcb[k];
       const uint64_t rng = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) << o;
       const uint32_t nsub = __popcll(runstart & rng);
@@ -548,12 +564,25 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       r->cMisc[k] = L | ((uint32_t)s.rCls[k] << 8) | ((uint32_t)s.rIdx[k] << 16) | (nsub << 24);
       for (uint32_t u = 0; u < n_unit; u++) r->W[k][u] = s.W[k][u];
     }
+    {  // period order (ascending T, ties by rank)
+      uint32_t pos = 0;
+      for (uint32_t j = 0; j < nch; j++) {
+        const uint32_t Tj = __shfl_sync(FULL, Tk, j);
+        pos += (Tj < Tk) || (Tj == Tk && j < (uint32_t)lane);
+      }
+      if (is_chain) r->pTab[pos] = uint4{Tk, M, (uint32_t)lane | (L << 8), sadd(s.W[lane][0], s.W[lane][1])};
+      // every period >= 64 ns: q * W < 2^62 / 64, so 64 such products cannot overflow a u64 sum
+      const bool wide_ok = !__any_sync(FULL, is_chain && Tk < 64u);
+      if (lane == 0) r->hflags = wide_ok ? REC_WIDE_OK : 0u;
+    }
     // ---- accelerator segments (rank order) ------------------------------------------------------------
     for (uint32_t q = lane; q < n_aseg; q += 32) {
       const uint32_t u = s.qUnit[q], rk = s.qRank[q];
       r->aBase2[q] = sadd(sadd(s.qAstar[q], s.maxA[u][rk]), s.pre2[u][rk]);
-      r->aEps[q] = s.aEps[s.qAcc[q]];
-      r->aCbE[q] = s.bE[s.qCb[q]];
+      if (sound) {
+        r->aEps[q] = s.aEps[s.qAcc[q]];
+        r->aCbE[q] = s.bE[s.qCb[q]];
+      }
       r->aMisc[q] = rk | (u << 8) | ((uint32_t)s.sCanon[s.bSub[s.qCb[q]]] << 16) | ((uint32_t)s.qCb[q] << 24);
     }
     if (lane == 0) { r->n_chain = (uint8_t)nch; r->n_sub = (uint8_t)n_sub; r->n_aseg = (uint8_t)n_aseg; r->n_unit = (uint8_t)n_unit; }

@@ -24,7 +24,7 @@ def test_bench_small_run_contract():
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
     assert sum(d["bins"][0::2]) == 20000
     assert 0 < sum(d["bins"][1::2]) < 20000
-    assert d["gpu_launches"] >= 3 * 2
+    assert d["gpu_launches"] >= 3  # one fused_kernel launch per step (device-resident batch)
     assert d["des"]["sim_le_bound_violations"] == 0
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in d["roofline"], k

@@ -20,6 +20,7 @@ L.emu_pack.argtypes = [vp, vp, vp]
 L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
 L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp]
 L.emu_record_bytes.restype = ctypes.c_uint32
+L.emu_fused.argtypes = [vp, vp, vp, vp, vp]
 
 
 def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
@@ -41,6 +42,18 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     L.emu_analyze(rec.ctypes.data, n, hb.c.comm_cost, hb.c.flags | 0x4, hb.c.n_bins if hb.c.set_bin else 0,
                   None, sv.ctypes.data, bv.ctypes.data if hb.c.set_bin else None)
     out.update(sched_v=sv[:n], bins_v=bv[:2 * hb.c.n_bins])
+    # the fused kernel (paam_pack_analyze): full mode and verdict-only
+    fst = np.full(max(n, 1), -9, np.int32)
+    fw = np.zeros(nch, np.uint64)
+    fs = np.zeros(max(n, 1), np.uint8)
+    fb = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
+    L.emu_fused(ctypes.addressof(hb.c), fst.ctypes.data, fw.ctypes.data, fs.ctypes.data, fb.ctypes.data if hb.c.set_bin else None)
+    vb = Batch.from_host(dict(batch, flags=batch.get("flags", 0) | 0x4))
+    fsv = np.zeros(max(n, 1), np.uint8)
+    fbv = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
+    L.emu_fused(ctypes.addressof(vb.c), None, None, fsv.ctypes.data, fbv.ctypes.data if hb.c.set_bin else None)
+    out.update(f_status=fst[:n], f_wcrt=fw[:hb.c.n_chains], f_sched=fs[:n], f_bins=fb[:2 * hb.c.n_bins],
+               f_sched_v=fsv[:n], f_bins_v=fbv[:2 * hb.c.n_bins])
     if horizon is not None:
         from paper_2404_06452_b200.paam import PaamSimOut
         a = {k: np.zeros(nch, np.uint64) for k in ("resp", "count", "misses", "drops")}
@@ -64,6 +77,13 @@ def compare(batch, horizon=None, seed=0, first=0, label="", fifo=False):
     ow, osch, ost, ob = O.analyze(batch)
     ok = np.array_equal(ost, e["status"]) and np.array_equal(ow, e["wcrt"]) and np.array_equal(osch, e["sched"])
     ok = ok and np.array_equal(osch, e["sched_v"]) and np.array_equal(e["bins"], e["bins_v"])
+    okf = (np.array_equal(ost, e["f_status"]) and np.array_equal(ow, e["f_wcrt"]) and np.array_equal(osch, e["f_sched"])
+           and np.array_equal(osch, e["f_sched_v"]) and np.array_equal(e["bins"], e["f_bins"])
+           and np.array_equal(e["bins"], e["f_bins_v"]))
+    if not okf:
+        bad = np.nonzero(ow != e["f_wcrt"])[0][:5]
+        print(f"  FUSED MISMATCH status o={ost[:8]} f={e['f_status'][:8]} wcrt bad {bad} o={ow[bad]} f={e['f_wcrt'][bad]}")
+    ok = ok and okf
     msg = [f"{label}: analyze {'OK' if ok else 'MISMATCH'}"]
     if not ok:
         bad = np.nonzero(ow != e["wcrt"])[0][:5]

@@ -1,0 +1,5 @@
+#include "../../paper_2404_06452_b200/csrc/fused.cu"
+extern "C" void emu_fused(const paam_batch* b, int32_t* status, uint64_t* wcrt, uint8_t* sched, int64_t* bins) {
+  gridDim.x = 1;
+  emu::launch_block(0, paam::FW * 32, [&]() { paam::fused_kernel(*b, status, wcrt, sched, bins); });
+}
