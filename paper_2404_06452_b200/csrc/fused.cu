@@ -21,7 +21,7 @@ namespace paam {
 
 namespace {
 
-constexpr int FW = 4;  // warps per block
+constexpr int FW = 8;  // warps per block
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t MAXSEG = 192;
 constexpr int F_WARP_BINS = 32;
@@ -86,7 +86,7 @@ struct FSmem {
   union {
     struct {  // the set's segments, staged by coalesced loads; dead after the accelerator-segment pass
       uint32_t gW[MAXSEG];
-      uint8_t gKind[MAXSEG], gAcc[MAXSEG], gUnit[MAXSEG];
+      uint8_t gMeta[MAXSEG];  // kind | accelerator << 1 | unit << 3 (the values of a valid set fit)
     };
     struct {  // what a lane reads of other lanes / chains
       uint4 pTab[MAXC];  // period order: {T, M, rank | L << 8, W[rank][0] + W[rank][1]}
@@ -263,13 +263,18 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
 }
 
 #ifndef FUSED_MINB
-#define FUSED_MINB 7  // shared memory allows 7 blocks of 4 warps per SM; the register cap follows (73)
+#define FUSED_MINB 4  // 4 blocks of 8 warps (7 KB of shared memory per warp): 32 warps, 64 registers
 #endif
 __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     fused_kernel(paam_batch b, int32_t* __restrict__ status_out, uint64_t* __restrict__ out_wcrt,
                  uint8_t* __restrict__ out_sched, int64_t* __restrict__ out_bins) {
+#ifdef PAAM_WARP_EMU
   __shared__ FSmem smem[FW];
-  __shared__ unsigned int wbins_all[FW][2 * F_WARP_BINS];
+#else
+  extern __shared__ __align__(16) unsigned char fsmem_raw[];  // FW * sizeof(FSmem), dynamic (> 48 KB)
+  FSmem* smem = reinterpret_cast<FSmem*>(fsmem_raw);
+#endif
+  __shared__ unsigned int bbins[2 * F_WARP_BINS];  // the block's bin counters (shared-memory atomics)
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   FSmem& s = smem[threadIdx.x >> 5];
@@ -277,11 +282,10 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
   const bool sound = (flags & PAAM_FLAG_BLOCKING_SOUND) != 0;
   const bool lazy_s = !sound;
   const uint32_t n_bins = b.set_bin ? b.n_bins : 0u;
-  unsigned int* wbins = wbins_all[threadIdx.x >> 5];
-  const bool warp_bins = out_bins && n_bins && n_bins <= F_WARP_BINS;
-  if (warp_bins) {
-#pragma unroll 1
-    for (uint32_t i = lane; i < 2 * n_bins; i += 32) wbins[i] = 0;
+  const bool blk_bins = out_bins && n_bins && n_bins <= F_WARP_BINS;  // uniform over the grid
+  if (blk_bins) {
+    for (uint32_t i = threadIdx.x; i < 2 * n_bins; i += FW * 32) bbins[i] = 0;
+    __syncthreads();
   }
   const uint64_t comm = b.comm_cost;
   // Blocked assignment (as pack.cu): warp w owns the contiguous sets [lo, hi); each set's start
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       st = PAAM_SET_ERANGE;
     uint32_t n_aseg = 0, n_sub = 0, n_unit = 0;
     uint64_t runstart = 0, cstart = 0;
-    uint32_t T = 0, D = 0, prio = 0, cls = 0, cbo = 0, cbn = 0, rank = 0;
+    uint32_t T = 0, D = 0, prio = 0, cls = 0, cbo = 0, cbn = 0, rank = 0, ppos = 0;  // lane = chain index
     if (st == PAAM_SET_OK) {
       // ---- load + validate (as pack.cu) ---------------------------------------------------------------
       bool erange = false, edang = false, eaccel = false, eshape = false, edup = false, edl = false, ecore = false;
@@ -362,8 +366,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       cstart = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(cstart_bit >> 32)) << 32) |
                __reduce_or_sync(FULL, (uint32_t)cstart_bit);
       __syncwarp();
-      // segments: lane per segment, staged with their per-segment validation
-      #pragma unroll 1
+      // ---- segments: lane per segment, staged with their per-segment validation
+      #pragma unroll 2  // two passes' loads in flight
       for (uint32_t i = lane; i < nseg; i += 32) {
         const uint64_t w = b.seg_wcet[sg0 + i];
         const uint32_t kind = b.seg_kind[sg0 + i], a = b.seg_accel[sg0 + i], u = b.seg_unit[sg0 + i];
@@ -374,12 +378,10 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           else edang |= (u >= s.aUnits[a]);
         }
         s.gW[i] = (uint32_t)min(w, (uint64_t)SAT);
-        s.gKind[i] = (uint8_t)kind;
-        s.gAcc[i] = (uint8_t)a;
-        s.gUnit[i] = (uint8_t)u;
+        s.gMeta[i] = (uint8_t)(min(kind, 1u) | (min(a, 3u) << 1) | (min(u, 7u) << 3));
       }
       __syncwarp();
-      // callbacks: lane per callback, walking its staged segments
+      // ---- callbacks: lane per callback, walking its staged segments
       uint32_t prev_exec = 0xffffffffu;
       bool malformed = false;
       #pragma unroll 1
@@ -394,13 +396,13 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           uint32_t prev_kind = 0xffffffffu;
           #pragma unroll 1
           for (uint32_t k = so - sg0; k < se - sg0; k++) {
-            const uint32_t kind = s.gKind[k], w = s.gW[k];
+            const uint32_t meta = s.gMeta[k], kind = meta & 1u, w = s.gW[k];
             eshape |= (kind == prev_kind);
             prev_kind = kind;
             if (kind == 0) {
               E = sadd(E, w);
             } else {
-              if (na == 0) { fa = s.gAcc[k]; fu = s.gUnit[k]; fw = w; }
+              if (na == 0) { fa = (meta >> 1) & 3u; fu = meta >> 3; fw = w; }
               na++;
             }
           }
@@ -430,11 +432,17 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           for (uint32_t i = first; i + 1 < j; i++) eshape |= (s.bExec[i] == s.bExec[j]);
         }
       }
-      {  // chain ranks, duplicate priorities
-        uint32_t rk = 0;
+      // ---- ranks
+      {  // chain ranks and period positions (ascending T; equal periods by chain index), one pass
+        uint32_t rk = 0, below = 0;
+        const uint32_t Tme = lane < (int)nch ? T : 0xffffffffu;
         #pragma unroll 1
-        for (uint32_t d = 0; d < nch; d++) rk += (__shfl_sync(FULL, prio, d) > prio);
+        for (uint32_t d = 0; d < nch; d++) {
+          rk += (__shfl_sync(FULL, prio, d) > prio);
+          below += (__shfl_sync(FULL, Tme, d) < Tme);
+        }
         rank = rk;
+        ppos = below + __popc(__match_any_sync(FULL, Tme) & lt);
         const uint32_t valid = nch >= 32 ? FULL : (1u << nch) - 1u;
         const uint32_t same = __match_any_sync(FULL, prio) & valid & ~(1u << lane);
         edup |= (lane < (int)nch && same != 0);
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         for (uint32_t i = lane; i < nch; i += 32) out_wcrt[c0 + i] = UNS;
       if (!st3) psg = b.cb_seg_off[pcb];
     } else {
-      // ======================== derivation (valid set) =================================================
+      // ---- derivation (valid set) ======================================================================
       const bool is_chain = lane < (int)nch;
       if (is_chain) {
         s.rank_of[lane] = (uint8_t)rank;
@@ -517,7 +525,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         if ((runstart >> j) & 1ull) s.sJ0[sid] = (uint8_t)j;
       }
       __syncwarp();
-      // accelerator segments: A*, unit, rank, in rank order
+      // ---- accelerator segments: A*, unit, rank, in rank order
       #pragma unroll 1
       for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
         const uint32_t j = pass * 32 + lane;
@@ -540,14 +548,14 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
             const uint32_t so = b.cb_seg_off[cb0 + j] - sg0, se = b.cb_seg_off[cb0 + j + 1] - sg0;
             #pragma unroll 1
             for (uint32_t k = so; k < se; k++)
-              if (s.gKind[k] == 1) put(s.gAcc[k], s.gUnit[k], s.gW[k]);
+              if (s.gMeta[k] & 1u) put((s.gMeta[k] >> 1) & 3u, s.gMeta[k] >> 3, s.gW[k]);
           }
         }
       }
       __syncwarp();  // the staged segments are dead from here on (their space becomes analysis state)
       if ((flags & PAAM_FLAG_WFD_UNITS) && lane == 0) f_wfd_units(s, nac, ncb, cstart);
       __syncwarp();
-      // per chain (lane = rank): W[k][u], max A*[u][k], accelerator use mask
+      // ---- per chain (lane = rank): W[k][u], max A*[u][k], accelerator use mask
       uint32_t use = 0;
       #pragma unroll 1
       for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
@@ -565,7 +573,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       }
       __syncwarp();
       if (!st3) { psg = b.cb_seg_off[pcb]; st3 = true; }
-      // buckets (A5) and LP blocking per (unit, rank)
+      // ---- buckets (A5) and LP blocking per (unit, rank)
       #pragma unroll 1
       for (uint32_t a = 0; a < nac; a++) {
         const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
@@ -602,26 +610,17 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         const uint32_t ex = lane == 0 ? 0u : prev;
         s.pre2[u][lane] = sadd(ex, ex);
       }
-      // chains by rank: mu constants, period order (lane = rank)
-      const uint32_t Tk = is_chain ? s.rT[lane] : 0xffffffffu;
-      uint32_t ppos = 0;
+      // ---- chains: mu constants, period table (lane = chain index; ppos from the rank pass)
       {
         uint32_t M = 0, L = 0;
         if (is_chain) {
-          make_magic(Tk, &M, &L);
-          s.cML[lane] = uint2{M, L};
-        }
-        #pragma unroll 1
-        for (uint32_t j = 0; j < nch; j++) {
-          const uint32_t Tj = __shfl_sync(FULL, Tk, j);
-          ppos += (Tj < Tk) || (Tj == Tk && j < (uint32_t)lane);
-        }
-        if (is_chain) {
-          s.pTab[ppos] = uint4{Tk, M, (uint32_t)lane | (L << 8), sadd(s.W[lane][0], s.W[lane][1])};
-          s.posOf[lane] = (uint8_t)ppos;
+          make_magic(T, &M, &L);
+          s.cML[rank] = uint2{M, L};
+          s.pTab[ppos] = uint4{T, M, rank | (L << 8), sadd(s.W[rank][0], s.W[rank][1])};
+          s.posOf[rank] = (uint8_t)ppos;
         }
       }
-      const bool wide = !__any_sync(FULL, is_chain && Tk < 64u);  // see analyze.cu eval_eq5
+      const bool wide = !__any_sync(FULL, is_chain && T < 64u);  // see analyze.cu eval_eq5
       __syncwarp();
 
       // ---- sub-chains (lane = sub-chain id, callback order): everything stays in registers -----------
@@ -706,8 +705,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       const uint32_t xm = hpm | hppm;
       const bool critical = act && s.rCls[rk] == 0;
       bool sexact = !lazy_s;
-      // lmask: period positions of the chains of rank < rk (exclusive OR-scan over ranks)
-      uint32_t pb = is_chain ? (1u << ppos) : 0u;
+      // ---- lmask: period positions of the chains of rank < rk (exclusive OR-scan over ranks)
+      uint32_t pb = is_chain ? (1u << s.posOf[lane]) : 0u;  // lane = rank
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(FULL, pb, o);
@@ -803,9 +802,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
       if (out_bins && bin_ok) {
-        if (warp_bins) {
-          wbins[2 * bin]++;
-          if (sched) wbins[2 * bin + 1]++;
+        if (blk_bins) {
+          atomicAdd(&bbins[2 * bin], 1u);
+          if (sched) atomicAdd(&bbins[2 * bin + 1], 1u);
         } else {
           atomicAdd((unsigned long long*)&out_bins[2 * bin], 1ull);
           if (sched) atomicAdd((unsigned long long*)&out_bins[2 * bin + 1], 1ull);
@@ -816,11 +815,10 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
     nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
   }
-  if (warp_bins) {
-    __syncwarp();
-    #pragma unroll 1
-    for (uint32_t i = lane; i < 2 * n_bins; i += 32)
-      if (wbins[i]) atomicAdd((unsigned long long*)&out_bins[i], (unsigned long long)wbins[i]);
+  if (blk_bins) {  // every warp of the block is done: one global atomic per non-zero counter
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 2 * n_bins; i += FW * 32)
+      if (bbins[i]) atomicAdd((unsigned long long*)&out_bins[i], (unsigned long long)bbins[i]);
   }
 }
 
@@ -833,12 +831,15 @@ int launch_fused(const paam_batch* b, int32_t* status, uint64_t* out_wcrt, uint8
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel, FW * 32, 0);
+  constexpr size_t SMEM = FW * sizeof(FSmem);
+  static const cudaError_t attr = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  if (attr != cudaSuccess) return fail_cuda(attr, "fused_kernel: shared memory attribute");
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel, FW * 32, SMEM);
   if (per_sm < 1) per_sm = 1;
   const uint32_t need = (b->n_sets + FW - 1) / FW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  fused_kernel<<<grid, FW * 32, 0, st>>>(*b, status, out_wcrt, out_sched, out_bins);
+  fused_kernel<<<grid, FW * 32, SMEM, st>>>(*b, status, out_wcrt, out_sched, out_bins);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "fused_kernel launch");
