@@ -2,17 +2,18 @@
 """bench.py -- chain sets analysed per second (PAAM WCRT fixed points) on N B200s.
 
 One step = the whole hot path over this rank's batch of synthetic chain sets that is already
-resident in HBM: paam_pack_analyze (validate + derive, §8(a) step 2, pipelined in two chunks with the
-Lemma 2 / Eq.5 fixed points, end-to-end WCRT, verdict and bin counts of steps 3-6) -> (N > 1) one NCCL
-all-reduce of the bin counts.  Weak scaling: every rank owns SETS_PER_GPU consecutive set indices of
+resident in HBM: paam_pack_analyze = one fused_kernel launch (validate + derive, §8(a) step 2, then
+the Lemma 2 / Eq.5 fixed points, end-to-end WCRT, verdict and bin counts of steps 3-6, the derived
+records kept on chip) -> (N > 1) one NCCL all-reduce of the bin counts.  Weak scaling: every rank owns SETS_PER_GPU consecutive set indices of
 the config-4 stream (seed 4), so N = 8 is exactly config 4 (16M sets) and N = 1 is the config-3
 recipe on 2M sets.
 
-Extra legs in the same JSON line: per-kernel times from a sequential pass (roofline of the dominant
-kernel and of the other one), verdict_only (PAAM_FLAG_VERDICT_ONLY), e2e (the same metric from
-pinned host buffers through paam_pack_analyze, H2D / D2H inside the timed region),
-e2e_device_generate (paam_sweep: device generation included), des (config-5 leg: paam_simulate on
-100k sets, 10 s horizon, sim <= bound census, with and without digests), cpu_baseline (the oracle).
+Extra legs in the same JSON line: the kernel's per-launch time (roofline: HBM, issue and ALU views),
+the split entry points (paam_repack + paam_analyze) for reference, verdict_only (PAAM_FLAG_VERDICT_ONLY),
+e2e (the same metric from pinned host buffers through paam_pack_analyze with every WCRT copied back,
+H2D / D2H inside the timed region) and e2e_verdict_only, e2e_device_generate (paam_sweep: device
+generation included), des (config-5 leg: paam_simulate on 1M sets, 10 s horizon, sim <= bound
+census, misses / drops / stopped runs, with and without digests), cpu_baseline (the oracle).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -101,8 +102,15 @@ def dist_setup(n_gpus):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU over NCCL; PAAM_DIST_BACKEND=gloo runs the same N > 1 path over gloo (CUDA
+        # tensors, host staging), e.g. several ranks on one GPU in the multi-process test
+        backend = os.environ.get("PAAM_DIST_BACKEND", "nccl")
+        dev = local % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -256,7 +264,17 @@ def run_ours(args):
     ms = max_over_ranks(ms_local, world)
     value = world * n * args.steps / (ms / 1e3)
 
-    # ---- per-kernel durations: the same kernels launched one after the other on `stream` ------------
+    # ---- the timed kernel's launch durations: CUDA events around each launch on `stream` -----------
+    # (one fused_kernel launch per step: paam_pack_analyze on a device-resident batch)
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    for k in range(args.steps):
+        kev[k][0].record(stream)
+        sets.pack_analyze(raw, wcrt, sched, bins, stream=stream)
+        kev[k][1].record(stream)
+    stream.synchronize()
+    fused_ms = [e[0].elapsed_time(e[1]) for e in kev]
+    # the split entry points (paam_repack -> paam_analyze: pack_kernel writes records, analyze_kernel
+    # reads them), timed the same way for reference
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     for k in range(args.steps):
         ev[k][0].record(stream)
@@ -267,9 +285,8 @@ def run_ours(args):
     stream.synchronize()
     pack_ms = [e[0].elapsed_time(e[1]) for e in ev]
     ana_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    seq_ms = sum(e[0].elapsed_time(e[2]) for e in ev) / args.steps
     bins.zero_()
-    sets.analyze(None, None, bins, stream=stream)  # one clean pass for the reported bin counts
+    sets.pack_analyze(raw, wcrt, sched, bins, stream=stream)  # one clean pass for the reported bin counts
     if dist is not None:
         allreduce_bins(bins, stream=stream)
     stream.synchronize()
@@ -335,7 +352,9 @@ def run_ours(args):
     stream.synchronize()
 
     # ---- e2e: the same metric through the C ABI with HOST buffers (copies inside the region) ------
-    e2e = None
+    # Each step copies the pinned host batch in (chunked, overlapped with the kernel of earlier chunks)
+    # and reads every WCRT, verdict and the bin counts back: the full output of the timed step.
+    e2e = e2e_vo = None
     if not args.no_e2e:
         from gen.inputs import generate_host
 
@@ -344,116 +363,155 @@ def run_ours(args):
 
         host = generate_host(gp, SEED, first, n, pinned_alloc=pinned)
         hb = paam.Batch.from_host(host)
+        hvb = paam.Batch.from_host(dict(host, flags=paam.PAAM_FLAG_VERDICT_ONLY))
+        wcrt_h = torch.empty(hb.c.n_chains, dtype=torch.int64, pin_memory=True)
         sched_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         bins_h = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
         hsets = paam.Sets(hb, stream=stream)
         ebins = torch.zeros_like(bins)
 
-        def e2e_step():
+        def e2e_step(batch, with_wcrt):
             with torch.cuda.stream(stream):
                 ebins.zero_()
-            # H2D of the raw batch in chunks (copy engine) overlapped with pack + analyze of earlier chunks
-            hsets.pack_analyze(hb, None, sched, ebins, stream=stream)
+            hsets.pack_analyze(batch, wcrt if with_wcrt else None, sched, ebins, stream=stream)
             if dist is not None:
                 allreduce_bins(ebins, stream=stream)
             with torch.cuda.stream(stream):
-                sched_h.copy_(sched, non_blocking=True)       # D2H: verdicts + bin counts
+                if with_wcrt:
+                    wcrt_h.copy_(wcrt, non_blocking=True)  # D2H: every WCRT
+                sched_h.copy_(sched, non_blocking=True)    # D2H: verdicts + bin counts
                 bins_h.copy_(ebins, non_blocking=True)
             stream.synchronize()
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        barrier(world)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+
+        def timed(batch, with_wcrt):
+            for _ in range(max(1, args.warmup)):
+                e2e_step(batch, with_wcrt)
+            barrier(world)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                e2e_step(batch, with_wcrt)
+            return max_over_ranks(time.perf_counter() - t0, world)
+        e2e_s = timed(hb, True)
+        if not np.array_equal(wcrt_h.numpy(), wcrt.cpu().numpy()):
+            raise RuntimeError("e2e WCRTs differ from the device-resident run")
         e2e = {"value": world * n * args.steps / e2e_s, "unit": "chain-sets/s",
-               "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
-               "ms_per_step": 1e3 * e2e_s / args.steps}
+               "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": 8 * hb.c.n_chains + n + 8 * 2 * gp.n_bins,
+               "ms_per_step": 1e3 * e2e_s / args.steps,
+               "note": "paam_pack_analyze from pinned host buffers (u64 CSR batch, chunked H2D overlapped with the "
+                       "kernel) + D2H of every WCRT, verdict and bin count; host wall clock, max over ranks"}
+        vo_s = timed(hvb, False)
+        e2e_vo = {"value": world * n * args.steps / vo_s, "unit": "chain-sets/s",
+                  "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
+                  "ms_per_step": 1e3 * vo_s / args.steps,
+                  "note": "as e2e with PAAM_FLAG_VERDICT_ONLY: verdicts and bins only"}
         hsets.free()
+    sets.pack_analyze(raw, wcrt, sched, vbins, stream=stream)  # the handle again describes `raw` (DES leg)
+    stream.synchronize()
 
     # ---- config 5 leg: the paired DES (paam_simulate) with the sim <= bound census -------------------
     des = None
     if args.des_sets > 0:
         nd = min(args.des_sets, n)
-        resp = torch.empty(raw.c.n_chains, dtype=torch.int64, device=dev)
-        dig = torch.empty(n, dtype=torch.int64, device=dev)
-        viol = torch.zeros(1, dtype=torch.int64, device=dev)
+        z = lambda k: torch.zeros(k, dtype=torch.int64, device=dev)
+        resp, cnt, miss, drop = (z(raw.c.n_chains) for _ in range(4))
+        dig, viol, stopped = z(n), z(1), z(1)
+        status = torch.empty(n, dtype=torch.int32, device=dev)
+        wit = torch.full((2 * 64,), -1, dtype=torch.int32, device=dev)
         hz = int(args.des_horizon_s * 1e9)
         sets.simulate(hz, 3, resp, None, dig, None, None, first_index=first, n=min(nd, 1024), stream=stream)  # warm-up
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = paam.kernel_launches()
         e0.record(stream)
-        sets.simulate(hz, 3, resp, None, dig, wcrt, viol, first_index=first, n=nd, stream=stream)
+        sets.simulate(hz, 3, resp, cnt, dig, wcrt, viol, first_index=first, n=nd, stream=stream, out_misses=miss,
+                      out_drops=drop, out_status=status, out_witness=wit, out_stopped=stopped)
         e1.record(stream)
         stream.synchronize()
         des_ms = max_over_ranks(e0.elapsed_time(e1), world)
         des_launches = paam.kernel_launches() - l0
-        v = viol.clone()
+        tot = torch.stack([viol[0], stopped[0], cnt.sum(), miss.sum(), drop.sum()]).clone()
         e0.record(stream)  # the same simulation without event digests (out_digest = NULL)
         sets.simulate(hz, 3, resp, None, None, wcrt, None, first_index=first, n=nd, stream=stream)
         e1.record(stream)
         stream.synchronize()
         des_nd_ms = max_over_ranks(e0.elapsed_time(e1), world)
         if dist is not None:
-            dist.all_reduce(v)
+            dist.all_reduce(tot)
+        tot = tot.tolist()
         des = {"metric": "chain-sets simulated/sec (PAAM DES, config-5 leg)", "value": world * nd / (des_ms / 1e3),
                "unit": "chain-sets/s", "sets_per_gpu": nd, "horizon_s": args.des_horizon_s, "seed": 3,
                "ms": des_ms, "digests": True, "value_without_digests": world * nd / (des_nd_ms / 1e3),
-               "sim_le_bound_violations": int(v.item()), "gpu_launches": des_launches,
-               "scope": "violations counted in sets the analysis declares schedulable (every CRITICAL chain R* <= D)"}
+               "sim_le_bound_violations": int(tot[0]), "stopped_sets": int(tot[1]),
+               "completed_instances": int(tot[2]), "deadline_misses": int(tot[3]), "be_drops": int(tot[4]),
+               "gpu_launches": des_launches,
+               "scope": "violations counted in the sets the analysis declares schedulable (every CRITICAL chain "
+                        "R* <= D) whose run was not stopped; stopped_sets = runs stopped by PAAM_SIM_BACKLOG / STEPCAP"}
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (by measured duration) ------------------------------------
+    # ---- roofline of the timed kernel ---------------------------------------------------------------
+    # fused_kernel is the whole step.  Algorithmic bytes per launch: the raw CSR batch it must read
+    # (§8(b) paam_batch) + the outputs it must write (u64 WCRT per chain, u8 verdict per set, bins).
     pk = peaks()
     hbm_peak = pk.get("hbm_gbs", 6533.2)
-    work = work_per_set(gp, first)
-    ana_avg = sum(ana_ms) / len(ana_ms)
-    pack_avg = sum(pack_ms) / len(pack_ms)
-    alu_peak = 148 * 128 * 1.965e9 / 1e12  # T lane-ops/s: 148 SMs x 4 SMSP x 32 lanes (alu + fma pipes)
+    clk_ghz = (clk.get("sm_mhz") or 1965.0) / 1e3
+    fused_avg = sum(fused_ms) / len(fused_ms)
     traffic = measured_traffic_per_set()
-    # pack_kernel: algorithmic bytes = the raw batch it must read + the record fields it must write
-    # (config 3: one sub-chain per chain, one accelerator segment per callback, 2 units):
-    # header 32 B + 4 B x (4 per chain + 2 W per chain + 9 per sub-chain + 4 per segment)
-    rec_used = 32 * n + 4 * (15 * raw.c.n_chains + 4 * raw.c.n_cbs)
-    pack_bytes = in_bytes + rec_used
-    pack_roof = {"bound": "hbm", "achieved": pack_bytes / (pack_avg / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                 "frac": pack_bytes / (pack_avg / 1e3) / 1e9 / hbm_peak,
-                 "traffic": None if traffic is None else traffic.get("pack_kernel", 0) * n,
-                 "kernel": "pack_kernel", "kernel_ms": pack_avg, "algorithmic_bytes": pack_bytes,
-                 "bytes_per_set": pack_bytes / n}
-    ops = work["mu_regrouped_per_set"] * OPS_PER_MU * n
-    ana_roof = {"bound": "alu", "achieved": ops / (ana_avg / 1e3) / 1e12, "peak": alu_peak,
-                "unit": "Tops/s (int32 lane-ops)", "frac": ops / (ana_avg / 1e3) / 1e12 / alu_peak,
-                "traffic": None if traffic is None else traffic.get("analyze_kernel", 0) * n,
-                "kernel": "analyze_kernel", "kernel_ms": ana_avg, "ops_per_set": work["mu_regrouped_per_set"] * OPS_PER_MU,
-                "peak_source": "derived: 148 SMs x 128 int32 lanes/clk (B300_MICROARCH alu+fma pipes) x 1.965 GHz",
-                "hbm_achieved_GBps": (rec_bytes * n) / (ana_avg / 1e3) / 1e9}
     issue = ncu_issue_stats()
-    pack_roof["ncu_issue"] = issue.get("pack_kernel")
-    ana_roof["ncu_issue"] = issue.get("analyze_kernel")
-    dominant = pack_roof if pack_avg >= ana_avg else ana_roof
-    other = ana_roof if dominant is pack_roof else pack_roof
-    roof = dict(dominant)
-    roof.update({"share_of_sequential_step": dominant["kernel_ms"] / seq_ms, "sequential_step_ms": seq_ms,
-                 "peak_of": "measured (MEASURED_PEAKS.json)" if (pk and dominant is pack_roof) else
-                            ("derived" if dominant is ana_roof else "fallback"),
-                 "note": "kernel_ms from a sequential repack+analyze pass on the bench stream; the timed step "
-                         "overlaps pack and analyze chunks on two internal streams (paam_pack_analyze)"})
+    out_bytes = 8 * raw.c.n_chains + n + 16 * gp.n_bins
+    alg_bytes = in_bytes + out_bytes
+    roof = {"bound": "hbm", "achieved": alg_bytes / (fused_avg / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": alg_bytes / (fused_avg / 1e3) / 1e9 / hbm_peak,
+            "traffic": None if not traffic or "fused_kernel" not in traffic else traffic["fused_kernel"] * n,
+            "kernel": "fused_kernel", "kernel_ms": fused_avg, "share_of_step": fused_avg / (ms / args.steps),
+            "algorithmic_bytes": alg_bytes, "bytes_per_set": alg_bytes / n,
+            "peak_of": "measured (MEASURED_PEAKS.json hbm_gbs)" if pk else "fallback (B200_PROFILING.md)",
+            "ncu_issue": issue.get("fused_kernel"),
+            "note": "one launch per step; per-launch CUDA events on the bench stream. The kernel is issue-bound "
+                    "(see issue): its HBM traffic is the raw batch once, the derived records stay on chip"}
+    # issue roofline: warp-instructions per set (ncu) x sets/s vs 148 SMs x 4 schedulers x clock
+    iss = issue.get("fused_kernel") or {}
+    if iss.get("warp_inst_per_set"):
+        ach = iss["warp_inst_per_set"] * n / (fused_avg / 1e3) / 1e12
+        peak_issue = 148 * 4 * clk_ghz / 1e3
+        roof["issue"] = {"achieved": ach, "peak": peak_issue, "unit": "T warp-instructions/s", "frac": ach / peak_issue,
+                         "warp_inst_per_set": iss["warp_inst_per_set"]}
+    # the algorithmic integer work (oracle-counted regrouped mu-terms x 4 ops) against the ALU roof
+    work = work_per_set(gp, first)
+    alu_peak = 148 * 128 * clk_ghz / 1e3  # T lane-ops/s: 148 SMs x 128 int32 lanes/clk (alu + fma pipes)
+    ops = work["mu_regrouped_per_set"] * OPS_PER_MU * n
+    other = {"bound": "alu", "achieved": ops / (fused_avg / 1e3) / 1e12, "peak": alu_peak,
+             "unit": "Tops/s (int32 lane-ops)", "frac": ops / (fused_avg / 1e3) / 1e12 / alu_peak,
+             "kernel": "fused_kernel", "ops_per_set": work["mu_regrouped_per_set"] * OPS_PER_MU,
+             "peak_source": "derived: 148 SMs x 128 int32 lanes/clk (B300_MICROARCH alu+fma pipes) x measured SM clock"}
+    split = {"pack_kernel_ms": sum(pack_ms) / len(pack_ms), "analyze_kernel_ms": sum(ana_ms) / len(ana_ms),
+             "note": "paam_repack + paam_analyze (records written to / read from HBM), same batch, for reference",
+             "ncu": {k: issue.get(k) for k in ("pack_kernel", "analyze_kernel")},
+             "dram_bytes_per_set": {k: (traffic or {}).get(k) for k in ("pack_kernel", "analyze_kernel")}}
+    if des is not None:
+        di = issue.get("simulate_kernel") or {}
+        if di.get("warp_inst_per_set"):
+            ach = di["warp_inst_per_set"] * des["value"] / world / 1e12
+            peak_issue = 148 * 4 * clk_ghz / 1e3
+            des["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_issue, "unit": "T warp-instructions/s",
+                               "frac": ach / peak_issue, "traffic": None if not traffic or "simulate_kernel" not in traffic
+                               else traffic["simulate_kernel"] * nd,
+                               "kernel": "simulate_kernel", "warp_inst_per_set": di["warp_inst_per_set"],
+                               "note": "issue roofline: the DES state lives in shared memory (DRAM traffic is the raw "
+                                       "batch and the outputs); warp-instructions per set from the committed ncu capture"}
     out = {"metric": METRIC, "value": value, "unit": "chain-sets/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
            "config": {"workload": workload_name(n), "sets_per_gpu": n, "global_sets": world * n, "seed": SEED,
-                      "l2": f"inputs larger than L2: {(in_bytes + rec_bytes * n) / 1e9:.1f} GB/GPU resident",
+                      "l2": f"inputs larger than L2: the {in_bytes / 1e9:.1f} GB raw batch is read once per step",
                       "parallelism": f"dp{world} (set-index shards, NCCL all-reduce of bin counts)"},
-           "gpu_launches": int(launches), "clocks": clk, "roofline": roof, "roofline_other_kernel": other,
-           "bins": bins.cpu().tolist()}
+           "gpu_launches": int(launches), "clocks": clk, "roofline": roof, "roofline_alu": other,
+           "split_path": split, "bins": bins.cpu().tolist()}
     if e2e:
         out["e2e"] = e2e
+        out["e2e_verdict_only"] = e2e_vo
     if e2e_gen:
         out["e2e_device_generate"] = e2e_gen
     out["verdict_only"] = verdict_only
@@ -510,7 +568,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--des-sets", type=int, default=100_000, help="sets per GPU for the DES leg (0 = skip)")
+    ap.add_argument("--des-sets", type=int, default=1_000_000, help="sets per GPU for the DES leg (config 5: 1M; 0 = skip)")
     ap.add_argument("--des-horizon-s", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
