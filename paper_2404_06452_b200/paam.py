@@ -356,17 +356,24 @@ class Sweeper:
             pass
 
 
-def analyze(batch, stream=None):
-    """Pack + analyse a batch; returns numpy (wcrt[n_chains] u64, sched[n] u8, status[n] i32, bins)."""
+def analyze(batch, stream=None, fused=False):
+    """Analyse a batch; returns numpy (wcrt[n_chains] u64, sched[n] u8, status[n] i32, bins).
+    fused=False: paam_pack + paam_analyze (records through HBM); fused=True: paam_pack_analyze (one
+    fused_kernel launch, the bench's path; a host batch is copied in chunks overlapping the kernel)."""
     import torch
     n = batch.n_sets
     dev = torch.device("cuda")
-    status = np.zeros(max(n, 1), np.int32) if batch.c.mem == PAAM_MEM_HOST else torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-    sets = Sets(batch, status, stream)
-    wcrt = torch.empty(max(batch.c.n_chains, 1), dtype=torch.int64, device=dev)
-    sched = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    host = batch.c.mem == PAAM_MEM_HOST
+    mk_status = lambda: np.full(max(n, 1), -9, np.int32) if host else torch.full((max(n, 1),), -9, dtype=torch.int32, device=dev)
+    status = mk_status()
+    sets = Sets(batch, None if fused else status, stream)
+    wcrt = torch.full((max(batch.c.n_chains, 1),), -5, dtype=torch.int64, device=dev)
+    sched = torch.full((max(n, 1),), 7, dtype=torch.uint8, device=dev)
     bins = torch.zeros(max(sets.n_bins * 2, 1), dtype=torch.int64, device=dev)
-    sets.analyze(wcrt, sched, bins if sets.n_bins else None, stream=stream)
+    if fused:
+        sets.pack_analyze(batch, wcrt, sched, bins if sets.n_bins else None, out_status=status, stream=stream)
+    else:
+        sets.analyze(wcrt, sched, bins if sets.n_bins else None, stream=stream)
     torch.cuda.synchronize()
     st = status if isinstance(status, np.ndarray) else status.cpu().numpy()
     out = (wcrt.cpu().numpy().view(np.uint64)[:batch.c.n_chains], sched.cpu().numpy()[:n], st[:n],

@@ -30,15 +30,20 @@ def gpu_device_path(batch):
     return paam.analyze(paam.Batch.from_host_to_device(batch))
 
 
-def assert_same(batch, gpu):
+def assert_same(batch, gpu, fused_too=True):
+    """The given GPU result (split path: paam_pack + paam_analyze) and the fused path (paam_pack_analyze,
+    fused_kernel, host batch) against the oracle, element by element."""
     ow, osch, ost, ob = O.analyze(batch, nthreads=NPROC)
-    gw, gsch, gst, gb = gpu
-    assert np.array_equal(ost, gst), np.nonzero(ost != gst)[0][:10]
-    bad = np.nonzero(ow != gw)[0]
-    assert bad.size == 0, (bad[:10], ow[bad[:10]], gw[bad[:10]])
-    assert np.array_equal(osch, gsch)
-    if batch.get("n_bins"):
-        assert np.array_equal(ob, gb)
+    results = [("split", gpu)]
+    if fused_too:
+        results.append(("fused", paam.analyze(paam.Batch.from_host(batch), fused=True)))
+    for name, (gw, gsch, gst, gb) in results:
+        assert np.array_equal(ost, gst), (name, np.nonzero(ost != gst)[0][:10])
+        bad = np.nonzero(ow != gw)[0]
+        assert bad.size == 0, (name, bad[:10], ow[bad[:10]], gw[bad[:10]])
+        assert np.array_equal(osch, gsch), name
+        if batch.get("n_bins"):
+            assert np.array_equal(ob, gb), name
 
 
 def test_worked_examples_on_gpu():
