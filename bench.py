@@ -451,6 +451,8 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
+    case_studies = case_study_leg(paam, torch, dev) if not args.no_case_studies else None
+
     # ---- roofline of the timed kernel ---------------------------------------------------------------
     # fused_kernel is the whole step.  Algorithmic bytes per launch: the raw CSR batch it must read
     # (§8(b) paam_batch) + the outputs it must write (u64 WCRT per chain, u8 verdict per set, bins).
@@ -515,6 +517,8 @@ def run_ours(args):
     if e2e_gen:
         out["e2e_device_generate"] = e2e_gen
     out["verdict_only"] = verdict_only
+    if case_studies:
+        out["case_studies"] = case_studies
     if des:
         out["des"] = des
     if world == 1 and not args.no_cpu_baseline:
@@ -524,6 +528,48 @@ def run_ours(args):
     print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def case_study_leg(paam, torch, dev, phasings=256, horizon_ms=3000):
+    """Configs 1a / 1b: the paper's Case Study 3 (n = 6 and n = 1) and the Case-Study-1
+    shaped set (invented numbers, gen/inputs.CS1_SHAPED) through the fused path, and the DES over
+    `phasings` release phasings (the set replicated, phases from (seed, set index)) in PAAM mode and in
+    the FIFO_DIRECT baseline the paper compares against."""
+    import numpy as np
+    from gen.inputs import MS, US, case_study_1_shaped, case_study_3, flatten
+    out = {}
+    for name, s in (("cs3_n6", case_study_3(6)), ("cs3_n1", case_study_3(1)), ("cs1_shaped", case_study_1_shaped())):
+        b = flatten([s] * phasings, comm_cost=100 * US)
+        wcrt, sched, status, _ = paam.analyze(paam.Batch.from_host(b), fused=True)
+        m = len(s.chains)
+        hb = paam.Batch.from_host(b)
+        sets = paam.Sets(hb)
+        bound = torch.from_numpy(wcrt.view(np.int64).copy()).to(dev)
+        res = {}
+        for mode in ("paam", "fifo_direct"):
+            resp = torch.zeros(hb.c.n_chains, dtype=torch.int64, device=dev)
+            viol = torch.zeros(1, dtype=torch.int64, device=dev)
+            st = torch.empty(phasings, dtype=torch.int32, device=dev)
+            sets.simulate(horizon_ms * MS, 1, resp, bound=bound, out_violations=viol, out_status=st,
+                          fifo=(mode == "fifo_direct"))
+            torch.cuda.synchronize()
+            r = resp.cpu().numpy().view(np.uint64).reshape(phasings, m)
+            res[mode] = {"max_observed_ms": [round(float(x) / 1e6, 3) for x in r.max(axis=0)],
+                         "violations": int(viol.item()), "stopped_runs": int((st.cpu().numpy() != 0).sum())}
+            if res[mode]["stopped_runs"]:
+                res[mode]["note"] = ("runs stopped by PAAM_SIM_BACKLOG (a CRITICAL chain's backlog outgrew the device's "
+                                     "instance slots, D14): their maxima cover the exact prefix, lower bounds")
+        sets.free()
+        w = wcrt[:m]
+        out[name] = {"schedulable": bool(sched[0]),
+                     "critical": [ch.cls == 0 for ch in s.chains],
+                     "wcrt_bound_ms": [None if x == paam.UNSCHED else round(float(x) / 1e6, 3) for x in w],
+                     "des_paam": res["paam"], "des_fifo_direct": res["fifo_direct"],
+                     "phasings": phasings, "horizon_ms": horizon_ms}
+    out["note"] = ("configs 1a (Case Study 3, PAPER.md:971-974) and 1b (Case Study 1's shape, PAPER.md:488-499, "
+                   "invented numbers); bounds from the fused kernel, DES maxima over the phasings; the DES of "
+                   "BE chains is unbounded by the analysis (their bound is UNSCHED)")
+    return out
 
 
 def work_per_set(gp, first, sample=4000):
@@ -568,6 +614,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-case-studies", action="store_true")
     ap.add_argument("--des-sets", type=int, default=1_000_000, help="sets per GPU for the DES leg (config 5: 1M; 0 = skip)")
     ap.add_argument("--des-horizon-s", type=float, default=10.0)
     args = ap.parse_args()

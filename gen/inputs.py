@@ -301,3 +301,48 @@ def with_candidate(s: System, T, prio, cbs, D=None, cls=CRITICAL) -> System:
     t = copy.deepcopy(s)
     t.chain(T=T, D=D, prio=prio, cls=cls, cbs=cbs)
     return t
+
+
+# ----------------------------------------------------------------------------------------------
+# The paper's case-study chain sets (configs 1a / 1b of SURVEY.md §8(d)); inputs only.
+def case_study_3(buckets: int = 6) -> System:
+    """Case Study 3 (SPEC.md:456-457 split): two critical chains T = D = 120 / 220 ms
+    and four BE chains T = 52 ms, each one callback CPU 1 ms + GPU 50 ms + CPU 1 ms, six single-threaded
+    executors on their own cores, the GPU server on core 0 with n buckets (6 = PAAM's default, P:344;
+    1 = TPU-like), eps = 391 us, kappa = 130 us."""
+    s = System()
+    g = s.accel(buckets=buckets, units=1, server_core=0, eps=391 * US, kappa=130 * US)
+    specs = [(120, 6, CRITICAL), (220, 5, CRITICAL), (52, 4, BEST_EFFORT), (52, 3, BEST_EFFORT),
+             (52, 2, BEST_EFFORT), (52, 1, BEST_EFFORT)]
+    for i, (T, prio, cls) in enumerate(specs):
+        x = s.executor(core=1 + i, prio=1, wait=SUSPEND)
+        s.chain(T=T * MS, prio=prio, cls=cls, cbs=[cb(x, cpu(1 * MS), acc(g, 50 * MS), cpu(1 * MS))])
+    return s
+
+
+# Config 1b: Case Study 1's SHAPE (PAPER.md:488-499), with INVENTED numbers: the paper's chain figure is
+# missing (SPEC.md:469), so the periods, the CPU WCETs E and the chain lengths below are this
+# repository's, labelled as such.  What follows the paper: 8 chains, critical chains 1-6 (chain 1
+# highest priority, chain 6 lowest) and BE 1-2 duplicating chains 1 and 3; every callback has one GPU
+# segment of A = 10 ms; the critical chains run on four single-threaded executors on cores 2-7, the BE
+# chains on their own executors on cores 2-3; the PAAM server with six buckets on core 0.
+CS1_SHAPED = [  # (T = D ms, callbacks' CPU WCETs E ms, executor)   -- invented values
+    (400, (4, 2), 0), (500, (2, 3, 2), 0), (600, (6, 4), 1), (800, (3, 3), 1), (1000, (5, 2, 3), 2),
+    (1200, (4, 6), 3)]
+
+
+def case_study_1_shaped() -> System:
+    """Config 1b (labelled invented numbers, see CS1_SHAPED)."""
+    s = System()
+    g = s.accel(buckets=6, units=1, server_core=0, eps=391 * US, kappa=130 * US)
+    xs = [s.executor(core=2 + i, prio=2, wait=SUSPEND) for i in range(4)]  # critical executors, cores 2-5
+    xbe = [s.executor(core=2, prio=1, wait=SUSPEND), s.executor(core=3, prio=1, wait=SUSPEND)]  # BE, cores 2-3
+
+    def callbacks(es, x):
+        return [cb(x, cpu(e * MS // 2), acc(g, 10 * MS), cpu(e * MS - e * MS // 2)) for e in es]
+    for i, (T, es, xi) in enumerate(CS1_SHAPED):
+        s.chain(T=T * MS, prio=8 - i, cls=CRITICAL, cbs=callbacks(es, xs[xi]))
+    for j, src in enumerate((0, 2)):  # BE 1 = chain 1, BE 2 = chain 3 (duplicates), lowest priorities
+        T, es, _ = CS1_SHAPED[src]
+        s.chain(T=T * MS, prio=2 - j, cls=BEST_EFFORT, cbs=callbacks(es, xbe[j]))
+    return s

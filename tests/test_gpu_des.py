@@ -9,7 +9,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from gen.inputs import MS, System, cb, config2_params, config3_params, cpu, flatten, generate_host, make_params
+from gen.inputs import MS, System, case_study_1_shaped, cb, config2_params, config3_params, cpu, flatten, generate_host, make_params
 from oracle import oracle as O
 from paper_2404_06452_b200 import paam
 from tests.ref_scan import random_small_system
@@ -94,7 +94,7 @@ def check(batch, horizon, seed, first_index=0, fifo=False):
 
 def test_worked_examples_des():
     systems = [two_chain_accel_system(kappa=100_000, buckets=2), app_b_two_chains(), cs3_system(6), cs3_system(1),
-               a10_system()]
+               a10_system(), case_study_1_shaped()]  # configs 1a (CS3) and 1b (CS1-shaped)
     b = flatten(systems, comm_cost=0)
     for seed in (0, 1, 2, 3):
         check(b, 1_500 * MS, seed)

@@ -17,6 +17,7 @@ from gen.inputs import (CRITICAL, MS, US, Seg, System, acc, cb, config2_params, 
 from oracle import oracle as O
 from paper_2404_06452_b200 import paam
 from tests.ref_scan import random_small_system
+from gen.inputs import case_study_1_shaped
 from tests.test_oracle_pins import GOLD, a10_system, app_b_two_chains, cs3_system, two_chain_accel_system
 
 NPROC = os.cpu_count() or 1
@@ -48,7 +49,7 @@ def assert_same(batch, gpu, fused_too=True):
 
 def test_worked_examples_on_gpu():
     systems = [two_chain_accel_system(), two_chain_accel_system(eps=391 * US), app_b_two_chains(),
-               cs3_system(6), cs3_system(1), a10_system()]
+               cs3_system(6), cs3_system(1), a10_system(), case_study_1_shaped()]  # + config 1b
     for flags in (0, 1):
         b = flatten(systems, comm_cost=0, flags=flags)
         assert_same(b, gpu_host_path(b))
