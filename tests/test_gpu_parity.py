@@ -85,7 +85,7 @@ def mutate_invalid(s: System, rng):
     elif k == 5:
         s.execs[0] = (10, 1, 0)  # server core of accelerator 0
     elif k == 6:
-        s.chains[0].T = 1 << 31
+        s.chains[0].T = 1 << 48
     elif k == 7:
         s.chains[0].cbs[0].segs.append(Seg(s.chains[0].cbs[0].segs[-1].kind, 1))
     elif k == 8 and len(s.execs) > 1:

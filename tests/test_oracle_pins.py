@@ -199,7 +199,7 @@ def test_bucket_map(m, n, want):
     (lambda s: setattr(s.chains[0].cbs[0].segs[1], "accel", 3), 3),
     (lambda s: setattr(s.chains[0].cbs[0].segs[0], "wcet", 0), 4),
     (lambda s: s.execs.__setitem__(0, (0, 1, 0)), 7),
-    (lambda s: setattr(s.chains[0], "T", 1 << 31), 1),
+    (lambda s: setattr(s.chains[0], "T", 1 << 48), 1),
     (lambda s: s.chains[0].cbs[0].segs.append(acc(0, 1)), 4),
 ])
 def test_validation(mutate, code):
@@ -301,3 +301,20 @@ def test_out_of_range_bin_is_a_range_error():
     _, sched, status, bins = O.analyze(b)
     assert status.tolist() == [0, 1, 0] and sched.tolist() == [1, 0, 1]
     assert bins.tolist() == [1, 1, 1, 1]
+
+
+def test_wide_times_scale_exactly():
+    """Times of 2^31 ns and beyond (u64 boundary; domain < 2^48 ns, A14): the analysis is
+    homogeneous of degree one in time (mu(R, T) = ceil(R/T) + 1 is scale-invariant), so App. B's
+    two-chain set with every time x1000 (T = 20 s / 50 s) has R = 11 s / 40 s exactly."""
+    s = app_b_two_chains()
+    for ch in s.chains:
+        ch.T *= 1000
+        ch.D *= 1000
+        for c in ch.cbs:
+            for g in c.segs:
+                g.wcet *= 1000
+    b, (wcrt, sched, status, _) = run([s])
+    assert status[0] == 0 and sched[0] == 1
+    assert wcrt.tolist() == [x * 1000 for x in GOLD["two_chains_one_executor"]["R"]]
+    assert max(ch.T for ch in s.chains) > (1 << 31)
