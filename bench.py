@@ -285,7 +285,8 @@ def run_ours(args):
     stream.synchronize()
     pack_ms = [e[0].elapsed_time(e[1]) for e in ev]
     ana_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    bins.zero_()
+    with torch.cuda.stream(stream):
+        bins.zero_()  # on the kernel's stream (a default-stream zero could race the kernel)
     sets.pack_analyze(raw, wcrt, sched, bins, stream=stream)  # one clean pass for the reported bin counts
     if dist is not None:
         allreduce_bins(bins, stream=stream)
@@ -297,6 +298,7 @@ def run_ours(args):
     vb.flags |= paam.PAAM_FLAG_VERDICT_ONLY
     vbatch = types.SimpleNamespace(c=vb)
     vbins = torch.zeros_like(bins)
+    stream.wait_stream(torch.cuda.current_stream())  # the allocations / zeroing above precede the kernels
     for _ in range(args.warmup):
         sets.pack_analyze(vbatch, None, sched, vbins, stream=stream)
     stream.synchronize()
@@ -322,6 +324,7 @@ def run_ours(args):
         sched_g = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         bins_g = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
         gbins = torch.zeros_like(bins)
+        stream.wait_stream(torch.cuda.current_stream())
         sweeper = paam.Sweeper()
 
         def gen_step():
@@ -369,6 +372,7 @@ def run_ours(args):
         bins_h = torch.empty(2 * gp.n_bins, dtype=torch.int64, pin_memory=True)
         hsets = paam.Sets(hb, stream=stream)
         ebins = torch.zeros_like(bins)
+        stream.wait_stream(torch.cuda.current_stream())
 
         def e2e_step(batch, with_wcrt):
             with torch.cuda.stream(stream):
@@ -418,6 +422,7 @@ def run_ours(args):
         status = torch.empty(n, dtype=torch.int32, device=dev)
         wit = torch.full((2 * 64,), -1, dtype=torch.int32, device=dev)
         hz = int(args.des_horizon_s * 1e9)
+        stream.wait_stream(torch.cuda.current_stream())  # the zeroed outputs precede the kernels
         sets.simulate(hz, 3, resp, None, dig, None, None, first_index=first, n=min(nd, 1024), stream=stream)  # warm-up
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = paam.kernel_launches()

@@ -19,9 +19,12 @@
  *
  * Conventions.
  *   - Every time is an unsigned 64-bit integer number of nanoseconds.  Each individual
- *     period, deadline, WCET, eps, kappa and comm cost must be < 2^31 - 1 ns (about 2.1 s): the device
- *     path computes in 32-bit integers with sums saturating just above the deadline, which is exact
- *     because any value above the deadline is a miss.
+ *     period, deadline, WCET, eps and kappa must be < 2^48 ns (about 78 hours; PAAM_SET_ERANGE
+ *     otherwise), the comm cost too (PAAM_EINVAL).  A set whose times are all < 2^31 - 1 ns (about
+ *     2.1 s) runs on the u32 kernels, whose sums saturate just above the deadline -- exact, because any
+ *     value above the deadline is a miss; a set with a larger time is handed over
+ *     to an exact u64 path (wide.cu) with the same results and statuses.  The DES computes in 32-bit
+ *     time distances: it reports such a set PAAM_SIM_WIDE and needs comm cost < 2^31 - 1 ns.
  *   - Indices inside a set are set-local (executor, accelerator, unit); CSR offset arrays are global.
  *   - All calls are asynchronous on the given CUDA stream unless stated otherwise.  Exceptions that
  *     synchronise the stream: paam_pack / paam_repack with host-resident input, paam_pack_analyze
@@ -56,7 +59,8 @@ typedef void* paam_stream_t; /* a cudaStream_t (may be NULL = legacy default str
 /* ---- per-set validation status (out_status[i]) -------------------------------------------- */
 /* Checked in this order; the first failing rule is reported. */
 #define PAAM_SET_OK 0
-#define PAAM_SET_ERANGE 1    /* over the size caps below, T == 0, or a time >= 2^31 - 1 ns */
+#define PAAM_SET_ERANGE 1    /* over the size caps below, T == 0, a time >= 2^48 ns, or a utilisation
+                                bin >= n_bins (such a set is counted in no bin) */
 #define PAAM_SET_EDANGLING 2 /* chain without callbacks, callback without segments, executor or
                                 unit index out of range */
 #define PAAM_SET_EACCEL 3    /* ACCEL segment on an undeclared accelerator */
@@ -263,6 +267,8 @@ int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_sta
 #define PAAM_SIM_INVALID 1
 #define PAAM_SIM_BACKLOG 2
 #define PAAM_SIM_STEPCAP 3
+#define PAAM_SIM_WIDE 4    /* not simulated: the set has a time >= 2^31 - 1 ns (the DES computes in 32-bit time
+                              distances); the analysis handles such sets exactly (u64 path) */
 typedef struct {
   uint64_t *resp, *count, *misses, *drops;
   uint64_t* digest;

@@ -237,8 +237,10 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
     const uint32_t nhdr = nset < n ? __ldg(hdr_base + (size_t)nset * HDR_STRIDE) : 0u;
     __syncwarp();
     const int32_t status = r.status;
+    const bool handed = status == REC_STATUS_WIDE;  // a wide set: wide_kernel writes its outputs
     uint32_t sched = 0;
-    if (status != PAAM_SET_OK) {
+    if (handed) {
+    } else if (status != PAAM_SET_OK) {
       if (out_wcrt)
         for (uint32_t i = lane; i < r.n_out; i += 32) out_wcrt[r.chain_base + i] = UNS;
       if (out_fail && lane == 0) out_fail[set] = -2 - status;  // admission: rejected by validation
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       }
     }
   verdict_done:
-    if (lane == 0) {
+    if (lane == 0 && !handed) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
       if (out_bins && r.bin < n_bins) {  // (pack stores bin = ~0 for an out-of-range bin: ERANGE)
         if (warp_bins) {

@@ -21,7 +21,9 @@ struct paam_sets {
   paam_batch dev;    // the packed batch with device pointers (paam_simulate reads its structure)
   cudaStream_t side[3];  // internal streams of paam_pack_analyze: pack, analyze, H2D copies (created on first use)
   cudaEvent_t ev[17], evc[8];  // evc: chunk copies done
-  unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18
+  unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18,
+                          // 20: number of wide sets listed (wide.cu)
+  uint32_t* wide_list;    // [cap] the sets handed over to the u64 path by the last pack / fused launch
   int device;             // the CUDA device the handle lives on (made current by every call)
   bool rec_valid;         // rec holds the records of `dev` (false after the fused paam_pack_analyze, which writes
                           // none: the next paam_analyze / paam_admit / paam_simulate packs them first)
@@ -117,7 +119,8 @@ int ensure_streams(paam_sets* sets) {
 int ensure_records(const paam_sets* cs, cudaStream_t st) {
   paam_sets* sets = const_cast<paam_sets*>(cs);
   if (sets->rec_valid) return PAAM_OK;
-  if (int rc = launch_pack(&sets->dev, sets->rec, nullptr, st)) return rc;
+  cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
+  if (int rc = launch_pack(&sets->dev, sets->rec, nullptr, sets->wide_list, sets->tickets + 20, st)) return rc;
   sets->rec_valid = true;
   return PAAM_OK;
 }
@@ -125,7 +128,7 @@ int ensure_records(const paam_sets* cs, cudaStream_t st) {
 int check_batch(const paam_batch* b) {
   if (!b) return fail(PAAM_EINVAL, "NULL batch");
   if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
-  if (b->comm_cost >= LIM) return fail(PAAM_EINVAL, "batch.comm_cost must be < 2^31 - 1 ns");
+  if (b->comm_cost >= LIMW) return fail(PAAM_EINVAL, "batch.comm_cost must be < 2^48 ns");
   if (b->flags & ~(PAAM_FLAG_BLOCKING_SOUND | PAAM_FLAG_WFD_UNITS | PAAM_FLAG_VERDICT_ONLY))
     return fail(PAAM_EINVAL, "unknown flag");
   if (b->set_bin && b->n_bins == 0) return fail(PAAM_EINVAL, "set_bin given with n_bins == 0");
@@ -175,7 +178,11 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
       status_dev = sets->dstatus;
     }
   }
-  rc = launch_pack(&d, sets->rec, status_dev, st);
+  cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
+  rc = launch_pack(&d, sets->rec, status_dev, sets->wide_list, sets->tickets + 20, st);
+  if (rc) return rc;
+  // the wide sets (a time >= 2^31 - 1 ns): validated on the u64 path (statuses only here)
+  rc = launch_wide(&d, sets->wide_list, sets->tickets + 20, status_dev, nullptr, nullptr, nullptr, nullptr, st);
   if (rc) return rc;
   if (batch->mem == PAAM_MEM_HOST) {
     if (out_status && batch->n_sets)
@@ -212,6 +219,7 @@ extern "C" int paam_pack(const paam_batch* batch, paam_sets** out, int32_t* out_
     return fail_cuda(e, "paam_pack: ticket cudaMalloc");
   }
   e = cudaMalloc((void**)&s->rec, sizeof(Record) * (size_t)(batch->n_sets ? batch->n_sets : 1));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->wide_list, sizeof(uint32_t) * (size_t)(batch->n_sets ? batch->n_sets : 1));
   if (e != cudaSuccess) {
     paam_free(s);  // releases the tickets
     return fail_cuda(e, "paam_pack: record cudaMalloc");
@@ -233,8 +241,13 @@ extern "C" int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcr
     return fail(PAAM_EINVAL, "paam_analyze: PAAM_FLAG_VERDICT_ONLY writes no WCRTs (out_wcrt must be NULL)");
   if (int rc = use_device(sets)) return rc;
   if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
-  return launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
-                        sets->n_bins ? out_bins : nullptr, sets->tickets + 16, (cudaStream_t)stream);
+  int rc = launch_analyze(sets->rec, n, sets->comm, sets->flags, sets->n_bins, out_wcrt, out_sched,
+                          sets->n_bins ? out_bins : nullptr, sets->tickets + 16, (cudaStream_t)stream);
+  if (rc) return rc;
+  paam_batch v = sets->dev;  // the wide sets of the first n
+  v.n_sets = n;
+  return launch_wide(&v, sets->wide_list, sets->tickets + 20, nullptr, out_wcrt, out_sched, sets->n_bins ? out_bins : nullptr,
+                     nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_t* out_wcrt,
@@ -243,8 +256,13 @@ extern "C" int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decisi
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_admit: n exceeds the packed sets");
   if (int rc = use_device(sets)) return rc;
   if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
-  return launch_analyze(sets->rec, n, sets->comm, sets->flags & ~PAAM_FLAG_VERDICT_ONLY, 0, out_wcrt, nullptr, nullptr,
-                        const_cast<paam_sets*>(sets)->tickets + 17, (cudaStream_t)stream, out_decision);
+  int rc = launch_analyze(sets->rec, n, sets->comm, sets->flags & ~PAAM_FLAG_VERDICT_ONLY, 0, out_wcrt, nullptr, nullptr,
+                          const_cast<paam_sets*>(sets)->tickets + 17, (cudaStream_t)stream, out_decision);
+  if (rc) return rc;
+  paam_batch v = sets->dev;
+  v.n_sets = n;
+  return launch_wide(&v, sets->wide_list, sets->tickets + 20, nullptr, out_wcrt, nullptr, nullptr, out_decision,
+                     (cudaStream_t)stream);
 }
 
 extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon, uint64_t seed, uint64_t first_index,
@@ -252,6 +270,8 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (n > sets->n_sets) return fail(PAAM_EINVAL, "paam_simulate: n exceeds the packed sets");
   if (sim_flags & ~(uint32_t)PAAM_SIM_FIFO_DIRECT) return fail(PAAM_EINVAL, "paam_simulate: unknown sim flag");
+  if (sets->dev.comm_cost >= LIM)
+    return fail(PAAM_EINVAL, "paam_simulate: the DES needs comm_cost < 2^31 - 1 ns (32-bit time distances)");
   paam_sim_out o{};
   if (out) o = *out;
   if (o.witness && !o.violations) return fail(PAAM_EINVAL, "paam_simulate: witness needs violations");
@@ -280,7 +300,14 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   int32_t* status_dev = out_status;
   if (!host) {
     // steps 2-6 in one kernel (fused.cu): the derived records stay on chip
-    if ((rc = launch_fused(&d, status_dev, out_wcrt, out_sched, const_cast<int64_t*>(bins), st))) return rc;
+    cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
+    if ((rc = launch_fused(&d, sets->wide_list, sets->tickets + 20, status_dev, out_wcrt, out_sched,
+                           const_cast<int64_t*>(bins), st)))
+      return rc;
+    // the sets it handed over (a time >= 2^31 - 1 ns): exact u64 path
+    if ((rc = launch_wide(&d, sets->wide_list, sets->tickets + 20, status_dev, out_wcrt, out_sched,
+                          const_cast<int64_t*>(bins), nullptr, st)))
+      return rc;
   } else {
     // Host batch: K chunks; chunk i's slice of every array is copied H2D on side[2] while the kernel of
     // chunk i-1 runs on side[0] (copy engines alongside the SMs).
@@ -354,8 +381,13 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
       view.set_exec_off += lo;
       view.set_accel_off += lo;
       if (view.set_bin) view.set_bin += lo;
-      if ((rc = launch_fused(&view, status_dev ? status_dev + lo : nullptr, out_wcrt, out_sched ? out_sched + lo : nullptr,
+      cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), sets->side[0]);
+      if ((rc = launch_fused(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
+                             out_sched ? out_sched + lo : nullptr,
                              const_cast<int64_t*>(bins), sets->side[0])))
+        return rc;
+      if ((rc = launch_wide(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
+                            out_sched ? out_sched + lo : nullptr, const_cast<int64_t*>(bins), nullptr, sets->side[0])))
         return rc;
     }
     cudaEventRecord(sets->ev[9], sets->side[0]);
@@ -392,6 +424,7 @@ extern "C" void paam_free(paam_sets* sets) {
   cudaSetDevice(sets->device);
   if (sets->rec) cudaFree(sets->rec);
   if (sets->tickets) cudaFree(sets->tickets);
+  if (sets->wide_list) cudaFree(sets->wide_list);
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
   if (sets->side[0]) {

@@ -30,7 +30,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 #endif
 
 constexpr uint32_t SAT = 0x7FFFFFFFu;
-constexpr uint64_t LIM = 0x7FFFFFFFull;  // inputs must be < LIM (validation, PAAM_SET_ERANGE)
+constexpr uint64_t LIM = 0x7FFFFFFFull;  // the u32 kernels take the sets whose every time is < LIM (A14)
 
 __device__ __forceinline__ uint32_t sadd(uint32_t a, uint32_t b) { return min(a + b, SAT); }  // a,b <= SAT
 __device__ __forceinline__ uint32_t smul(uint32_t a, uint32_t b) {
@@ -95,6 +95,9 @@ constexpr int MAXU = 8;    // accelerator units (all accelerators of the set)
 constexpr int MAXX = 32;   // executors
 constexpr int MAXCB = 64;  // callbacks
 constexpr uint32_t REC_WIDE_OK = 1u;  // Record::hflags
+constexpr uint64_t LIMW = 1ull << 48;   // every input time must be < LIMW (else PAAM_SET_ERANGE); times >= LIM go
+                                        // to the exact u64 path (wide.cu)
+constexpr int32_t REC_STATUS_WIDE = 0x100;  // internal status: handed over to wide.cu
 
 struct __align__(16) Record {
   // header
@@ -145,14 +148,18 @@ int fail_cuda(cudaError_t e, const char* what);
 int fail(int code, const char* what);
 
 // launchers (defined in the kernel files)
-int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status, cudaStream_t st);
+int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status, uint32_t* wide_list,
+                uint32_t* wide_count, cudaStream_t st);
 // ticket: one device counter (zeroed by the launcher on `st`) for dynamic work distribution
 int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags, uint32_t n_bins,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
                    cudaStream_t st, int32_t* out_fail = nullptr);
 // §8(a) steps 2-6 in one kernel (fused.cu): no record is written
-int launch_fused(const paam_batch* b, int32_t* status, uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins,
-                 cudaStream_t st);
+int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
+                 uint8_t* out_sched, int64_t* out_bins, cudaStream_t st);
+// the exact u64 path over the sets listed by the u32 kernels (wide.cu); out_fail: admission decisions
+int launch_wide(const paam_batch* b, const uint32_t* list, const uint32_t* count, int32_t* status, uint64_t* out_wcrt,
+                uint8_t* out_sched, int64_t* out_bins, int32_t* out_fail, cudaStream_t st);
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
                     uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st);
 #endif

@@ -266,7 +266,8 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
 #define FUSED_MINB 4  // 4 blocks of 8 warps (7 KB of shared memory per warp): 32 warps, 64 registers
 #endif
 __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
-    fused_kernel(paam_batch b, int32_t* __restrict__ status_out, uint64_t* __restrict__ out_wcrt,
+    fused_kernel(paam_batch b, uint32_t* __restrict__ wide_list, uint32_t* __restrict__ wide_count,
+                 int32_t* __restrict__ status_out, uint64_t* __restrict__ out_wcrt,
                  uint8_t* __restrict__ out_sched, int64_t* __restrict__ out_bins) {
 #ifdef PAAM_WARP_EMU
   __shared__ FSmem smem[FW];
@@ -322,9 +323,11 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     if (st == PAAM_SET_OK) {
       // ---- load + validate (as pack.cu) ---------------------------------------------------------------
       bool erange = false, edang = false, eaccel = false, eshape = false, edup = false, edl = false, ecore = false;
+      bool wide = false;  // a time in [2^31 - 1, 2^48) ns: the set goes to the u64 path
       if (lane < (int)nch) {
         const uint64_t T64 = b.chain_T[c0 + lane], D64 = b.chain_D[c0 + lane];
-        erange |= (T64 == 0 || T64 >= LIM || D64 >= LIM);
+        erange |= (T64 == 0 || T64 >= LIMW || D64 >= LIMW);
+        wide |= (T64 >= LIM || D64 >= LIM);  // exact only on the u64 path (wide.cu)
         T = (uint32_t)min(T64, (uint64_t)SAT);
         D = (uint32_t)min(D64, (uint64_t)SAT);
         prio = b.chain_prio[c0 + lane];
@@ -338,7 +341,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       if (lane < (int)nac) {
         const uint32_t n = b.accel_buckets[a0 + lane], u = b.accel_units[a0 + lane];
         const uint64_t e = b.accel_eps[a0 + lane], kp = b.accel_kappa[a0 + lane];
-        erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIM || kp >= LIM);
+        erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIMW || kp >= LIMW);
+        wide |= (e >= LIM || kp >= LIM);
         s.aN[lane] = n;
         s.aUnits[lane] = u;
         s.aEps[lane] = (uint32_t)min(e, (uint64_t)SAT);
@@ -371,7 +375,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       for (uint32_t i = lane; i < nseg; i += 32) {
         const uint64_t w = b.seg_wcet[sg0 + i];
         const uint32_t kind = b.seg_kind[sg0 + i], a = b.seg_accel[sg0 + i], u = b.seg_unit[sg0 + i];
-        erange |= (w >= LIM);
+        erange |= (w >= LIMW);
+        wide |= (w >= LIM);
         eshape |= (kind > 1) || (w == 0);
         if (kind == 1) {
           if (a >= nac) eaccel = true;
@@ -466,6 +471,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       erange |= (n_aseg > MAXA) || (n_unit > MAXU);
       if (__any_sync(FULL, malformed)) st = PAAM_SET_EDANGLING;
       else if (__any_sync(FULL, erange)) st = PAAM_SET_ERANGE;
+      else if (__any_sync(FULL, wide)) st = REC_STATUS_WIDE;  // handed over: wide.cu validates and analyses it
       else if (__any_sync(FULL, edang)) st = PAAM_SET_EDANGLING;
       else if (__any_sync(FULL, eaccel)) st = PAAM_SET_EACCEL;
       else if (__any_sync(FULL, eshape)) st = PAAM_SET_ESHAPE;
@@ -475,9 +481,13 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       else if (__any_sync(FULL, ecore)) st = PAAM_SET_ECORE;
     }
     if (!st2) { pcb = b.chain_cb_off[pc]; st2 = true; }
-    if (lane == 0 && status_out) status_out[set] = st;
+    const bool handed = st == REC_STATUS_WIDE;  // every output of a handed-over set is wide_kernel's
+    if (lane == 0 && handed) wide_list[atomicAdd(wide_count, 1u)] = set;
+    if (lane == 0 && status_out && !handed) status_out[set] = st;
     uint32_t sched = 0;
-    if (st != PAAM_SET_OK) {
+    if (handed) {
+      if (!st3) psg = b.cb_seg_off[pcb];
+    } else if (st != PAAM_SET_OK) {
       if (out_wcrt)
         #pragma unroll 1
         for (uint32_t i = lane; i < nch; i += 32) out_wcrt[c0 + i] = UNS;
@@ -799,7 +809,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         sched = __all_sync(FULL, ok) ? 1u : 0u;
       }
     }
-    if (lane == 0) {
+    if (lane == 0 && !handed) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
       if (out_bins && bin_ok) {
         if (blk_bins) {
@@ -825,7 +835,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
 }  // namespace
 
 #ifndef PAAM_WARP_EMU
-int launch_fused(const paam_batch* b, int32_t* status, uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins,
+int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
+                 uint8_t* out_sched, int64_t* out_bins,
                  cudaStream_t st) {
   if (b->n_sets == 0) return PAAM_OK;
   int dev = 0, sms = 148, per_sm = 1;
@@ -839,7 +850,7 @@ int launch_fused(const paam_batch* b, int32_t* status, uint64_t* out_wcrt, uint8
   const uint32_t need = (b->n_sets + FW - 1) / FW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  fused_kernel<<<grid, FW * 32, SMEM, st>>>(*b, status, out_wcrt, out_sched, out_bins);
+  fused_kernel<<<grid, FW * 32, SMEM, st>>>(*b, wide_list, wide_count, status, out_wcrt, out_sched, out_bins);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "fused_kernel launch");

@@ -535,8 +535,8 @@ extern "C" void paam_raw_free(paam_raw* raw) {
 struct paam_sweeper {
   uint32_t chunk;
   paam_raw raw[2];          // capacity-laid-out raw batches (ping-pong)
-  paam::Record* rec[2];     // packed records of the chunk being analysed
-  unsigned int* tickets;    // analyze work counters, one per buffer
+  uint32_t* wide[2];        // sets of the chunk handed over to the u64 path (wide.cu), one list per buffer
+  unsigned int* tickets;    // their counts, one per buffer
   cudaStream_t sg, sa;      // generation / pack + analysis
   cudaEvent_t start, gen_done[2], ana_done[2], join[2];
   int device;
@@ -549,7 +549,10 @@ extern "C" int paam_sweep_create(uint32_t chunk, paam_sweeper** out) {
   if (!h) return fail(PAAM_ENOMEM, "paam_sweep_create: host allocation");
   h->chunk = chunk;
   cudaError_t e = cudaGetDevice(&h->device);
-  for (int i = 0; i < 2; i++) h->raw[i].device = h->device;
+  for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+    h->raw[i].device = h->device;
+    e = cudaMalloc((void**)&h->wide[i], sizeof(uint32_t) * (size_t)chunk);
+  }
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->tickets, sizeof(unsigned int) * 2);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sg, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sa, cudaStreamNonBlocking);
@@ -591,8 +594,12 @@ extern "C" int paam_sweep(paam_sweeper* h, const paam_gen_params* params, uint64
     if (int rc = generate_into(&h->raw[bi], p, seed, first_index + lo, cnt, comm_cost, flags, h->sg, h->chunk)) return rc;
     cudaEventRecord(h->gen_done[bi], h->sg);
     cudaStreamWaitEvent(h->sa, h->gen_done[bi], 0);
-    if (int rc = launch_fused(&h->raw[bi].b, nullptr, nullptr, out_sched ? out_sched + lo : nullptr,
-                              p.n_bins ? out_bins : nullptr, h->sa))  // steps 2-6, records on chip
+    cudaMemsetAsync(h->tickets + bi, 0, sizeof(unsigned int), h->sa);
+    if (int rc = launch_fused(&h->raw[bi].b, h->wide[bi], h->tickets + bi, nullptr, nullptr,
+                              out_sched ? out_sched + lo : nullptr, p.n_bins ? out_bins : nullptr, h->sa))  // steps 2-6
+      return rc;
+    if (int rc = launch_wide(&h->raw[bi].b, h->wide[bi], h->tickets + bi, nullptr, nullptr,
+                             out_sched ? out_sched + lo : nullptr, p.n_bins ? out_bins : nullptr, nullptr, h->sa))
       return rc;
     cudaEventRecord(h->ana_done[bi], h->sa);
   }
@@ -611,7 +618,7 @@ extern "C" void paam_sweep_free(paam_sweeper* h) {
   for (int i = 0; i < 2; i++) {
     if (h->raw[i].buf) cudaFree(h->raw[i].buf);
     if (h->raw[i].scr) cudaFree(h->raw[i].scr);
-    if (h->rec[i]) cudaFree(h->rec[i]);
+    if (h->wide[i]) cudaFree(h->wide[i]);
   }
   if (h->tickets) cudaFree(h->tickets);
   if (h->sg) cudaStreamDestroy(h->sg);

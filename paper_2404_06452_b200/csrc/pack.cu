@@ -131,7 +131,9 @@ __device__ PAAM_COLD void wfd_units(Scratch& s, uint32_t nac, uint32_t ncb, uint
 #define PACK_MINB 8
 #endif
 __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch b, Record* __restrict__ recs,
-                                                          int32_t* __restrict__ status_out) {
+                                                          int32_t* __restrict__ status_out,
+                                                          uint32_t* __restrict__ wide_list,
+                                                          uint32_t* __restrict__ wide_count) {
   __shared__ Scratch smem[WARPS];
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
@@ -177,9 +179,11 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     if (st == PAAM_SET_OK) {
       // ---- load: chains (lane), accelerators (lane), executors (lane) ---------------------------
       bool erange = false, edang = false, eaccel = false, eshape = false, edup = false, edl = false, ecore = false;
+      bool wide = false;  // a time in [2^31 - 1, 2^48) ns: the set goes to the u64 path (wide.cu)
       if (lane < nch) {
         const uint64_t T64 = b.chain_T[c0 + lane], D64 = b.chain_D[c0 + lane];
-        erange |= (T64 == 0 || T64 >= LIM || D64 >= LIM);
+        erange |= (T64 == 0 || T64 >= LIMW || D64 >= LIMW);
+        wide |= (T64 >= LIM || D64 >= LIM);
         T = (uint32_t)min(T64, (uint64_t)SAT);
         D = (uint32_t)min(D64, (uint64_t)SAT);
         prio = b.chain_prio[c0 + lane];
@@ -193,7 +197,8 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       if (lane < nac) {
         const uint32_t n = b.accel_buckets[a0 + lane], u = b.accel_units[a0 + lane];
         const uint64_t e = b.accel_eps[a0 + lane], kp = b.accel_kappa[a0 + lane];
-        erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIM || kp >= LIM);
+        erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIMW || kp >= LIMW);
+        wide |= (e >= LIM || kp >= LIM);
         s.aN[lane] = n;
         s.aUnits[lane] = u;
         s.aEps[lane] = (uint32_t)min(e, (uint64_t)SAT);
@@ -232,7 +237,8 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       for (uint32_t i = lane; i < nseg; i += 32) {
         const uint64_t w = b.seg_wcet[sg0 + i];
         const uint32_t kind = b.seg_kind[sg0 + i], a = b.seg_accel[sg0 + i], u = b.seg_unit[sg0 + i];
-        erange |= (w >= LIM);
+        erange |= (w >= LIMW);
+        wide |= (w >= LIM);
         eshape |= (kind > 1) || (w == 0);
         if (kind == 1) {
           if (a >= nac) eaccel = true;
@@ -324,6 +330,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       // reference: it is reported before the checks of the segments the callbacks no longer cover)
       if (__any_sync(FULL, malformed)) st = PAAM_SET_EDANGLING;
       else if (__any_sync(FULL, erange)) st = PAAM_SET_ERANGE;
+      else if (__any_sync(FULL, wide)) st = REC_STATUS_WIDE;  // handed over: wide.cu validates and analyses it
       else if (__any_sync(FULL, edang)) st = PAAM_SET_EDANGLING;
       else if (__any_sync(FULL, eaccel)) st = PAAM_SET_EACCEL;
       else if (__any_sync(FULL, eshape)) st = PAAM_SET_ESHAPE;
@@ -339,7 +346,8 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       r->chain_base = c0;
       r->bin = (b.set_bin && bin >= b.n_bins) ? 0xffffffffu : bin;  // analyze skips an out-of-range bin
       r->n_out = nch;
-      if (status_out) status_out[set] = st;
+      if (status_out && st != REC_STATUS_WIDE) status_out[set] = st;
+      if (st == REC_STATUS_WIDE) wide_list[atomicAdd(wide_count, 1u)] = set;
       if (st != PAAM_SET_OK) { r->n_chain = 0; r->n_sub = 0; r->n_aseg = 0; r->n_unit = 0; }
     }
     if (st != PAAM_SET_OK) {
@@ -595,7 +603,8 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
 }  // namespace
 
 #ifndef PAAM_WARP_EMU
-int launch_pack(const paam_batch* b, Record* rec, int32_t* status, cudaStream_t st) {
+int launch_pack(const paam_batch* b, Record* rec, int32_t* status, uint32_t* wide_list, uint32_t* wide_count,
+                cudaStream_t st) {
   if (b->n_sets == 0) return PAAM_OK;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -605,7 +614,7 @@ int launch_pack(const paam_batch* b, Record* rec, int32_t* status, cudaStream_t 
   const uint32_t need = (b->n_sets + WARPS - 1) / WARPS;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  pack_kernel<<<grid, WARPS * 32, 0, st>>>(*b, rec, status);
+  pack_kernel<<<grid, WARPS * 32, 0, st>>>(*b, rec, status, wide_list, wide_count);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "pack_kernel launch");

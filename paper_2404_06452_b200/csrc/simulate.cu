@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         if (o.drops) o.drops[c0 + i] = 0;
       }
       if (lane == 0 && out_digest) out_digest[set] = 0;
-      if (lane == 0 && o.status) o.status[set] = PAAM_SIM_INVALID;
+      if (lane == 0 && o.status) o.status[set] = rec.status == REC_STATUS_WIDE ? PAAM_SIM_WIDE : PAAM_SIM_INVALID;
       continue;
     }
     const uint32_t x0 = b.set_exec_off[set], nex = b.set_exec_off[set + 1] - x0;

@@ -65,7 +65,7 @@ class PaamSimOut(ctypes.Structure):
                [("max_witness", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
 
 
-PAAM_SIM_OK, PAAM_SIM_INVALID, PAAM_SIM_BACKLOG, PAAM_SIM_STEPCAP = 0, 1, 2, 3
+PAAM_SIM_OK, PAAM_SIM_INVALID, PAAM_SIM_BACKLOG, PAAM_SIM_STEPCAP, PAAM_SIM_WIDE = 0, 1, 2, 3, 4
 PAAM_SIM_QCAP = 4
 
 

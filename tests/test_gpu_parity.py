@@ -379,3 +379,74 @@ def test_host_pipeline_rejects_non_monotone_offsets():
     sets = paam.Sets(hb)
     with pytest.raises(paam.PaamError, match="invalid argument"):
         sets.pack_analyze(paam.Batch.from_host(bad), None, None, None)
+
+
+def _scaled(s, f):
+    for ch in s.chains:
+        ch.T *= f
+        ch.D *= f
+        for c in ch.cbs:
+            for g in c.segs:
+                g.wcet *= f
+    s.accels = [(bk, u, sc, e * f, k * f) for (bk, u, sc, e, k) in s.accels]
+    return s
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_wide_time_sets_take_the_u64_path(flags):
+    """Sets with a time >= 2^31 - 1 ns (u64 boundary; A14: < 2^48) are handed over by the u32
+    kernels to wide_kernel and analysed exactly: mixed with ordinary sets, every WCRT, verdict, status
+    and bin equals the oracle's, on the split and the fused path; App. B x 1000 gives 11 s / 40 s."""
+    rng = random.Random(900 + flags)
+    systems = []
+    for i in range(1500):
+        s = random_small_system(rng, max_chains=6, tmax=200)
+        if i % 2:
+            s = _scaled(s, 1 << 26)
+        systems.append(mutate_invalid(s, rng) if i % 3 == 0 else s)
+    for i, s in enumerate(systems):
+        s.bin = i % 5
+    b = flatten(systems, comm_cost=3 << 20, flags=flags, n_bins=5)
+    assert (b["chain_T"] >= (1 << 31) - 1).sum() > 500
+    assert_same(b, gpu_host_path(b))
+    assert_same(b, gpu_device_path(b), fused_too=False)
+    app = app_b_two_chains()
+    gw, gsch, _, _ = gpu_host_path(flatten([_scaled(app, 1000)], comm_cost=0))
+    assert gw.tolist() == [x * 1000 for x in GOLD["two_chains_one_executor"]["R"]]
+
+
+def test_wide_time_sets_admission_and_des_status():
+    """paam_admit decides wide sets on the u64 path too; the DES reports them PAAM_SIM_WIDE (it computes in
+    32-bit time distances) and simulates the others."""
+    rng = random.Random(77)
+    systems = [random_small_system(rng, max_chains=5, tmax=200) for _ in range(200)]
+    systems = [_scaled(s, 1 << 26) if i % 2 else s for i, s in enumerate(systems)]
+    b = flatten(systems, comm_cost=1)
+    ow, osch, ost, _ = O.analyze(b, nthreads=NPROC)
+    hb = paam.Batch.from_host(b)
+    sets = paam.Sets(hb)
+    dec = torch.full((len(systems),), -9, dtype=torch.int32, device="cuda")
+    sets.admit(dec)
+    st = torch.full((len(systems),), -9, dtype=torch.int32, device="cuda")
+    resp = torch.zeros(max(hb.c.n_chains, 1), dtype=torch.int64, device="cuda")
+    sets.simulate(400, 1, resp, out_status=st)
+    torch.cuda.synchronize()
+    d = dec.cpu().numpy()
+    off = b["set_chain_off"]
+    for i in range(len(systems)):
+        c0, c1 = int(off[i]), int(off[i + 1])
+        if ost[i] != 0:
+            assert d[i] == -2 - ost[i]
+        elif osch[i]:
+            assert d[i] == -1
+        else:  # the highest-priority CRITICAL chain with R* > D
+            bad = [c for c in range(c1 - c0) if b["chain_class"][c0 + c] == 0 and (ow[c0 + c] == O.UNSCHED or ow[c0 + c] > b["chain_D"][c0 + c])]
+            assert d[i] == max(bad, key=lambda c: b["chain_prio"][c0 + c])
+    s = st.cpu().numpy()
+    lim = (1 << 31) - 1
+    wide = np.array([any(ch.T >= lim or ch.D >= lim or any(g.wcet >= lim for c in ch.cbs for g in c.segs)
+                         for ch in x.chains) or any(e >= lim or k >= lim for (_b, _u, _c, e, k) in x.accels)
+                     for x in systems])
+    assert wide.sum() > 50
+    assert (s[wide] == paam.PAAM_SIM_WIDE).all()
+    assert (s[~wide] != paam.PAAM_SIM_WIDE).all()

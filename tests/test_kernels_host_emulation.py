@@ -38,7 +38,7 @@ def _build(asan):
     target = "libpaam_emu_asan.so" if asan else "libpaam_emu.so"
     flags = "-fsanitize=address,undefined -fno-omit-frame-pointer" if asan else ""
     cmd = (f"g++ -O1 -g -std=c++20 -fPIC -pthread -DPAAM_WARP_EMU {flags} -I../../include -shared -o {target} "
-           "emu_pack.cpp emu_analyze.cpp emu_simulate.cpp emu_fused.cpp")
+           "emu_pack.cpp emu_analyze.cpp emu_simulate.cpp emu_fused.cpp emu_wide.cpp")
     subprocess.run(cmd, shell=True, cwd=EMU, check=True)
     return target
 

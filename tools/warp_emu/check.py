@@ -16,11 +16,12 @@ from paper_2404_06452_b200.paam import Batch  # noqa  (only for the batch struct
 
 L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("PAAM_EMU_LIB", "libpaam_emu.so")))
 vp = ctypes.c_void_p
-L.emu_pack.argtypes = [vp, vp, vp]
+L.emu_pack.argtypes = [vp, vp, vp, vp, vp]
+L.emu_wide.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
 L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
 L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp]
 L.emu_record_bytes.restype = ctypes.c_uint32
-L.emu_fused.argtypes = [vp, vp, vp, vp, vp]
+L.emu_fused.argtypes = [vp, vp, vp, vp, vp, vp, vp]
 
 
 def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
@@ -28,30 +29,44 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     n = hb.n_sets
     rec = np.zeros((max(n, 1), L.emu_record_bytes()), np.uint8)
     st = np.zeros(max(n, 1), np.int32)
-    L.emu_pack(ctypes.addressof(hb.c), rec.ctypes.data, st.ctypes.data)
+    wl = np.zeros(max(n, 1), np.uint32)  # sets handed over to the u64 path (wide.cu)
+    wc = np.zeros(1, np.uint32)
+    L.emu_pack(ctypes.addressof(hb.c), rec.ctypes.data, st.ctypes.data, wl.ctypes.data, wc.ctypes.data)
+    L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, st.ctypes.data, None, None, None, None)
+    wide = lambda w_, s_, b_: L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, None, w_, s_, b_, None)
     nch = max(hb.c.n_chains, 1)
     w = np.zeros(nch, np.uint64)
     sc = np.zeros(max(n, 1), np.uint8)
     bins = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
     L.emu_analyze(rec.ctypes.data, n, hb.c.comm_cost, hb.c.flags, hb.c.n_bins if hb.c.set_bin else 0,
                   w.ctypes.data, sc.ctypes.data, bins.ctypes.data if hb.c.set_bin else None)
+    wide(w.ctypes.data, sc.ctypes.data, bins.ctypes.data if hb.c.set_bin else None)
     out = dict(status=st[:n], wcrt=w[:hb.c.n_chains], sched=sc[:n], bins=bins[:2 * hb.c.n_bins])
     # PAAM_FLAG_VERDICT_ONLY (0x4): no WCRTs, early exit at the first CRITICAL miss; same verdicts / bins
     sv = np.zeros(max(n, 1), np.uint8)
     bv = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
     L.emu_analyze(rec.ctypes.data, n, hb.c.comm_cost, hb.c.flags | 0x4, hb.c.n_bins if hb.c.set_bin else 0,
                   None, sv.ctypes.data, bv.ctypes.data if hb.c.set_bin else None)
+    wide(None, sv.ctypes.data, bv.ctypes.data if hb.c.set_bin else None)
     out.update(sched_v=sv[:n], bins_v=bv[:2 * hb.c.n_bins])
     # the fused kernel (paam_pack_analyze): full mode and verdict-only
     fst = np.full(max(n, 1), -9, np.int32)
     fw = np.zeros(nch, np.uint64)
     fs = np.zeros(max(n, 1), np.uint8)
     fb = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
-    L.emu_fused(ctypes.addressof(hb.c), fst.ctypes.data, fw.ctypes.data, fs.ctypes.data, fb.ctypes.data if hb.c.set_bin else None)
+    fl, fc = np.zeros(max(n, 1), np.uint32), np.zeros(1, np.uint32)
+    L.emu_fused(ctypes.addressof(hb.c), fl.ctypes.data, fc.ctypes.data, fst.ctypes.data, fw.ctypes.data, fs.ctypes.data,
+                fb.ctypes.data if hb.c.set_bin else None)
+    L.emu_wide(ctypes.addressof(hb.c), fl.ctypes.data, fc.ctypes.data, fst.ctypes.data, fw.ctypes.data, fs.ctypes.data,
+               fb.ctypes.data if hb.c.set_bin else None, None)
     vb = Batch.from_host(dict(batch, flags=batch.get("flags", 0) | 0x4))
     fsv = np.zeros(max(n, 1), np.uint8)
     fbv = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
-    L.emu_fused(ctypes.addressof(vb.c), None, None, fsv.ctypes.data, fbv.ctypes.data if hb.c.set_bin else None)
+    fc[0] = 0
+    L.emu_fused(ctypes.addressof(vb.c), fl.ctypes.data, fc.ctypes.data, None, None, fsv.ctypes.data,
+                fbv.ctypes.data if hb.c.set_bin else None)
+    L.emu_wide(ctypes.addressof(vb.c), fl.ctypes.data, fc.ctypes.data, None, None, fsv.ctypes.data,
+               fbv.ctypes.data if hb.c.set_bin else None, None)
     out.update(f_status=fst[:n], f_wcrt=fw[:hb.c.n_chains], f_sched=fs[:n], f_bins=fb[:2 * hb.c.n_bins],
                f_sched_v=fsv[:n], f_bins_v=fbv[:2 * hb.c.n_bins])
     if horizon is not None:

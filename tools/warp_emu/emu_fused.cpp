@@ -1,5 +1,6 @@
 #include "../../paper_2404_06452_b200/csrc/fused.cu"
-extern "C" void emu_fused(const paam_batch* b, int32_t* status, uint64_t* wcrt, uint8_t* sched, int64_t* bins) {
+extern "C" void emu_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* wcrt,
+                          uint8_t* sched, int64_t* bins) {
   gridDim.x = 1;
-  emu::launch_block(0, paam::FW * 32, [&]() { paam::fused_kernel(*b, status, wcrt, sched, bins); });
+  emu::launch_block(0, paam::FW * 32, [&]() { paam::fused_kernel(*b, wide_list, wide_count, status, wcrt, sched, bins); });
 }

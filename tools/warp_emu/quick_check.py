@@ -19,3 +19,19 @@ ok &= compare(generate_host(config2_params(cpu_only_frac=0.25), 2, 0, 400), labe
 ok &= compare(generate_host(make_params(exec_mode=1, n_exec=4, xexec_frac=0.5, spin_frac=0.5, cpu_only_frac=0.2), 6, 0, 300), label="modeB")
 ok &= compare(generate_host(make_params(accels=((6, 3, 391000, 130000), (1, 2, 391000, 0))), 3, 0, 300), label="5 units")
 print("ALL", ok)
+# wide sets: random systems with every time scaled past 2^31 ns, mixed with ordinary ones
+def scaled(s, f):
+    for ch in s.chains:
+        ch.T *= f; ch.D *= f
+        for c in ch.cbs:
+            for g in c.segs: g.wcet *= f
+    s.accels = [(bk, u, sc, e * f, k * f) for (bk, u, sc, e, k) in s.accels]
+    return s
+rng2 = random.Random(5)
+mix = []
+for i in range(300):
+    s = random_small_system(rng2, max_chains=6, tmax=200)
+    mix.append(scaled(s, 1 << 26) if i % 2 else s)
+for fl in (0, 1, 2):
+    ok &= compare(flatten(mix, comm_cost=3 << 20, flags=fl), label=f"wide mix flags {fl}")
+print("ALL2", ok)
