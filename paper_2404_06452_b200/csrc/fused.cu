@@ -96,6 +96,9 @@ struct FSmem {
   };
 };
 
+#ifdef PAAM_EMU_STATS
+unsigned long long emu_stats[8];  // debugging statistics of the host emulation (never on the device)
+#endif
 __constant__ uint32_t kInv16F[33] = {0u, 65537u, 32769u, 21846u, 16385u, 13108u, 10923u, 9363u, 8193u, 7282u, 6554u, 5958u, 5462u, 5042u, 4682u, 4370u, 4097u, 3856u, 3641u, 3450u, 3277u, 3121u, 2979u, 2850u, 2731u, 2622u, 2521u, 2428u, 2341u, 2260u, 2185u, 2115u, 2049u};
 
 __device__ __forceinline__ uint32_t f_scan_sat_incl(uint32_t v, int lane) {
@@ -210,6 +213,9 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
     const uint4 p = s.pTab[i];
     if (p.x >= R) break;
     m &= m - 1;
+#ifdef PAAM_EMU_STATS
+    atomicAdd(&emu_stats[3], 1ull);  // Lemma-3 floor terms
+#endif
     const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
     uint32_t wu = p.w;
     if (wsel) {
@@ -746,9 +752,16 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       __syncwarp();
       bool dirty = act;
       bool miss = false;
+#ifdef PAAM_EMU_STATS
+      if (lane == 0) emu_stats[0]++;  // sets
+#endif
       #pragma unroll 1
       for (;;) {
         uint32_t F = R, nH = Hst;
+#ifdef PAAM_EMU_STATS
+        if (lane == 0) emu_stats[1]++;  // warp iterates
+        if (dirty) atomicAdd(&emu_stats[2], 1ull);  // lane evaluations
+#endif
         if (dirty) {
           if (wide) f_eval<true>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
           else f_eval<false>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
