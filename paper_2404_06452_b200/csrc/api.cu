@@ -22,9 +22,8 @@ struct paam_sets {
   cudaStream_t side[3];  // internal streams of paam_pack_analyze: pack, analyze, H2D copies (created on first use)
   cudaEvent_t ev[17], evc[8];  // evc: chunk copies done
   unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18,
-                          // 20: number of wide sets listed (wide.cu), 21-23: DES tickets and list count
+                          // 20: number of wide sets listed (wide.cu)
   uint32_t* wide_list;    // [cap] the sets handed over to the u64 path by the last pack / fused launch
-  uint32_t* des_list;     // [cap] DES: sets with more than 16 chains or executors (allocated on first use)
   int device;             // the CUDA device the handle lives on (made current by every call)
   bool rec_valid;         // rec holds the records of `dev` (false after the fused paam_pack_analyze, which writes
                           // none: the next paam_analyze / paam_admit / paam_simulate packs them first)
@@ -279,13 +278,8 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
   if (!o.witness) o.max_witness = 0;
   if (int rc = use_device(sets)) return rc;
   if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
-  paam_sets* ms = const_cast<paam_sets*>(sets);
-  if (!ms->des_list) {  // the sets the two-per-warp DES pass hands to the one-per-warp pass
-    const cudaError_t e = cudaMalloc((void**)&ms->des_list, sizeof(uint32_t) * (size_t)(ms->cap ? ms->cap : 1));
-    if (e != cudaSuccess) return fail_cuda(e, "paam_simulate: list cudaMalloc");
-  }
-  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, &o, ms->tickets + 21,
-                         ms->des_list, (cudaStream_t)stream);
+  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, &o,
+                         const_cast<paam_sets*>(sets)->tickets + 18, (cudaStream_t)stream);
 }
 
 extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
@@ -431,7 +425,6 @@ extern "C" void paam_free(paam_sets* sets) {
   if (sets->rec) cudaFree(sets->rec);
   if (sets->tickets) cudaFree(sets->tickets);
   if (sets->wide_list) cudaFree(sets->wide_list);
-  if (sets->des_list) cudaFree(sets->des_list);
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
   if (sets->side[0]) {

@@ -1,13 +1,8 @@
-// simulate.cu -- §8(a) steps 7-8: discrete-event simulation of PAAM arbitration, one lane group per set.
+// simulate.cu -- §8(a) steps 7-8: discrete-event simulation of PAAM arbitration, one warp per set.
 //
 // Semantics: DESIGN.md App. A (rules D1-D17), derived from the paper's execution model
 // (PiCAS executors P:135-136, fixed-priority cores P:136, PAAM server rules R1-R4 P:366-373,
-// eps / kappa overheads P:374, bucket FIFO on equal priority P:320).
-// Lane groups: a set is simulated by a group of G lanes.  G = 16 (two sets per warp, in lock-step)
-// takes every set with at most 16 chains and 16 executors -- all of config 3 -- and G = 32 (one set
-// per warp) the larger ones, which the G = 16 launch lists for it.  Both groups of a warp run the
-// same instruction stream: every loop runs while either group needs it, each group's work predicated
-// by its own condition, and every collective is a group-masked one.  Lane ownership within a group:
+// eps / kappa overheads P:374, bucket FIFO on equal priority P:320).  Lane ownership:
 //   lane k  = chain of rank k (k = 0 highest priority): its <= QCAP live instances, release
 //             schedule, statistics.  D14 queues every release of a chain (an unbounded backlog,
 //             S:311); a release that finds all QCAP slots live stops the set's run and reports
@@ -22,12 +17,11 @@
 // when something is provably left for it (zero-length work due now, an executor that just got its
 // core with ready work), so every skipped pass would have been a no-op.  Each sub-phase is
 // lane-parallel over the entities it touches (they touch disjoint state; shared statistics use
-// shared-memory atomics); "best" choices are group reductions over rank-ordered lanes, so the
-// highest priority is the lowest set bit of a ballot.  Time then jumps to the group-min next event.
-// When a group's set ends, the group takes the next set (its staging runs while the other group
-// waits, a short stretch against a whole simulation).  Instance slots are packed one byte per slot
-// per chain (byte-compare scans).  The event digest is a sum of per-record FNV-1a-64 hashes (order
-// independent), reduced at the end, computed only when requested.
+// shared-memory atomics); "best" choices are warp reductions over rank-ordered lanes, so the
+// highest priority is the lowest set bit of a ballot.  Time then jumps to the warp-min next event.
+// Instance slots are packed one byte per slot per chain (byte-compare scans).  The event digest is
+// a sum of per-record FNV-1a-64 hashes (order independent), reduced at the end, computed only when
+// requested.
 #include "../../gen/paam_gen.h"
 #include "common.cuh"
 
@@ -72,44 +66,41 @@ __device__ __forceinline__ uint32_t rep4(uint32_t v) { return v * 0x01010101u; }
 __device__ __forceinline__ uint32_t slots_eq(uint32_t w, uint32_t v) { return __vcmpeq4(w, rep4(v)) & 0x01010101u; }
 __device__ __forceinline__ uint32_t slot_of(uint32_t m) { return (uint32_t)(__ffs(m) - 1) >> 3; }
 
-// Per-set shared state of a G-lane group: chains and executors are lane-indexed (<= G of each).
-template <int G>
 struct DesSmem {
   // static (per set)
-  uint32_t cT[G], cD[G];
-  uint64_t cPhase[G];
-  uint8_t cCls[G], cLocal[G], cCb0[G], cNcb[G];
+  uint32_t cT[MAXC], cD[MAXC];
+  uint64_t cPhase[MAXC];
+  uint8_t cCls[MAXC], cLocal[MAXC], cCb0[MAXC], cNcb[MAXC];
   uint8_t bExec[MAXCB], bNseg[MAXCB];
   uint8_t bSeg0[MAXCB];
   uint32_t gW[MAXG];
   uint8_t gKind[MAXG], gUnit[MAXG], gBkt[MAXG];
-  uint32_t xSameCore[G];
-  uint8_t xWait[G], xcanon[G];
-  uint32_t ubase[4];
+  uint32_t xSameCore[MAXX];
+  uint8_t xWait[MAXX];
   uint32_t uEps[MAXU], uKap[MAXU], uN[MAXU];
   // dynamic
   union {
-    InstWide iw[G][QCAP];
+    InstWide iw[MAXC][QCAP];
     struct {  // WFD scratch of the static staging (dead before the dynamic state exists)
       uint64_t wu[MAXCB];
       uint8_t wo[MAXCB], wn[MAXCB], wc[MAXCB];
     } wfd;
   };
-  uint32_t iState[G], iCb[G], iWUnit[G], iStarted[G];
+  uint32_t iState[MAXC], iCb[MAXC], iWUnit[MAXC], iStarted[MAXC];
   __device__ __forceinline__ InstRef ref(uint32_t c, uint32_t q) {
     InstWide& w = iw[c][q];
     return InstRef{byte_of(iState[c], q), byte_of(iCb[c], q), byte_of(iWUnit[c], q), byte_of(iStarted[c], q),
                    w.ready_at, w.k, w.seq, w.rem};
   }
-  uint32_t exRem[G];
-  uint64_t exTimer[G];
-  uint8_t exChain[G], exSlot[G], exSeg[G], exPhase[G];
+  uint32_t exRem[MAXX];
+  uint64_t exTimer[MAXX];
+  uint8_t exChain[MAXX], exSlot[MAXX], exSeg[MAXX], exPhase[MAXX];
   uint64_t unEnd[MAXU];
   uint32_t unRem[MAXU];
   uint8_t unState[MAXU], unChain[MAXU], unSlot[MAXU];
   uint32_t uQ[MAXU];  // requests queued on the unit (waiting, started or not; the running one included)
-  unsigned long long maxResp[G];
-  uint32_t cnt[G], miss[G];
+  unsigned long long maxResp[MAXC];
+  uint32_t cnt[MAXC], miss[MAXC];
 };
 
 // FNV-1a-64 of a 32-byte event record (D17) in two parts: the state after the record's 8-byte time
@@ -141,9 +132,14 @@ __device__ __forceinline__ uint64_t fnv_rest(uint64_t h, uint32_t kind, uint32_t
   return fnv_field(h, bk);
 }
 
-template <int G>
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
 struct Ctx {
-  DesSmem<G>& S;
+  DesSmem& S;
   uint64_t t, horizon, comm;
   uint64_t dig;  // this lane's partial digest
   bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
@@ -198,495 +194,428 @@ struct Ctx {
   }
 };
 
-#ifndef SIM_MINB16
-#define SIM_MINB16 6  // G = 16: two 4.3 KB sets per warp
+#ifndef SIM_MINB
+#define SIM_MINB 8  // measured: 8 blocks of 4 warps (64 registers) beat 6, 7 and 9
 #endif
-#ifndef SIM_MINB32
-#define SIM_MINB32 8  // G = 32: one 6.2 KB set per warp
-#endif
-template <int G>
-struct SimLB { static constexpr int minb = G == 16 ? SIM_MINB16 : SIM_MINB32; };
-
-// The G-lane group kernel.  Sets are taken one per atomic ticket per group (a set's cost varies by
-// orders of magnitude).  only != NULL: the sets to take are only[0 .. *only_count) (the G = 32 pass
-// over the sets the G = 16 pass listed in big_list, because they have more than 16 chains or executors).
-template <int G>
-__global__ void __launch_bounds__(SW * 32, SimLB<G>::minb)
-    simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, paam_sim_out o, unsigned int* __restrict__ ticket,
-                    const uint32_t* __restrict__ only, const uint32_t* __restrict__ only_count,
-                    uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
-  constexpr uint32_t GM = G == 32 ? FULL : (1u << G) - 1u;
+__global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
+                                                           uint64_t horizon, uint64_t seed, uint64_t first_index,
+                                                           uint32_t sim_flags, paam_sim_out o,
+                                                           unsigned int* __restrict__ ticket) {
   uint64_t* __restrict__ out_resp = o.resp;
   uint64_t* __restrict__ out_count = o.count;
   uint64_t* __restrict__ out_digest = o.digest;
   const uint64_t* __restrict__ bound = o.bound;
-  __shared__ DesSmem<G> smem[SW][32 / G];
-  const uint32_t lane = threadIdx.x & 31, grp = lane / G, gl = lane % G, goff = grp * G;
-  const uint32_t gmask = GM << goff;
-  const uint32_t ltg = (lanemask_lt() >> goff) & GM;  // lanes of the group below this one
-  DesSmem<G>& S = smem[threadIdx.x >> 5][grp];
-  // group collectives: every lane of the warp executes them (both groups in lock-step)
-  auto gballot = [&](bool p) -> uint32_t { return (__ballot_sync(FULL, p) >> goff) & GM; };
-  auto gany = [&](bool p) -> bool { return gballot(p) != 0u; };
-  auto gshfl = [&](uint32_t v, uint32_t src) -> uint32_t { return __shfl_sync(FULL, v, goff + src); };
-  const uint32_t total = only ? *only_count : n;
-  const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
+  __shared__ DesSmem smem[SW];
+  const uint32_t lane = threadIdx.x & 31;
+  DesSmem& S = smem[threadIdx.x >> 5];
+  // dynamic work distribution: a set's simulation cost varies by orders of magnitude (chains,
+  // periods, horizon), so warps take one set per atomic ticket instead of a fixed stride
+  auto next_set = [&]() {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  for (uint32_t set = next_set(); set < n; set = next_set()) {
+    const Record& rec = recs[set];
+    const uint32_t c0 = b.set_chain_off[set], c1 = b.set_chain_off[set + 1];
+    const uint32_t nch = c1 - c0;
+    if (rec.status != PAAM_SET_OK) {
+      for (uint32_t i = lane; i < nch; i += 32) {
+        if (out_resp) out_resp[c0 + i] = 0;
+        if (out_count) out_count[c0 + i] = 0;
+        if (o.misses) o.misses[c0 + i] = 0;
+        if (o.drops) o.drops[c0 + i] = 0;
+      }
+      if (lane == 0 && out_digest) out_digest[set] = 0;
+      if (lane == 0 && o.status) o.status[set] = rec.status == REC_STATUS_WIDE ? PAAM_SIM_WIDE : PAAM_SIM_INVALID;
+      continue;
+    }
+    const uint32_t x0 = b.set_exec_off[set], nex = b.set_exec_off[set + 1] - x0;
+    const uint32_t a0 = b.set_accel_off[set], nac = b.set_accel_off[set + 1] - a0;
+    const uint32_t cb0 = b.chain_cb_off[c0], ncb = b.chain_cb_off[c1] - cb0;
+    const uint32_t sg0 = b.cb_seg_off[cb0], nseg = b.cb_seg_off[cb0 + ncb] - sg0;
 
-  // per-group state (group-uniform values are held by every lane of the group)
-  bool live = false, done = false;
-  uint32_t set = 0, c0 = 0, nch = 0, nex = 0, n_unit = 0;
-  Ctx<G> C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr, 0};
-  uint32_t next_k = 0;          // lane = rank
-  uint64_t next_rel = NONE64;   // release time of instance next_k (D2)
-  uint32_t seq = 0;             // group-uniform
-  bool on_core = false;         // lane = canonical executor
-  uint32_t drops = 0;
-  uint64_t steps = 0;
-  int32_t stop = PAAM_SIM_OK;   // group-uniform: why the run stopped early (PAAM_SIM_BACKLOG / _STEPCAP)
-  bool backlog = false;         // lane = chain: a release found every instance slot live
-  bool is_chain = false, is_exec = false, is_unit = false;
-
-  for (;;) {
-    // ===================== groups without a set take the next one =====================
-    const bool need = !live && !done;
-    if (__any_sync(FULL, need)) {
-      uint32_t tk = 0;
-      if (need && gl == 0) tk = atomicAdd(ticket, 1u);
-      tk = gshfl(tk, 0);
-      bool stg = false;
-      if (need) {
-        if (tk >= total) {
-          done = true;
-        } else {
-          set = only ? only[tk] : tk;
-          const Record& rec = recs[set];
-          c0 = b.set_chain_off[set];
-          nch = b.set_chain_off[set + 1] - c0;
-          nex = b.set_exec_off[set + 1] - b.set_exec_off[set];
-          if (rec.status != PAAM_SET_OK) {  // not simulated: zero outputs, the reason in status
-            for (uint32_t i = gl; i < nch; i += G) {
-              if (out_resp) out_resp[c0 + i] = 0;
-              if (out_count) out_count[c0 + i] = 0;
-              if (o.misses) o.misses[c0 + i] = 0;
-              if (o.drops) o.drops[c0 + i] = 0;
-            }
-            if (gl == 0 && out_digest) out_digest[set] = 0;
-            if (gl == 0 && o.status) o.status[set] = rec.status == REC_STATUS_WIDE ? PAAM_SIM_WIDE : PAAM_SIM_INVALID;
-          } else if (nch > (uint32_t)G || nex > (uint32_t)G) {  // for the G = 32 pass
-            if (gl == 0) big_list[atomicAdd(big_count, 1u)] = set;
-          } else {
-            stg = true;
-            n_unit = rec.n_unit;
-          }
-        }
+    // ---- static staging ----------------------------------------------------------------------------
+    // chains: rank = number of higher priorities
+    uint32_t my_prio = lane < nch ? b.chain_prio[c0 + lane] : 0u, rank = 0;
+    for (uint32_t d = 0; d < nch; d++) rank += (__shfl_sync(FULL, my_prio, d) > my_prio);
+    uint32_t chain_of_rank_cb0 = 0;
+    if (lane < nch) {
+      const uint64_t T = b.chain_T[c0 + lane];
+      S.cT[rank] = (uint32_t)T;
+      S.cD[rank] = (uint32_t)b.chain_D[c0 + lane];
+      S.cCls[rank] = b.chain_class[c0 + lane];
+      S.cLocal[rank] = (uint8_t)lane;
+      chain_of_rank_cb0 = b.chain_cb_off[c0 + lane] - cb0;
+      S.cCb0[rank] = (uint8_t)chain_of_rank_cb0;
+      S.cNcb[rank] = (uint8_t)(b.chain_cb_off[c0 + lane + 1] - cb0 - chain_of_rank_cb0);
+      S.cPhase[rank] = pg_phase(seed, first_index + set, lane, T);  // D2
+    }
+    // executors: canonical order (core asc, process priority desc)
+    uint32_t xcore = lane < nex ? b.exec_core[x0 + lane] : 0x100u + lane;
+    uint32_t xprio = lane < nex ? b.exec_prio[x0 + lane] : 0u;
+    uint32_t xpos = 0;
+    for (uint32_t y = 0; y < nex; y++) {
+      const uint32_t cy = __shfl_sync(FULL, xcore, y), py = __shfl_sync(FULL, xprio, y);
+      xpos += (cy < xcore) || (cy == xcore && py > xprio);
+    }
+    __shared__ uint8_t xcanon_all[SW][MAXX];
+    uint8_t* xcanon = xcanon_all[threadIdx.x >> 5];
+    if (lane < nex) {
+      xcanon[lane] = (uint8_t)xpos;
+      S.xWait[xpos] = b.exec_wait[x0 + lane];
+    }
+    {
+      const uint32_t same = __match_any_sync(FULL, xcore);
+      // translate the same-core lane mask to canonical positions
+      uint32_t m = 0;
+      for (uint32_t y = 0; y < nex; y++) {
+        const uint32_t py = __shfl_sync(FULL, xpos, y);  // every lane shuffles (no divergent shuffle)
+        if ((same >> y) & 1u) m |= 1u << py;
       }
-      // ---- static staging (groups with stg; the other group's lanes are predicated off) ------------
-      const uint32_t x0 = stg ? b.set_exec_off[set] : 0u;
-      const uint32_t a0 = stg ? b.set_accel_off[set] : 0u, nac = stg ? b.set_accel_off[set + 1] - a0 : 0u;
-      const uint32_t cb0 = stg ? b.chain_cb_off[c0] : 0u, ncb = stg ? b.chain_cb_off[c0 + nch] - cb0 : 0u;
-      const uint32_t sg0 = stg ? b.cb_seg_off[cb0] : 0u, nseg = stg ? b.cb_seg_off[cb0 + ncb] - sg0 : 0u;
-      // chains: rank = number of higher priorities
-      const bool cl = stg && gl < nch;
-      const uint32_t my_prio = cl ? b.chain_prio[c0 + gl] : 0u;
-      uint32_t rank = 0;
-      for (uint32_t d = 0; d < (uint32_t)G; d++) {
-        const uint32_t pd = gshfl(my_prio, d);
-        rank += (d < nch && pd > my_prio);
-      }
-      if (cl) {
-        const uint64_t T = b.chain_T[c0 + gl];
-        S.cT[rank] = (uint32_t)T;
-        S.cD[rank] = (uint32_t)b.chain_D[c0 + gl];
-        S.cCls[rank] = b.chain_class[c0 + gl];
-        S.cLocal[rank] = (uint8_t)gl;
-        const uint32_t o0 = b.chain_cb_off[c0 + gl] - cb0;
-        S.cCb0[rank] = (uint8_t)o0;
-        S.cNcb[rank] = (uint8_t)(b.chain_cb_off[c0 + gl + 1] - cb0 - o0);
-        S.cPhase[rank] = pg_phase(seed, first_index + set, gl, T);  // D2
-      }
-      // executors: canonical order (core asc, process priority desc)
-      const bool xl = stg && gl < nex;
-      const uint32_t xcore = xl ? b.exec_core[x0 + gl] : 0x100u + gl;
-      const uint32_t xprio = xl ? b.exec_prio[x0 + gl] : 0u;
-      uint32_t xpos = 0;
-      for (uint32_t y = 0; y < (uint32_t)G; y++) {
-        const uint32_t cy = gshfl(xcore, y), py = gshfl(xprio, y);
-        xpos += y < nex && ((cy < xcore) || (cy == xcore && py > xprio));
-      }
-      if (xl) {
-        S.xcanon[gl] = (uint8_t)xpos;
-        S.xWait[xpos] = b.exec_wait[x0 + gl];
-      }
-      {
-        // executors sharing a core, as a mask over canonical positions (group-local match key)
-        const uint32_t same = (__match_any_sync(FULL, xcore | (grp << 12)) >> goff) & GM;
-        uint32_t m = 0;
-        for (uint32_t y = 0; y < (uint32_t)G; y++) {
-          const uint32_t py = gshfl(xpos, y);
-          if (y < nex && ((same >> y) & 1u)) m |= 1u << py;
-        }
-        if (xl) S.xSameCore[xpos] = m;
-      }
-      __syncwarp();
-      // accelerators / units
-      if (stg && gl == 0) {
-        uint32_t u = 0;
-        for (uint32_t a = 0; a < nac; a++) {
-          S.ubase[a] = u;
-          const uint32_t nb = b.accel_buckets[a0 + a], nu = b.accel_units[a0 + a];
-          const uint32_t e = (uint32_t)b.accel_eps[a0 + a];
-          const uint32_t k = (nb > 1 && !fifo) ? (uint32_t)b.accel_kappa[a0 + a] : 0u;  // A6
-          for (uint32_t v = 0; v < nu; v++, u++) { S.uEps[u] = e; S.uKap[u] = k; S.uN[u] = nb; }
-        }
-      }
-      __syncwarp();
-      // callbacks and segments
-      for (uint32_t j = gl; j < ncb; j += G) {
-        const uint32_t so = b.cb_seg_off[cb0 + j] - sg0;
-        S.bExec[j] = S.xcanon[b.cb_exec[cb0 + j]];
-        S.bSeg0[j] = (uint8_t)so;
-        S.bNseg[j] = (uint8_t)(b.cb_seg_off[cb0 + j + 1] - sg0 - so);
-      }
-      for (uint32_t g = gl; g < nseg; g += G) {
-        const uint32_t kind = b.seg_kind[sg0 + g];
-        S.gKind[g] = (uint8_t)kind;
-        S.gW[g] = (uint32_t)b.seg_wcet[sg0 + g];
-        S.gUnit[g] = kind == 1 ? (uint8_t)(S.ubase[b.seg_accel[sg0 + g]] + b.seg_unit[sg0 + g]) : (uint8_t)0;
-      }
-      __syncwarp();
-      if (stg && (b.flags & PAAM_FLAG_WFD_UNITS) && gl == 0) {  // WFD unit assignment, as pack_kernel
-        uint64_t* wu = S.wfd.wu;
-        uint8_t *wo = S.wfd.wo, *wn = S.wfd.wn, *wc = S.wfd.wc;
-        for (uint32_t a = 0; a < nac; a++) {
-          const uint32_t nu = b.accel_units[a0 + a];
-          uint32_t ni = 0;
-          for (uint32_t j = 0; j < ncb; j++) {
-            uint32_t k = 0;
-            for (uint32_t q = 0; q < nch; q++) if (S.cCb0[q] <= j && j < S.cCb0[q] + S.cNcb[q]) k = q;
-            uint64_t A = 0;
-            for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
-              if (S.gKind[g] == 1 && b.seg_accel[sg0 + g] == a) A += S.gW[g];
-            if (A) { wu[ni] = (A << 24) / S.cT[k]; wc[ni] = (uint8_t)j; ni++; }
-          }
-          wfd_place(ni, wu, nu, wo, wn);
-          for (uint32_t i = 0; i < ni; i++) {
-            const uint32_t j = wc[i];
-            for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
-              if (S.gKind[g] == 1 && b.seg_accel[sg0 + g] == a) S.gUnit[g] = (uint8_t)(S.ubase[a] + wn[i]);
-          }
-        }
-      }
-      __syncwarp();
-      // buckets (A5): per accelerator, chains using it ranked by priority, groups of ceil(m_a/n)
-      {
-        uint32_t use = 0;  // lane = rank
-        if (cl) {
-          for (uint32_t j = S.cCb0[gl]; j < S.cCb0[gl] + S.cNcb[gl]; j++)
-            for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
-              if (S.gKind[g] == 1) {
-                uint32_t a = 0;
-                for (uint32_t q = 1; q < nac; q++) if (S.ubase[q] <= S.gUnit[g]) a = q;
-                use |= 1u << a;
-              }
-        }
-        uint32_t bk[4] = {0, 0, 0, 0};
-        for (uint32_t a = 0; a < 4; a++) {
-          const uint32_t U = gballot((use >> a) & 1u);
-          if (a < nac) {
-            const uint32_t ma = __popc(U), nb = b.accel_buckets[a0 + a];
-            const uint32_t gsz = ma ? (ma + nb - 1) / nb : 1u;
-            bk[a] = nb - 1 - __popc(U & ltg) / gsz;
-          }
-        }
-        if (cl)
-          for (uint32_t j = S.cCb0[gl]; j < S.cCb0[gl] + S.cNcb[gl]; j++)
-            for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
-              if (S.gKind[g] == 1) {
-                uint32_t a = 0;
-                for (uint32_t q = 1; q < nac; q++) if (S.ubase[q] <= S.gUnit[g]) a = q;
-                S.gBkt[g] = fifo ? (uint8_t)0 : (uint8_t)bk[a];
-              }
-      }
-      // dynamic state
-      if (stg) {
-        S.iState[gl] = rep4(I_FREE);
-        S.iWUnit[gl] = rep4(NOQ);
-        S.maxResp[gl] = 0;
-        S.cnt[gl] = 0;
-        S.miss[gl] = 0;
-        S.exPhase[gl] = P_NONE;
-        S.exChain[gl] = 0xff;
-        if (gl < (uint32_t)MAXU) { S.unState[gl] = U_IDLE; S.uQ[gl] = 0; }
-      }
-      __syncwarp();
-      if (stg) {
-        live = true;
-        C.t = 0;
-        C.dig = 0;
-        if (C.want_dig) C.th = fnv_time(0);
-        next_k = 0;
-        next_rel = gl < nch ? S.cPhase[gl] : NONE64;
-        seq = 0;
-        on_core = false;
-        drops = 0;
-        steps = 0;
-        stop = PAAM_SIM_OK;
-        backlog = false;
-        is_chain = gl < nch;
-        is_exec = gl < nex;
-        is_unit = gl < n_unit;
+      if (lane < nex) S.xSameCore[xpos] = m;
+    }
+    __syncwarp();
+    // accelerators / units
+    __shared__ uint32_t ubase_all[SW][4];
+    uint32_t* ubase = ubase_all[threadIdx.x >> 5];
+    if (lane == 0) {
+      uint32_t u = 0;
+      for (uint32_t a = 0; a < nac; a++) {
+        ubase[a] = u;
+        const uint32_t nb = b.accel_buckets[a0 + a], nu = b.accel_units[a0 + a];
+        const uint32_t e = (uint32_t)b.accel_eps[a0 + a];
+        const uint32_t k = (nb > 1 && !(sim_flags & PAAM_SIM_FIFO_DIRECT)) ? (uint32_t)b.accel_kappa[a0 + a] : 0u;  // A6
+        for (uint32_t v = 0; v < nu; v++, u++) { S.uEps[u] = e; S.uKap[u] = k; S.uN[u] = nb; }
       }
     }
-    if (__all_sync(FULL, done)) break;
-    if (!__any_sync(FULL, live)) continue;
+    __syncwarp();
+    const uint32_t n_unit = rec.n_unit;
+    // callbacks and segments
+    for (uint32_t j = lane; j < ncb; j += 32) {
+      const uint32_t so = b.cb_seg_off[cb0 + j] - sg0;
+      S.bExec[j] = xcanon[b.cb_exec[cb0 + j]];
+      S.bSeg0[j] = (uint8_t)so;
+      S.bNseg[j] = (uint8_t)(b.cb_seg_off[cb0 + j + 1] - sg0 - so);
+    }
+    for (uint32_t g = lane; g < nseg; g += 32) {
+      const uint32_t kind = b.seg_kind[sg0 + g];
+      S.gKind[g] = (uint8_t)kind;
+      S.gW[g] = (uint32_t)b.seg_wcet[sg0 + g];
+      S.gUnit[g] = kind == 1 ? (uint8_t)(ubase[b.seg_accel[sg0 + g]] + b.seg_unit[sg0 + g]) : (uint8_t)0;
+    }
+    __syncwarp();
+    if ((b.flags & PAAM_FLAG_WFD_UNITS) && lane == 0) {  // WFD unit assignment, as pack_kernel
+      uint64_t* wu = S.wfd.wu;
+      uint8_t *wo = S.wfd.wo, *wn = S.wfd.wn, *wc = S.wfd.wc;
+      for (uint32_t a = 0; a < nac; a++) {
+        const uint32_t nu = b.accel_units[a0 + a];
+        uint32_t ni = 0;
+        for (uint32_t j = 0; j < ncb; j++) {
+          uint32_t k = 0;
+          for (uint32_t q = 0; q < nch; q++) if (S.cCb0[q] <= j && j < S.cCb0[q] + S.cNcb[q]) k = q;
+          uint64_t A = 0;
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1 && b.seg_accel[sg0 + g] == a) A += S.gW[g];
+          if (A) { wu[ni] = (A << 24) / S.cT[k]; wc[ni] = (uint8_t)j; ni++; }
+        }
+        wfd_place(ni, wu, nu, wo, wn);
+        for (uint32_t i = 0; i < ni; i++) {
+          const uint32_t j = wc[i];
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1 && b.seg_accel[sg0 + g] == a) S.gUnit[g] = (uint8_t)(ubase[a] + wn[i]);
+        }
+      }
+    }
+    __syncwarp();
+    // buckets (A5): per accelerator, chains using it ranked by priority, groups of ceil(m_a/n)
+    {
+      uint32_t use = 0;  // lane = rank
+      if (lane < nch) {
+        for (uint32_t j = S.cCb0[lane]; j < S.cCb0[lane] + S.cNcb[lane]; j++)
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1) {
+              uint32_t a = 0;
+              for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= S.gUnit[g]) a = q;
+              use |= 1u << a;
+            }
+      }
+      const uint32_t lt = lanemask_lt();
+      uint32_t bk[4] = {0, 0, 0, 0};
+      for (uint32_t a = 0; a < nac; a++) {
+        const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
+        const uint32_t ma = __popc(U), nb = b.accel_buckets[a0 + a];
+        const uint32_t gsz = ma ? (ma + nb - 1) / nb : 1u;
+        bk[a] = nb - 1 - __popc(U & lt) / gsz;
+      }
+      if (lane < nch)
+        for (uint32_t j = S.cCb0[lane]; j < S.cCb0[lane] + S.cNcb[lane]; j++)
+          for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
+            if (S.gKind[g] == 1) {
+              uint32_t a = 0;
+              for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= S.gUnit[g]) a = q;
+              S.gBkt[g] = (sim_flags & PAAM_SIM_FIFO_DIRECT) ? (uint8_t)0 : (uint8_t)bk[a];
+            }
+    }
+    // dynamic state
+    if (lane < MAXC) {
+      S.iState[lane] = rep4(I_FREE);
+      S.iWUnit[lane] = rep4(NOQ);
+      S.maxResp[lane] = 0;
+      S.cnt[lane] = 0;
+      S.miss[lane] = 0;
+      S.exPhase[lane] = P_NONE;
+      S.exChain[lane] = 0xff;
+    }
+    if (lane < MAXU) { S.unState[lane] = U_IDLE; S.uQ[lane] = 0; }
+    __syncwarp();
 
-    // ===================== settle time t (D15), groups with a live set =====================
-    // A phase-A pass can leave work due at t only on an executor it advanced (a zero-length eps)
-    // -- units settle in (1), transits made in (1)/(2) arrive in (3) of the same pass, and releases
-    // are spaced by T -- and phase B can create due-now phase-A work only through a zero eps or
-    // kappa.  Passes are repeated exactly when such work exists, so every skipped pass is a no-op.
-    // The unit queues' occupancy (uQ) lets phase B skip units with no request to dispatch.
-    bool ended = false;      // group-uniform: the set's run is over (completed or stopped)
-    bool settling = live;    // group-uniform: this group's timestamp is not settled yet
-    bool run_a = live;       // group-uniform: another phase-A pass is due
+    const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
+    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr, fnv_time(0)};
+    uint32_t next_k = 0;  // lane = rank
+    uint64_t next_rel = (uint32_t)lane < nch ? S.cPhase[lane] : NONE64;  // release time of instance next_k (D2)
+    uint32_t seq = 0;     // warp-uniform
+    bool on_core = false; // lane = canonical executor
+    uint32_t drops = 0;
+    uint64_t steps = 0;
+    int32_t stop = PAAM_SIM_OK;  // warp-uniform: why the run stopped early (PAAM_SIM_BACKLOG / _STEPCAP)
+    bool backlog = false;         // lane = chain: a release found every instance slot live
+    const bool is_chain = lane < nch, is_exec = lane < nex, is_unit = lane < n_unit;
+
     for (;;) {
-      while (__any_sync(FULL, run_a)) {
-        // (1) units
-        if (run_a && is_unit) {
-          const uint32_t u = gl;
-          if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
-            if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
-            else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; }
-          }
-          if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
-            const uint32_t c = S.unChain[u], sl = S.unSlot[u];
-            InstRef I = S.ref(c, sl);
-            const uint32_t j = S.cCb0[c] + I.cb;
-            uint32_t x = S.bExec[j];
-            // the request's segment: the executor's current segment
-            const uint32_t g = S.bSeg0[j] + S.exSeg[x];
-            C.ev(EV_ACC_DONE, c, I.cb, S.exSeg[x], u, S.gBkt[g]);
-            I.wunit = NOQ;
-            S.uQ[u]--;
-            S.unState[u] = U_IDLE;
-            C.advance_segment(x);
-          }
-        }
-        __syncwarp();
-        // (2) executors: CPU / eps completions; enqueues sequenced by (chain, instance) (D7)
-        bool enq = false, adv = false;
-        uint32_t enq_key = 0xffffffffu;
-        if (run_a && is_exec) {
-          const uint32_t x = gl, ph = S.exPhase[x];
-          if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); adv = true; }
-          else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
-            S.exPhase[x] = P_WAIT;
-            enq = true;
-            enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.ref(S.exChain[x], S.exSlot[x]).k & 0xffffffu);
-          }
-        }
-        // (2) served every executor that was due, and advance_segment(x) changes executor x only, so
-        // only an executor (2) advanced can be due again (its next segment may be zero-length)
-        const bool due_x = adv && C.exec_due(gl);  // final for this pass: (3)/(4) leave executors alone
-        const uint32_t enq_mask = gballot(enq);
-        if (__any_sync(FULL, enq_mask != 0u)) {
-          uint32_t pos = 0;
-          uint32_t mm = enq_mask;
-          while (__any_sync(FULL, mm != 0u)) {
-            const uint32_t y = mm ? (uint32_t)__ffs(mm) - 1u : 0u;
-            const uint32_t ky = gshfl(enq_key, y);
-            if (mm) {
-              mm &= mm - 1;
-              pos += (ky < enq_key);
+      // ===================== settle time t (D15) =====================
+      // A phase-A pass can leave work due at t only on an executor it advanced (a zero-length eps)
+      // -- units settle in (1), transits made in (1)/(2) arrive in (3) of the same pass, and releases
+      // are spaced by T -- and phase B can create due-now phase-A work only through a zero eps or
+      // kappa.  Passes are repeated exactly when such work exists, so every skipped pass is a no-op.
+      // The unit queues' occupancy (uQ) lets phase B skip units with no request to dispatch.
+      bool run_a = true;
+      for (;;) {
+        while (run_a) {
+          // (1) units
+          if (is_unit) {
+            const uint32_t u = lane;
+            if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
+              if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
+              else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; }
+             
             }
-          }
-          if (enq) {
-            const uint32_t x = gl, c = S.exChain[x], sl = S.exSlot[x];
-            InstRef I = S.ref(c, sl);
-            const uint32_t g = S.bSeg0[S.cCb0[c] + I.cb] + S.exSeg[x];
-            I.seq = seq + pos;
-            I.wunit = S.gUnit[g];
-            I.started = 0;
-            atomicAdd(&S.uQ[S.gUnit[g]], 1u);
-            C.ev(EV_REQ_ENQUEUE, c, I.cb, S.exSeg[x], S.gUnit[g], S.gBkt[g]);
-          }
-          seq += __popc(enq_mask);
-        }
-        __syncwarp();
-        // (3) comm arrivals, (4) releases (D2, D14)
-        if (run_a && is_chain) {
-          const uint32_t c = gl;
-          for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
-            const uint32_t q = slot_of(tm);
-            if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; }
-          }
-          const uint64_t r = next_rel;
-          if (r == C.t && r < horizon) {
-            if (S.cCls[c] == 1)
-              for (uint32_t dm = slots_eq(S.iState[c], I_READY) & slots_eq(S.iCb[c], 0); dm; dm &= dm - 1) {
-                byte_of(S.iState[c], slot_of(dm)) = I_FREE;
-                drops++;
-                C.ev(EV_DROP, c, FULL, FULL, FULL, FULL);
-              }
-            const uint32_t fm = slots_eq(S.iState[c], I_FREE);
-            const int slot = fm ? (int)slot_of(fm) : -1;
-            if (slot < 0) {
-              backlog = true;  // D14: the new instance would be the chain's (QCAP+1)-th live one
-            } else {
-              InstRef I = S.ref(c, slot);
-              I.state = I_READY; I.k = next_k; I.cb = 0; I.wunit = NOQ;
-              C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
+            if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
+              const uint32_t c = S.unChain[u], sl = S.unSlot[u];
+              InstRef I = S.ref(c, sl);
+              const uint32_t j = S.cCb0[c] + I.cb;
+              uint32_t x = S.bExec[j];
+              // the request's segment: the executor's current segment
+              const uint32_t g = S.bSeg0[j] + S.exSeg[x];
+              C.ev(EV_ACC_DONE, c, I.cb, S.exSeg[x], u, S.gBkt[g]);
+              I.wunit = NOQ;
+              S.uQ[u]--;
+              S.unState[u] = U_IDLE;
+              C.advance_segment(x);
+             
             }
-            next_k++;
-            next_rel += S.cT[c];
-          }
-        }
-        __syncwarp();
-        // a backlog stop is checked only when the cheap vote fires (it almost never does)
-        const bool more_a = gany(due_x || backlog);
-        const bool any_backlog = gany(backlog);  // (every lane votes: no collective behind a short circuit)
-        if (run_a && more_a && any_backlog) {
-          stop = PAAM_SIM_BACKLOG;
-          ended = true;
-          settling = false;
-          run_a = false;
-        } else {
-          run_a = run_a && more_a;
-        }
-      }
-      if (!__any_sync(FULL, settling)) break;
-      // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
-      bool needB = false, dueB = false;  // another phase-B pass could act / B left phase-A work due now
-      uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
-      if (settling && is_chain) {
-        const uint32_t cbw = S.iCb[gl], cb0 = S.cCb0[gl];
-        for (uint32_t rm = slots_eq(S.iState[gl], I_READY); rm; rm &= rm - 1)
-          ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * slot_of(rm))) & 0xffu)];
-      }
-      const uint32_t has_ready = __reduce_or_sync(gmask, ready_x);
-      uint32_t wm = gballot(settling && is_exec && on_core && S.exPhase[gl] == P_NONE && ((has_ready >> gl) & 1u));
-      while (__any_sync(FULL, wm != 0u)) {
-        const bool act = wm != 0u;
-        const uint32_t x = act ? (uint32_t)__ffs(wm) - 1u : 0u;
-        if (act) wm &= wm - 1;
-        const uint32_t cand = gballot(act && ((ready_x >> x) & 1u));
-        const uint32_t c = (uint32_t)__ffs(cand) - 1u;
-        if (act && gl == c) {
-          int best = -1;
-          const uint32_t cbw = S.iCb[c];
-          for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1) {
-            const uint32_t q = slot_of(rm), qcb = (cbw >> (8 * q)) & 0xffu;
-            if (S.bExec[S.cCb0[c] + qcb] != x) continue;
-            if (best < 0) { best = (int)q; continue; }
-            const uint32_t kq = S.iw[c][q].k, kb = S.iw[c][best].k;  // older release = smaller k
-            if (kq < kb || (kq == kb && qcb < ((cbw >> (8 * best)) & 0xffu))) best = (int)q;
-          }
-          InstRef I = S.ref(c, best);
-          I.state = I_RUN;
-          S.exChain[x] = (uint8_t)c;
-          S.exSlot[x] = (uint8_t)best;
-          S.exSeg[x] = 0;
-          C.ev(EV_CB_START, c, I.cb, 0, FULL, FULL);
-          C.begin_segment(x);
-          dueB |= C.exec_due(x);
-          // this chain no longer offers that instance
-          ready_x = 0;
-          {
-            const uint32_t cbw2 = S.iCb[c], cb0 = S.cCb0[c];
-            for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1)
-              ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * slot_of(rm))) & 0xffu)];
-          }
-        }
-        __syncwarp();
-      }
-      // (6) core dispatch (D5): highest process priority runnable executor per core.  ready_x is
-      // current: (5) recomputed it on every chain lane whose instance it started.
-      {
-        const uint32_t hr = __reduce_or_sync(gmask, ready_x);
-        bool run = false;
-        if (settling && is_exec) {
-          const uint32_t ph = S.exPhase[gl];
-          run = ph == P_NONE ? ((hr >> gl) & 1u) : (ph == P_CPU || ph == P_EPS_SPIN) ? true
-              : ph == P_WAIT ? (S.xWait[gl] != 0) : false;
-        }
-        const uint32_t R = gballot(run);
-        const uint32_t cand = (settling && is_exec) ? (R & S.xSameCore[gl]) : 0u;
-        const bool oc = cand && (__ffs(cand) - 1 == (int)gl);
-        // an executor that just got its core while idle with ready work is the only thing another
-        // phase-B pass could act on ((5) serves every wanting executor once per pass; (7) units are
-        // independent of each other)
-        if (settling && is_exec) {
-          needB = oc && !on_core && S.exPhase[gl] == P_NONE;
-          on_core = oc;
-        }
-      }
-      // (7) unit dispatch (D8-D11).  Lane u decides whether unit u has anything to dispatch (queue
-      // occupancy, state); only those units are visited (dispatch on one unit changes no other's).
-      uint32_t umask;
-      {
-        bool cand = false;
-        if (settling && is_unit) {
-          const uint32_t ust = S.unState[gl], q = S.uQ[gl];
-          cand = fifo ? (ust == U_IDLE && q > 0)
-                      : ((ust == U_IDLE && q > 0) || (ust == U_RUN && S.uN[gl] > 1 && q > 1));
-        }
-        umask = gballot(cand);
-      }
-      while (__any_sync(FULL, umask != 0u)) {
-        const bool act = umask != 0u;
-        const uint32_t u = act ? (uint32_t)__ffs(umask) - 1u : 0u;
-        if (act) umask &= umask - 1;
-        const uint32_t ust = act ? S.unState[u] : (uint32_t)U_IDLE;
-        if (fifo) {  // FIFO_DIRECT: an idle unit starts the oldest request; never preempts
-          uint32_t myseq = 0xffffffffu;
-          int fslot = -1;
-          if (act && is_chain)
-            for (uint32_t wmq = slots_eq(S.iWUnit[gl], u); wmq; wmq &= wmq - 1) {
-              const uint32_t q = slot_of(wmq);
-              if (S.iw[gl][q].seq < myseq) { myseq = S.iw[gl][q].seq; fslot = (int)q; }
-            }
-          const uint32_t oldest = __reduce_min_sync(gmask, myseq);
-          if (act && oldest != 0xffffffffu && myseq == oldest) {
-            InstRef I = S.ref(gl, fslot);
-            const uint32_t j = S.cCb0[gl] + I.cb, x = S.bExec[j], seg = S.exSeg[x];
-            S.unChain[u] = (uint8_t)gl;
-            S.unSlot[u] = (uint8_t)fslot;
-            I.started = 1;
-            S.unState[u] = U_RUN;
-            S.unRem[u] = S.gW[S.bSeg0[j] + seg];
-            C.ev(EV_ACC_START, gl, I.cb, seg, u, 0u);
           }
           __syncwarp();
-          continue;
-        }
-        // best waiting request on u, excluding the running one: key = bucket | started | priority
-        uint32_t key = 0;
-        int bslot = -1;
-        if (act && is_chain) {
-          const uint32_t sw = S.iStarted[gl];
-          for (uint32_t wmq = slots_eq(S.iWUnit[gl], u); wmq; wmq &= wmq - 1) {
-            const int q = (int)slot_of(wmq);
-            if (ust == U_RUN && S.unChain[u] == gl && S.unSlot[u] == q) continue;
-            if (bslot < 0) { bslot = q; continue; }
-            const uint32_t sq = (sw >> (8 * q)) & 0xffu, sb = (sw >> (8 * bslot)) & 0xffu;
-            if (sq != sb) { if (sq) bslot = q; }
-            else if (S.iw[gl][q].seq < S.iw[gl][bslot].seq) bslot = q;
+          // (2) executors: CPU / eps completions; enqueues sequenced by (chain, instance) (D7)
+          bool enq = false, adv = false;
+          uint32_t enq_key = 0xffffffffu;
+          if (is_exec) {
+            const uint32_t x = lane, ph = S.exPhase[x];
+            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); adv = true; }
+            else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
+              S.exPhase[x] = P_WAIT;
+              enq = true;
+              enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.ref(S.exChain[x], S.exSlot[x]).k & 0xffffffu);
+             
+            }
           }
-          if (bslot >= 0) {
-            InstRef I = S.ref(gl, bslot);
-            const uint32_t g = S.bSeg0[S.cCb0[gl] + I.cb];  // bucket is per (chain, accelerator)
-            uint32_t bkt = 0;
-            for (uint32_t gg = g; gg < g + S.bNseg[S.cCb0[gl] + I.cb]; gg++)
-              if (S.gKind[gg] == 1 && S.gUnit[gg] == u) bkt = S.gBkt[gg];
-            key = 1u + ((bkt << 6) | ((uint32_t)I.started << 5) | (31u - gl));
+          // (2) served every executor that was due, and advance_segment(x) changes executor x only, so
+          // only an executor (2) advanced can be due again (its next segment may be zero-length)
+          const bool due_x = adv && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
+          const uint32_t enq_mask = __ballot_sync(FULL, enq);
+          if (enq_mask) {
+            uint32_t pos = 0;
+            uint32_t mm = enq_mask;
+            while (mm) {
+              const uint32_t y = __ffs(mm) - 1;
+              mm &= mm - 1;
+              pos += (__shfl_sync(FULL, enq_key, y) < enq_key);
+            }
+            if (enq) {
+              const uint32_t x = lane, c = S.exChain[x], sl = S.exSlot[x];
+              InstRef I = S.ref(c, sl);
+              const uint32_t g = S.bSeg0[S.cCb0[c] + I.cb] + S.exSeg[x];
+              I.seq = seq + pos;
+              I.wunit = S.gUnit[g];
+              I.started = 0;
+              atomicAdd(&S.uQ[S.gUnit[g]], 1u);
+              C.ev(EV_REQ_ENQUEUE, c, I.cb, S.exSeg[x], S.gUnit[g], S.gBkt[g]);
+            }
+            seq += __popc(enq_mask);
           }
+          __syncwarp();
+          // (3) comm arrivals, (4) releases (D2, D14)
+          if (is_chain) {
+            const uint32_t c = lane;
+            for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
+              const uint32_t q = slot_of(tm);
+              if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; }
+            }
+            const uint64_t r = next_rel;
+            if (r == C.t && r < horizon) {
+              if (S.cCls[c] == 1)
+                for (uint32_t dm = slots_eq(S.iState[c], I_READY) & slots_eq(S.iCb[c], 0); dm; dm &= dm - 1) {
+                  byte_of(S.iState[c], slot_of(dm)) = I_FREE;
+                  drops++;
+                  C.ev(EV_DROP, c, FULL, FULL, FULL, FULL);
+                }
+              const uint32_t fm = slots_eq(S.iState[c], I_FREE);
+              const int slot = fm ? (int)slot_of(fm) : -1;
+              if (slot < 0) {
+                backlog = true;  // D14: the new instance would be the chain's (QCAP+1)-th live one
+              } else {
+                InstRef I = S.ref(c, slot);
+                I.state = I_READY; I.k = next_k; I.cb = 0; I.wunit = NOQ;
+                C.ev(EV_RELEASE, c, FULL, FULL, FULL, FULL);
+              }
+              next_k++;
+              next_rel += S.cT[c];
+             
+            }
+          }
+          __syncwarp();
+          // a backlog stop is checked only when the cheap vote fires (it almost never does)
+          run_a = __any_sync(FULL, due_x || backlog);
+          if (run_a && __any_sync(FULL, backlog)) { stop = PAAM_SIM_BACKLOG; goto sim_done; }
         }
-        const uint32_t best = __reduce_max_sync(gmask, key);
-        if (act && best != 0) {
+        // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
+        bool needB = false, dueB = false;  // another phase-B pass could act / B left phase-A work due now
+        uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
+        if (is_chain) {
+          const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
+          for (uint32_t rm = slots_eq(S.iState[lane], I_READY); rm; rm &= rm - 1)
+            ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * slot_of(rm))) & 0xffu)];
+        }
+        const uint32_t has_ready = __reduce_or_sync(FULL, ready_x);
+        const uint32_t want = __ballot_sync(FULL, is_exec && on_core && S.exPhase[lane] == P_NONE && ((has_ready >> lane) & 1u));
+        uint32_t wm = want;
+        while (wm) {
+          const uint32_t x = __ffs(wm) - 1;
+          wm &= wm - 1;
+          const uint32_t cand = __ballot_sync(FULL, (ready_x >> x) & 1u);
+          const uint32_t c = __ffs(cand) - 1;
+          if (lane == c) {
+            int best = -1;
+            const uint32_t cbw = S.iCb[c];
+            for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1) {
+              const uint32_t q = slot_of(rm), qcb = (cbw >> (8 * q)) & 0xffu;
+              if (S.bExec[S.cCb0[c] + qcb] != x) continue;
+              if (best < 0) { best = (int)q; continue; }
+              const uint32_t kq = S.iw[c][q].k, kb = S.iw[c][best].k;  // older release = smaller k
+              if (kq < kb || (kq == kb && qcb < ((cbw >> (8 * best)) & 0xffu))) best = (int)q;
+            }
+            InstRef I = S.ref(c, best);
+            I.state = I_RUN;
+            S.exChain[x] = (uint8_t)c;
+            S.exSlot[x] = (uint8_t)best;
+            S.exSeg[x] = 0;
+            C.ev(EV_CB_START, c, I.cb, 0, FULL, FULL);
+            C.begin_segment(x);
+            dueB |= C.exec_due(x);
+            // this chain no longer offers that instance
+            ready_x = 0;
+            {
+              const uint32_t cbw2 = S.iCb[c], cb0 = S.cCb0[c];
+              for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1)
+                ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * slot_of(rm))) & 0xffu)];
+            }
+          }
+          __syncwarp();
+        }
+        // (6) core dispatch (D5): highest process priority runnable executor per core.  ready_x is
+        // current: (5) recomputed it on every chain lane whose instance it started.
+        {
+          const uint32_t hr = __reduce_or_sync(FULL, ready_x);
+          bool run = false;
+          if (is_exec) {
+            const uint32_t ph = S.exPhase[lane];
+            run = ph == P_NONE ? ((hr >> lane) & 1u) : (ph == P_CPU || ph == P_EPS_SPIN) ? true
+                : ph == P_WAIT ? (S.xWait[lane] != 0) : false;
+          }
+          const uint32_t R = __ballot_sync(FULL, run);
+          const uint32_t cand = is_exec ? (R & S.xSameCore[lane]) : 0u;
+          const bool oc = cand && (__ffs(cand) - 1 == lane);
+          // an executor that just got its core while idle with ready work is the only thing another
+          // phase-B pass could act on ((5) serves every wanting executor once per pass; (7) units are
+          // independent of each other)
+          needB = oc && !on_core && is_exec && S.exPhase[lane] == P_NONE;
+          on_core = oc;
+        }
+        // (7) unit dispatch (D8-D11).  Lane u decides whether unit u has anything to dispatch (queue
+        // occupancy, state); only those units are visited (dispatch on one unit changes no other's).
+        uint32_t umask;
+        {
+          bool cand = false;
+          if (is_unit) {
+            const uint32_t ust = S.unState[lane], q = S.uQ[lane];
+            cand = fifo ? (ust == U_IDLE && q > 0)
+                        : ((ust == U_IDLE && q > 0) || (ust == U_RUN && S.uN[lane] > 1 && q > 1));
+          }
+          umask = __ballot_sync(FULL, cand);
+        }
+        for (; umask; umask &= umask - 1) {
+          const uint32_t u = __ffs(umask) - 1;
+          const uint32_t ust = S.unState[u];
+          if (fifo) {  // FIFO_DIRECT: an idle unit starts the oldest request; never preempts
+            uint32_t myseq = 0xffffffffu;
+            int fslot = -1;
+            if (is_chain)
+              for (uint32_t wm = slots_eq(S.iWUnit[lane], u); wm; wm &= wm - 1) {
+                const uint32_t q = slot_of(wm);
+                if (S.iw[lane][q].seq < myseq) { myseq = S.iw[lane][q].seq; fslot = (int)q; }
+              }
+            const uint32_t oldest = __reduce_min_sync(FULL, myseq);
+            if (oldest == 0xffffffffu) continue;
+            if (myseq == oldest) {
+              InstRef I = S.ref(lane, fslot);
+              const uint32_t j = S.cCb0[lane] + I.cb, x = S.bExec[j], seg = S.exSeg[x];
+              S.unChain[u] = (uint8_t)lane;
+              S.unSlot[u] = (uint8_t)fslot;
+              I.started = 1;
+              S.unState[u] = U_RUN;
+              S.unRem[u] = S.gW[S.bSeg0[j] + seg];
+              C.ev(EV_ACC_START, lane, I.cb, seg, u, 0u);
+            }
+            __syncwarp();
+            continue;
+          }
+          // best waiting request on u, excluding the running one: key = bucket | started | priority
+          uint32_t key = 0;
+          int bslot = -1;
+          if (is_chain) {
+            const uint32_t sw = S.iStarted[lane];
+            for (uint32_t wm = slots_eq(S.iWUnit[lane], u); wm; wm &= wm - 1) {
+              const int q = (int)slot_of(wm);
+              if (ust == U_RUN && S.unChain[u] == lane && S.unSlot[u] == q) continue;
+              if (bslot < 0) { bslot = q; continue; }
+              const uint32_t sq = (sw >> (8 * q)) & 0xffu, sb = (sw >> (8 * bslot)) & 0xffu;
+              if (sq != sb) { if (sq) bslot = q; }
+              else if (S.iw[lane][q].seq < S.iw[lane][bslot].seq) bslot = q;
+            }
+            if (bslot >= 0) {
+              InstRef I = S.ref(lane, bslot);
+              const uint32_t g = S.bSeg0[S.cCb0[lane] + I.cb];  // bucket is per (chain, accelerator)
+              uint32_t bkt = 0;
+              for (uint32_t gg = g; gg < g + S.bNseg[S.cCb0[lane] + I.cb]; gg++)
+                if (S.gKind[gg] == 1 && S.gUnit[gg] == u) bkt = S.gBkt[gg];
+              key = 1u + ((bkt << 6) | ((uint32_t)I.started << 5) | (31u - lane));
+            }
+          }
+          const uint32_t best = __reduce_max_sync(FULL, key);
+          if (best == 0) continue;
           const uint32_t wc = 31u - ((best - 1u) & 31u);
           const uint32_t wbkt = (best - 1u) >> 6;
-          if (gl == wc) {
+          if (lane == wc) {
             InstRef I = S.ref(wc, bslot);
             const uint32_t j = S.cCb0[wc] + I.cb;
             const uint32_t x = S.bExec[j];
@@ -709,153 +638,123 @@ __global__ void __launch_bounds__(SW * 32, SimLB<G>::minb)
           }
           if (ust == U_RUN) {  // D9: preempt a lower bucket
             const uint32_t rc = S.unChain[u];
-            InstRef Rq = S.ref(rc, S.unSlot[u]);
-            const uint32_t rj = S.cCb0[rc] + Rq.cb, rx = S.bExec[rj], rseg = S.exSeg[rx];
+            InstRef R = S.ref(rc, S.unSlot[u]);
+            const uint32_t rj = S.cCb0[rc] + R.cb, rx = S.bExec[rj], rseg = S.exSeg[rx];
             const uint32_t rbkt = S.gBkt[S.bSeg0[rj] + rseg];
-            if (wbkt > rbkt && gl == 0) {
-              C.ev(EV_ACC_PREEMPT, rc, Rq.cb, rseg, u, rbkt);
-              Rq.rem = S.unRem[u];
-              S.unState[u] = U_SWOUT;
-              S.unEnd[u] = C.t + S.uKap[u];
-              dueB |= S.uKap[u] == 0;
+            if (wbkt > rbkt) {
+              if (lane == 0) {
+                C.ev(EV_ACC_PREEMPT, rc, R.cb, rseg, u, rbkt);
+                R.rem = S.unRem[u];
+                S.unState[u] = U_SWOUT;
+                S.unEnd[u] = C.t + S.uKap[u];
+                dueB |= S.uKap[u] == 0;
+              }
             }
+          } else {
           }
+          __syncwarp();
         }
-        __syncwarp();
+        // the timestamp is settled unless B left phase-A work due now or gave an idle executor with
+        // ready work its core (every other further A/B round would be a no-op)
+        const uint32_t vb = __reduce_or_sync(FULL, (needB ? 1u : 0u) | (dueB ? 2u : 0u));
+        if (!vb) break;
+        run_a = (vb & 2u) != 0;
       }
-      // the timestamp is settled unless B left phase-A work due now or gave an idle executor with
-      // ready work its core (every other further A/B round would be a no-op)
-      const uint32_t vb = __reduce_or_sync(gmask, (needB ? 1u : 0u) | (dueB ? 2u : 0u));
-      if (settling) {
-        if (!vb) settling = false;
-        else run_a = (vb & 2u) != 0;
+      // ===================== advance time =====================
+      // Every pending event lies less than 2^31 ns ahead (a period, eps, kappa, comm or remaining
+      // work, each < 2^31 - 1 ns), so the next event is found as a 32-bit distance from t.
+      uint32_t nd = 0xffffffffu;  // none
+      bool run_x = false, run_u = false;  // executor / unit whose remaining work shrinks with time
+      if (is_chain) {
+        const uint64_t r = next_rel;
+        if (r < horizon) nd = (uint32_t)(r - C.t);
+        for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
+          nd = min(nd, (uint32_t)(S.iw[lane][slot_of(tm)].ready_at - C.t));
       }
-      if (!__any_sync(FULL, settling)) break;
-    }
-    // ===================== advance time =====================
-    // Every pending event lies less than 2^31 ns ahead (a period, eps, kappa, comm or remaining
-    // work, each < 2^31 - 1 ns), so the next event is found as a 32-bit distance from t.
-    const bool adv_g = live && !ended;
-    uint32_t nd = 0xffffffffu;  // none
-    bool run_x = false, run_u = false;  // executor / unit whose remaining work shrinks with time
-    if (adv_g && is_chain) {
-      const uint64_t r = next_rel;
-      if (r < horizon) nd = (uint32_t)(r - C.t);
-      for (uint32_t tm = slots_eq(S.iState[gl], I_TRANSIT); tm; tm &= tm - 1)
-        nd = min(nd, (uint32_t)(S.iw[gl][slot_of(tm)].ready_at - C.t));
-    }
-    if (adv_g && is_exec) {
-      const uint32_t ph = S.exPhase[gl];
-      run_x = (ph == P_CPU || ph == P_EPS_SPIN) && on_core;
-      if (run_x) nd = min(nd, S.exRem[gl]);
-      if (ph == P_EPS_SUSP) nd = min(nd, (uint32_t)(S.exTimer[gl] - C.t));
-    }
-    if (adv_g && is_unit) {
-      const uint32_t us = S.unState[gl];
-      run_u = us == U_RUN;
-      if (run_u) nd = min(nd, S.unRem[gl]);
-      if (us == U_SWOUT || us == U_SWIN) nd = min(nd, (uint32_t)(S.unEnd[gl] - C.t));
-    }
-    nd = __reduce_min_sync(gmask, nd);
-    if (adv_g) {
-      if (nd == 0xffffffffu) {
-        ended = true;  // every released instance completed (D1)
-      } else if (++steps > STEP_CAP) {
-        stop = PAAM_SIM_STEPCAP;
-        ended = true;
-      } else {
-        const uint64_t nt = C.t + nd;
-        if (run_x) S.exRem[gl] -= nd;
-        if (run_u) S.unRem[gl] -= nd;
-        C.t = nt;
-        if (C.want_dig) C.th = fnv_time(nt);
+      if (is_exec) {
+        const uint32_t ph = S.exPhase[lane];
+        run_x = (ph == P_CPU || ph == P_EPS_SPIN) && on_core;
+        if (run_x) nd = min(nd, S.exRem[lane]);
+        if (ph == P_EPS_SUSP) nd = min(nd, (uint32_t)(S.exTimer[lane] - C.t));
       }
-    }
-    __syncwarp();
-
-    // ---- outputs of the groups whose run ended ------------------------------------------------------
-    if (__any_sync(FULL, ended)) {
-      // A stopped run's statistics cover the exact prefix up to the stop (lower bounds of the full run's);
-      // its chains are not checked against the bound (census[stopped] counts it instead).
-      uint64_t digest = C.dig;
-#pragma unroll
-      for (int of = G / 2; of > 0; of >>= 1) digest += __shfl_xor_sync(FULL, digest, of);  // group sum
-      bool viol = false, bad = false;
-      uint64_t bd = 0;
-      if (ended && is_chain) {
-        const uint32_t local = S.cLocal[gl];
-        if (out_resp) out_resp[c0 + local] = S.maxResp[gl];
-        if (out_count) out_count[c0 + local] = S.cnt[gl];
-        if (o.misses) o.misses[c0 + local] = S.miss[gl];
-        if (o.drops) o.drops[c0 + local] = drops;
-        if (bound) {
-          bd = bound[c0 + local];
-          if (S.cCls[gl] == 0 && (bd == PAAM_UNSCHED || bd > S.cD[gl])) bad = true;
-          viol = S.cCls[gl] == 0 && S.maxResp[gl] > bd;
-        }
+      if (is_unit) {
+        const uint32_t us = S.unState[lane];
+        run_u = us == U_RUN;
+        if (run_u) nd = min(nd, S.unRem[lane]);
+        if (us == U_SWOUT || us == U_SWIN) nd = min(nd, (uint32_t)(S.unEnd[lane] - C.t));
       }
-      const bool any_bad = gany(bad);
-      const bool set_sched = bound != nullptr && stop == PAAM_SIM_OK && !any_bad;
-      const uint32_t vm = gballot(ended && viol && set_sched);
-      if (ended && vm && o.violations) {  // sim > bound: count, and record the first max_witness witnesses
-        unsigned long long base = 0;
-        if (gl == 0) base = atomicAdd((unsigned long long*)o.violations, (unsigned long long)__popc(vm));
-        base = __shfl_sync(gmask, base, goff);
-        if ((vm >> gl) & 1u) {
-          const unsigned long long w = base + __popc(vm & ltg);
-          if (o.witness && w < o.max_witness) {
-            o.witness[2 * w] = set;
-            o.witness[2 * w + 1] = S.cLocal[gl];
-          }
-        }
-      }
-      if (ended && gl == 0) {
-        if (out_digest) out_digest[set] = digest;
-        if (o.status) o.status[set] = stop;
-        if (o.stopped && stop != PAAM_SIM_OK) atomicAdd((unsigned long long*)o.stopped, 1ull);
-      }
-      if (ended) live = false;
+      nd = __reduce_min_sync(FULL, nd);
+      if (nd == 0xffffffffu) break;
+      if (++steps > STEP_CAP) { stop = PAAM_SIM_STEPCAP; break; }
+      const uint64_t nt = C.t + nd;
+      if (run_x) S.exRem[lane] -= nd;
+      if (run_u) S.unRem[lane] -= nd;
+      C.t = nt;
+      if (C.want_dig) C.th = fnv_time(nt);
       __syncwarp();
     }
+
+  sim_done:
+    // ---- outputs ---------------------------------------------------------------------------------------
+    // A stopped run's statistics cover the exact prefix up to the stop (lower bounds of the full run's);
+    // its chains are not checked against the bound (census[stopped] counts it instead).
+    const uint64_t digest = warp_sum_u64(C.dig);
+    bool viol = false, set_sched = bound != nullptr && stop == PAAM_SIM_OK;
+    uint64_t bd = 0;
+    if (is_chain) {
+      const uint32_t local = S.cLocal[lane];
+      if (out_resp) out_resp[c0 + local] = S.maxResp[lane];
+      if (out_count) out_count[c0 + local] = S.cnt[lane];
+      if (o.misses) o.misses[c0 + local] = S.miss[lane];
+      if (o.drops) o.drops[c0 + local] = drops;
+      if (bound) {
+        bd = bound[c0 + local];
+        if (S.cCls[lane] == 0 && (bd == PAAM_UNSCHED || bd > S.cD[lane])) set_sched = false;
+        viol = S.cCls[lane] == 0 && S.maxResp[lane] > bd;
+      }
+    }
+    set_sched = __all_sync(FULL, set_sched || !is_chain);
+    const uint32_t vm = __ballot_sync(FULL, viol && set_sched);
+    if (vm && o.violations) {  // sim > bound: count, and record the first max_witness witnesses
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd((unsigned long long*)o.violations, (unsigned long long)__popc(vm));
+      base = __shfl_sync(FULL, base, 0);
+      if ((vm >> lane) & 1u) {
+        const unsigned long long w = base + __popc(vm & lanemask_lt());
+        if (o.witness && w < o.max_witness) {
+          o.witness[2 * w] = set;
+          o.witness[2 * w + 1] = S.cLocal[lane];
+        }
+      }
+    }
+    if (lane == 0) {
+      if (out_digest) out_digest[set] = digest;
+      if (o.status) o.status[set] = stop;
+      if (o.stopped && stop != PAAM_SIM_OK) atomicAdd((unsigned long long*)o.stopped, 1ull);
+    }
+    __syncwarp();
   }
 }
 
 }  // namespace
 
 #ifndef PAAM_WARP_EMU
-template <int G>
-static int launch_g(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket,
-                    const uint32_t* only, const uint32_t* only_count, uint32_t* big_list, uint32_t* big_count,
-                    uint32_t sets_hint, cudaStream_t st) {
+int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
+                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st) {
+  if (n == 0) return PAAM_OK;
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simulate_kernel<G>, SW * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, simulate_kernel, SW * 32, 0);
   if (per_sm < 1) per_sm = 1;
-  const uint32_t per_block = SW * (32 / G);
-  const uint32_t need = (sets_hint + per_block - 1) / per_block;
+  const uint32_t need = (n + SW - 1) / SW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
-  const uint32_t grid = need < cap ? (need ? need : 1u) : cap;
-  simulate_kernel<G><<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, *out, ticket, only,
-                                               only_count, big_list, big_count);
+  const uint32_t grid = need < cap ? need : cap;
+  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, *out, ticket);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "simulate_kernel launch");
-}
-
-// G = 16 over every set (two per warp); then G = 32 over the sets it listed (more than 16 chains or
-// executors).  tickets: 2 counters + 1 list count; big_list: n entries.
-int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* tickets,
-                    uint32_t* big_list, cudaStream_t st) {
-  if (n == 0) return PAAM_OK;
-  cudaMemsetAsync(tickets, 0, 3 * sizeof(unsigned int), st);
-  if (int rc = launch_g<16>(b, rec, n, horizon, seed, first_index, sim_flags, out, tickets, nullptr, nullptr, big_list,
-                            tickets + 2, n, st))
-    return rc;
-  return launch_g<32>(b, rec, n, horizon, seed, first_index, sim_flags, out, tickets + 1, big_list, tickets + 2,
-                      nullptr, nullptr, n, st);
 }
 
 #endif  // PAAM_WARP_EMU
