@@ -487,13 +487,17 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       else if (__any_sync(FULL, ecore)) st = PAAM_SET_ECORE;
     }
     if (!st2) { pcb = b.chain_cb_off[pc]; st2 = true; }
-    const bool handed = st == REC_STATUS_WIDE;  // every output of a handed-over set is wide_kernel's
-    if (lane == 0 && handed) wide_list[atomicAdd(wide_count, 1u)] = set;
-    if (lane == 0 && status_out && !handed) status_out[set] = st;
-    uint32_t sched = 0;
-    if (handed) {
+    if (st == REC_STATUS_WIDE) {  // every output of a handed-over set is wide_kernel's
+      if (lane == 0) wide_list[atomicAdd(wide_count, 1u)] = set;
       if (!st3) psg = b.cb_seg_off[pcb];
-    } else if (st != PAAM_SET_OK) {
+      __syncwarp();
+      c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
+      nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
+      continue;
+    }
+    if (lane == 0 && status_out) status_out[set] = st;
+    uint32_t sched = 0;
+    if (st != PAAM_SET_OK) {
       if (out_wcrt)
         #pragma unroll 1
         for (uint32_t i = lane; i < nch; i += 32) out_wcrt[c0 + i] = UNS;
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         sched = __all_sync(FULL, ok) ? 1u : 0u;
       }
     }
-    if (lane == 0 && !handed) {
+    if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
       if (out_bins && bin_ok) {
         if (blk_bins) {
