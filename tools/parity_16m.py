@@ -66,6 +66,7 @@ def main():
         chains += len(gw)
         print(f"[{first + n}/{args.sets}] wcrt mismatches {mism_wcrt} sched mismatches {mism_sched}", file=sys.stderr, flush=True)
     out = dict(sets=args.sets, chains=chains, seed=args.seed, workload="config 4 (config-3 recipe)",
+               path="paam_pack_analyze on a device batch = fused_kernel (+ wide_kernel for handed-over sets)",
                wcrt_mismatches=mism_wcrt, sched_mismatches=mism_sched,
                bins_equal=bool(np.array_equal(tot_bins_g, tot_bins_o)), bins=tot_bins_g.tolist(),
                schedulable=int(tot_bins_g[1::2].sum()), oracle_threads=nthreads,
