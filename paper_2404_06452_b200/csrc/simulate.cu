@@ -99,6 +99,7 @@ struct DesSmem {
   uint32_t unRem[MAXU];
   uint8_t unState[MAXU], unChain[MAXU], unSlot[MAXU];
   uint32_t uQ[MAXU];  // requests queued on the unit (waiting, started or not; the running one included)
+  uint8_t uDirty[MAXU];  // a running unit's queue or running request changed since its last preemption check
   unsigned long long maxResp[MAXC];
   uint32_t cnt[MAXC], miss[MAXC];
 };
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       S.exPhase[lane] = P_NONE;
       S.exChain[lane] = 0xff;
     }
-    if (lane < MAXU) { S.unState[lane] = U_IDLE; S.uQ[lane] = 0; }
+    if (lane < MAXU) { S.unState[lane] = U_IDLE; S.uQ[lane] = 0; S.uDirty[lane] = 0; }
     __syncwarp();
 
     const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
@@ -381,6 +382,9 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     int32_t stop = PAAM_SIM_OK;  // warp-uniform: why the run stopped early (PAAM_SIM_BACKLOG / _STEPCAP)
     bool backlog = false;         // lane = chain: a release found every instance slot live
     const bool is_chain = lane < nch, is_exec = lane < nex, is_unit = lane < n_unit;
+    // this lane's unit / executor / chain has an event due at the current t (set by the time advance from
+    // the lane's own minima; a repeated pass of phase A runs with all three set)
+    bool due_u = true, due_x = true, due_c = true;
 
     for (;;) {
       // ===================== settle time t (D15) =====================
@@ -392,12 +396,12 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       bool run_a = true;
       for (;;) {
         while (run_a) {
-          // (1) units
-          if (is_unit) {
+          // (1) units.  Only a unit whose phase end or completion is due at t has anything to do here.
+          if (is_unit && due_u) {
             const uint32_t u = lane;
             if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
               if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
-              else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; }
+              else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; S.uDirty[u] = 1; }
              
             }
             if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           // (2) executors: CPU / eps completions; enqueues sequenced by (chain, instance) (D7)
           bool enq = false, adv = false;
           uint32_t enq_key = 0xffffffffu;
-          if (is_exec) {
+          if (is_exec && due_x) {  // (1) leaves no executor due: a callback's next segment is never zero-length
             const uint32_t x = lane, ph = S.exPhase[x];
             if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); adv = true; }
             else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           }
           // (2) served every executor that was due, and advance_segment(x) changes executor x only, so
           // only an executor (2) advanced can be due again (its next segment may be zero-length)
-          const bool due_x = adv && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
+          const bool again_x = adv && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
           const uint32_t enq_mask = __ballot_sync(FULL, enq);
           if (enq_mask) {
             uint32_t pos = 0;
@@ -449,13 +453,14 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               I.wunit = S.gUnit[g];
               I.started = 0;
               atomicAdd(&S.uQ[S.gUnit[g]], 1u);
+              S.uDirty[S.gUnit[g]] = 1;
               C.ev(EV_REQ_ENQUEUE, c, I.cb, S.exSeg[x], S.gUnit[g], S.gBkt[g]);
             }
             seq += __popc(enq_mask);
           }
           __syncwarp();
           // (3) comm arrivals, (4) releases (D2, D14)
-          if (is_chain) {
+          if (is_chain && due_c) {
             const uint32_t c = lane;
             for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
               const uint32_t q = slot_of(tm);
@@ -485,7 +490,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           }
           __syncwarp();
           // a backlog stop is checked only when the cheap vote fires (it almost never does)
-          run_a = __any_sync(FULL, due_x || backlog);
+          run_a = __any_sync(FULL, again_x || backlog);
+          due_u = due_x = due_c = true;
           if (run_a && __any_sync(FULL, backlog)) { stop = PAAM_SIM_BACKLOG; goto sim_done; }
         }
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
@@ -557,9 +563,13 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         {
           bool cand = false;
           if (is_unit) {
+            // an idle unit with requests always dispatches; a running one re-checks preemption (D9) only
+            // if a request joined its queue or it resumed a request since its last check (otherwise the
+            // check would repeat its last, negative, outcome)
             const uint32_t ust = S.unState[lane], q = S.uQ[lane];
             cand = fifo ? (ust == U_IDLE && q > 0)
-                        : ((ust == U_IDLE && q > 0) || (ust == U_RUN && S.uN[lane] > 1 && q > 1));
+                        : ((ust == U_IDLE && q > 0) || (ust == U_RUN && S.uN[lane] > 1 && q > 1 && S.uDirty[lane]));
+            S.uDirty[lane] = 0;
           }
           umask = __ballot_sync(FULL, cand);
         }
@@ -663,28 +673,33 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       // ===================== advance time =====================
       // Every pending event lies less than 2^31 ns ahead (a period, eps, kappa, comm or remaining
       // work, each < 2^31 - 1 ns), so the next event is found as a 32-bit distance from t.
-      uint32_t nd = 0xffffffffu;  // none
+      uint32_t nd_c = 0xffffffffu, nd_x = 0xffffffffu, nd_u = 0xffffffffu;  // none
       bool run_x = false, run_u = false;  // executor / unit whose remaining work shrinks with time
       if (is_chain) {
         const uint64_t r = next_rel;
-        if (r < horizon) nd = (uint32_t)(r - C.t);
+        if (r < horizon) nd_c = (uint32_t)(r - C.t);
         for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
-          nd = min(nd, (uint32_t)(S.iw[lane][slot_of(tm)].ready_at - C.t));
+          nd_c = min(nd_c, (uint32_t)(S.iw[lane][slot_of(tm)].ready_at - C.t));
       }
       if (is_exec) {
         const uint32_t ph = S.exPhase[lane];
         run_x = (ph == P_CPU || ph == P_EPS_SPIN) && on_core;
-        if (run_x) nd = min(nd, S.exRem[lane]);
-        if (ph == P_EPS_SUSP) nd = min(nd, (uint32_t)(S.exTimer[lane] - C.t));
+        if (run_x) nd_x = S.exRem[lane];
+        if (ph == P_EPS_SUSP) nd_x = (uint32_t)(S.exTimer[lane] - C.t);
       }
       if (is_unit) {
         const uint32_t us = S.unState[lane];
         run_u = us == U_RUN;
-        if (run_u) nd = min(nd, S.unRem[lane]);
-        if (us == U_SWOUT || us == U_SWIN) nd = min(nd, (uint32_t)(S.unEnd[lane] - C.t));
+        if (run_u) nd_u = S.unRem[lane];
+        if (us == U_SWOUT || us == U_SWIN) nd_u = (uint32_t)(S.unEnd[lane] - C.t);
       }
-      nd = __reduce_min_sync(FULL, nd);
+      const uint32_t nd = __reduce_min_sync(FULL, min(nd_c, min(nd_x, nd_u)));
       if (nd == 0xffffffffu) break;
+      // with comm = 0 a callback completing at t makes its successor arrive at t (D13), so every chain
+      // lane checks its transits then
+      due_c = nd_c == nd || C.comm == 0;
+      due_x = nd_x == nd;
+      due_u = nd_u == nd;
       if (++steps > STEP_CAP) { stop = PAAM_SIM_STEPCAP; break; }
       const uint64_t nt = C.t + nd;
       if (run_x) S.exRem[lane] -= nd;
