@@ -25,6 +25,8 @@ struct paam_sets {
                           // 20: number of wide sets listed (wide.cu)
   uint32_t* wide_list;    // [cap] the sets handed over to the u64 path by the last pack / fused launch
   int device;             // the CUDA device the handle lives on (made current by every call)
+  void* sim_scratch;      // paam_simulate's event buffers (grown on demand)
+  size_t sim_scratch_bytes;
   bool rec_valid;         // rec holds the records of `dev` (false after the fused paam_pack_analyze, which writes
                           // none: the next paam_analyze / paam_admit / paam_simulate packs them first)
 };
@@ -278,8 +280,9 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
   if (!o.witness) o.max_witness = 0;
   if (int rc = use_device(sets)) return rc;
   if (int rc = ensure_records(sets, (cudaStream_t)stream)) return rc;
-  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, &o,
-                         const_cast<paam_sets*>(sets)->tickets + 18, (cudaStream_t)stream);
+  paam_sets* ms = const_cast<paam_sets*>(sets);
+  return launch_simulate(&sets->dev, sets->rec, n, horizon, seed, first_index, sim_flags, &o, ms->tickets + 18,
+                         &ms->sim_scratch, &ms->sim_scratch_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
@@ -427,6 +430,7 @@ extern "C" void paam_free(paam_sets* sets) {
   if (sets->wide_list) cudaFree(sets->wide_list);
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
+  if (sets->sim_scratch) cudaFree(sets->sim_scratch);
   if (sets->side[0]) {
     for (int i = 0; i < 3; i++) cudaStreamDestroy(sets->side[i]);
     for (int i = 0; i < 17; i++) cudaEventDestroy(sets->ev[i]);

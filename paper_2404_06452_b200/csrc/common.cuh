@@ -160,8 +160,10 @@ int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count,
 // the exact u64 path over the sets listed by the u32 kernels (wide.cu); out_fail: admission decisions
 int launch_wide(const paam_batch* b, const uint32_t* list, const uint32_t* count, int32_t* status, uint64_t* out_wcrt,
                 uint8_t* out_sched, int64_t* out_bins, int32_t* out_fail, cudaStream_t st);
+// scratch / scratch_bytes: the caller's device scratch for the DES event buffers (grown on demand)
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st);
+                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket,
+                    void** scratch, size_t* scratch_bytes, cudaStream_t st);
 #endif
 
 }  // namespace paam

@@ -20,8 +20,10 @@
 // shared-memory atomics); "best" choices are warp reductions over rank-ordered lanes, so the
 // highest priority is the lowest set bit of a ballot.  Time then jumps to the warp-min next event.
 // Instance slots are packed one byte per slot per chain (byte-compare scans).  The event digest is
-// a sum of per-record FNV-1a-64 hashes (order independent), reduced at the end, computed only when
-// requested.
+// a sum of per-record FNV-1a-64 hashes (order independent), computed only when requested: the lane
+// that makes an event appends its 16-byte record to the warp's event buffer (global scratch, L2-resident),
+// and the warp hashes the buffered records 32 at a time, one per lane, whenever the buffer could not take
+// another settle pass (and at the end of the run).
 #include "../../gen/paam_gen.h"
 #include "common.cuh"
 
@@ -37,6 +39,12 @@ constexpr int MAXG = 192;  // segments per set
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint64_t NONE64 = ~0ull;
 constexpr uint64_t STEP_CAP = PAAM_SIM_STEP_CAP;  // safety valve: a run past it stops (PAAM_SIM_STEPCAP)
+// Event buffer per warp.  One phase-A pass makes at most 4 events per unit (ACC_DONE, SEG_DONE, CB_DONE,
+// CHAIN_DONE), 3 per executor (SEG_DONE, CB_DONE, CHAIN_DONE; or REQ_ENQUEUE) and 5 per chain (QCAP
+// drops + RELEASE): <= 8*4 + 32*3 + 32*5 = 288; a phase-B pass at most one CB_START per executor and two
+// events per unit: <= 48.  The buffer is flushed before a pass that could overflow it.
+constexpr uint32_t EVCAP = 512;
+constexpr uint32_t EV_PASS_MAX = 288;
 
 enum { EV_RELEASE = 0, EV_DROP, EV_OVERFLOW, EV_CB_START, EV_SEG_DONE, EV_REQ_ENQUEUE, EV_ACC_START,
        EV_ACC_PREEMPT, EV_ACC_RESUME, EV_ACC_DONE, EV_CB_DONE, EV_CHAIN_DONE };
@@ -102,6 +110,7 @@ struct DesSmem {
   uint8_t uDirty[MAXU];  // a running unit's queue or running request changed since its last preemption check
   unsigned long long maxResp[MAXC];
   uint32_t cnt[MAXC], miss[MAXC];
+  uint32_t evN;  // records in the warp's event buffer
 };
 
 // FNV-1a-64 of a 32-byte event record (D17) in two parts: the state after the record's 8-byte time
@@ -123,14 +132,16 @@ __device__ __forceinline__ uint64_t fnv_field(uint64_t h, uint32_t v) {
   constexpr uint64_t P4 = 0x9ffaac085635bc91ull;  // P^4 mod 2^64, P = 0x100000001b3
   return (h ^ (v == 0xffffffffu ? 0xffu : v)) * P4;
 }
-__device__ __forceinline__ uint64_t fnv_rest(uint64_t h, uint32_t kind, uint32_t chain, uint32_t cb, uint32_t seg,
-                                             uint32_t unit, uint32_t bk) {
-  h = fnv_field(h, kind);
-  h = fnv_field(h, chain);
-  h = fnv_field(h, cb);
-  h = fnv_field(h, seg);
-  h = fnv_field(h, unit);
-  return fnv_field(h, bk);
+// A buffered record: {t low, t high, kind | chain << 8 | callback << 16 | segment << 24, unit | bucket << 8},
+// one byte per field (0xff: does not apply).
+__device__ __forceinline__ uint64_t fnv_record(uint4 e) {
+  uint64_t h = fnv_time(((uint64_t)e.y << 32) | e.x);
+  h = fnv_field(h, e.z & 0xffu);
+  h = fnv_field(h, (e.z >> 8) & 0xffu);
+  h = fnv_field(h, (e.z >> 16) & 0xffu);
+  h = fnv_field(h, e.z >> 24);
+  h = fnv_field(h, e.w & 0xffu);
+  return fnv_field(h, e.w >> 8);
 }
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
@@ -139,15 +150,39 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t ev_byte(uint32_t v) { return v == 0xffffffffu ? 0xffu : v; }
+
 struct Ctx {
   DesSmem& S;
   uint64_t t, horizon, comm;
   uint64_t dig;  // this lane's partial digest
   bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
-  bool want_dig; // the caller asked for digests (out_digest != NULL); otherwise events are not hashed
-  uint64_t th;   // FNV-1a state after the 8 bytes of t (kept current only when want_dig)
+  bool want_dig; // the caller asked for digests (out_digest != NULL); otherwise events are not recorded
+  uint4* evb;    // this warp's event buffer (EVCAP records)
   __device__ void ev(uint32_t kind, uint32_t c, uint32_t cb, uint32_t seg, uint32_t unit, uint32_t bk) {
-    if (want_dig) dig += fnv_rest(th, kind, S.cLocal[c], cb, seg, unit, bk);
+    if (want_dig) {
+      const uint32_t i = atomicAdd(&S.evN, 1u);
+#ifdef PAAM_WARP_EMU
+      if (i >= EVCAP) { fprintf(stderr, "simulate: event buffer overflow (%u, kind %u)\n", i, kind); abort(); }
+#endif
+      evb[i] = make_uint4((uint32_t)t, (uint32_t)(t >> 32),
+                          kind | ((uint32_t)S.cLocal[c] << 8) | (ev_byte(cb) << 16) | (ev_byte(seg) << 24),
+                          ev_byte(unit) | (ev_byte(bk) << 8));
+    }
+  }
+  // warp-converged, before a settle pass: could the pass overflow the buffer?  Lane 0's count decides for
+  // the warp -- a lane that already started the pass could have added records that the others' reads would
+  // see (no lane can pass the shuffle before every lane reached it, and no event is made between the
+  // previous collective and this one).
+  __device__ bool must_flush() { return __shfl_sync(0xffffffffu, S.evN, 0) > EVCAP - EV_PASS_MAX; }
+  // warp-converged: hash the buffered records, one per lane, and empty the buffer
+  __device__ void flush(uint32_t lane) {
+    __syncwarp();
+    const uint32_t n = S.evN;
+    for (uint32_t i = lane; i < n; i += 32) dig += fnv_record(evb[i]);
+    __syncwarp();
+    if (lane == 0) S.evN = 0;
+    __syncwarp();
   }
   // executor x has phase-A work due now (a zero-length eps leaves it due right after it starts)
   __device__ bool exec_due(uint32_t x) const {
@@ -201,7 +236,7 @@ struct Ctx {
 __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
                                                            uint64_t horizon, uint64_t seed, uint64_t first_index,
                                                            uint32_t sim_flags, paam_sim_out o,
-                                                           unsigned int* __restrict__ ticket) {
+                                                           unsigned int* __restrict__ ticket, uint4* __restrict__ evbuf) {
   uint64_t* __restrict__ out_resp = o.resp;
   uint64_t* __restrict__ out_count = o.count;
   uint64_t* __restrict__ out_digest = o.digest;
@@ -369,10 +404,12 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       S.exChain[lane] = 0xff;
     }
     if (lane < MAXU) { S.unState[lane] = U_IDLE; S.uQ[lane] = 0; S.uDirty[lane] = 0; }
+    if (lane == 0) S.evN = 0;
     __syncwarp();
 
     const bool fifo = (sim_flags & PAAM_SIM_FIFO_DIRECT) != 0;
-    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr, fnv_time(0)};
+    Ctx C{S, 0, horizon, b.comm_cost, 0, fifo, out_digest != nullptr && evbuf != nullptr,
+          evbuf + ((size_t)blockIdx.x * SW + (threadIdx.x >> 5)) * EVCAP};
     uint32_t next_k = 0;  // lane = rank
     uint64_t next_rel = (uint32_t)lane < nch ? S.cPhase[lane] : NONE64;  // release time of instance next_k (D2)
     uint32_t seq = 0;     // warp-uniform
@@ -396,6 +433,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       bool run_a = true;
       for (;;) {
         while (run_a) {
+          if (C.want_dig && C.must_flush()) C.flush(lane);
           // (1) units.  Only a unit whose phase end or completion is due at t has anything to do here.
           if (is_unit && due_u) {
             const uint32_t u = lane;
@@ -494,6 +532,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           due_u = due_x = due_c = true;
           if (run_a && __any_sync(FULL, backlog)) { stop = PAAM_SIM_BACKLOG; goto sim_done; }
         }
+        if (C.want_dig && C.must_flush()) C.flush(lane);
         // (5) executor choice (D4): per executor, the ready instance of the highest-priority chain
         bool needB = false, dueB = false;  // another phase-B pass could act / B left phase-A work due now
         uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
@@ -705,7 +744,6 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       if (run_x) S.exRem[lane] -= nd;
       if (run_u) S.unRem[lane] -= nd;
       C.t = nt;
-      if (C.want_dig) C.th = fnv_time(nt);
       __syncwarp();
     }
 
@@ -713,6 +751,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     // ---- outputs ---------------------------------------------------------------------------------------
     // A stopped run's statistics cover the exact prefix up to the stop (lower bounds of the full run's);
     // its chains are not checked against the bound (census[stopped] counts it instead).
+    if (C.want_dig) C.flush(lane);
     const uint64_t digest = warp_sum_u64(C.dig);
     bool viol = false, set_sched = bound != nullptr && stop == PAAM_SIM_OK;
     uint64_t bd = 0;
@@ -755,7 +794,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
 
 #ifndef PAAM_WARP_EMU
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
-                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket, cudaStream_t st) {
+                    uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket,
+                    void** scratch, size_t* scratch_bytes, cudaStream_t st) {
   if (n == 0) return PAAM_OK;
   cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   int dev = 0, sms = 148, per_sm = 1;
@@ -766,7 +806,20 @@ int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t
   const uint32_t need = (n + SW - 1) / SW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, *out, ticket);
+  uint4* evbuf = nullptr;
+  if (out->digest) {  // the event buffers of every resident warp (EVCAP records of 16 B each)
+    const size_t bytes = (size_t)grid * SW * EVCAP * sizeof(uint4);
+    if (*scratch_bytes < bytes) {
+      if (*scratch) cudaFree(*scratch);
+      *scratch = nullptr;
+      *scratch_bytes = 0;
+      const cudaError_t e = cudaMalloc(scratch, bytes);
+      if (e != cudaSuccess) return fail_cuda(e, "simulate event buffers");
+      *scratch_bytes = bytes;
+    }
+    evbuf = (uint4*)*scratch;
+  }
+  simulate_kernel<<<grid, SW * 32, 0, st>>>(*b, rec, n, horizon, seed, first_index, sim_flags, *out, ticket, evbuf);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "simulate_kernel launch");

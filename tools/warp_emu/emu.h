@@ -30,6 +30,7 @@ inline thread_local dim3emu threadIdx, blockIdx;
 inline dim3emu gridDim{1, 1, 1}, blockDim{32, 1, 1};
 
 struct uint4 { uint32_t x, y, z, w; };
+inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return uint4{x, y, z, w}; }
 struct uint2 { uint32_t x, y; };
 template <class T> inline T __ldg(const T* p) { return *p; }
 
