@@ -59,13 +59,13 @@ constexpr uint32_t NOQ = 0xffu;  // wunit of a request that is not queued
 struct InstWide {
   uint32_t k, seq;
   union {
-    uint64_t ready_at;  // I_TRANSIT: arrival of the next callback (D13)
+    uint32_t ready_at;  // I_TRANSIT: arrival of the next callback (D13), low 32 bits (see Ctx::t32)
     uint32_t rem;       // a preempted request: its remaining accelerator work
   };
 };
 struct InstRef {
   uint8_t &state, &cb, &wunit, &started;  // wunit: the unit a waiting request is queued on, else NOQ
-  uint64_t& ready_at;
+  uint32_t& ready_at;
   uint32_t &k, &seq, &rem;
 };
 __device__ __forceinline__ uint8_t& byte_of(uint32_t& w, uint32_t q) { return reinterpret_cast<uint8_t*>(&w)[q]; }
@@ -101,10 +101,9 @@ struct DesSmem {
                    w.ready_at, w.k, w.seq, w.rem};
   }
   uint32_t exRem[MAXX];
-  uint64_t exTimer[MAXX];
+  uint32_t exTimer[MAXX];  // P_EPS_SUSP: end of the eps timer (low 32 bits)
   uint8_t exChain[MAXX], exSlot[MAXX], exSeg[MAXX], exPhase[MAXX];
-  uint64_t unEnd[MAXU];
-  uint32_t unRem[MAXU];
+  uint32_t unEnd[MAXU];  // end of the unit's current phase (run / switch-out / switch-in), low 32 bits
   uint8_t unState[MAXU], unChain[MAXU], unSlot[MAXU];
   uint32_t uQ[MAXU];  // requests queued on the unit (waiting, started or not; the running one included)
   uint8_t uDirty[MAXU];  // a running unit's queue or running request changed since its last preemption check
@@ -132,8 +131,8 @@ __device__ __forceinline__ uint64_t fnv_field(uint64_t h, uint32_t v) {
   constexpr uint64_t P4 = 0x9ffaac085635bc91ull;  // P^4 mod 2^64, P = 0x100000001b3
   return (h ^ (v == 0xffffffffu ? 0xffu : v)) * P4;
 }
-// A buffered record: {t low, t high, kind | chain << 8 | callback << 16 | segment << 24, unit | bucket << 8},
-// one byte per field (0xff: does not apply).
+// A record: {t low, t high, kind | chain << 8 | callback << 16 | segment << 24, unit | bucket << 8}, one
+// byte per field (0xff: does not apply), chain = the set-local index (buffered as the rank).
 __device__ __forceinline__ uint64_t fnv_record(uint4 e) {
   uint64_t h = fnv_time(((uint64_t)e.y << 32) | e.x);
   h = fnv_field(h, e.z & 0xffu);
@@ -152,9 +151,13 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 
 __device__ __forceinline__ uint32_t ev_byte(uint32_t v) { return v == 0xffffffffu ? 0xffu : v; }
 
+// Every pending event lies less than 2^31 ns ahead of t (a period, eps, kappa, comm or remaining work,
+// each < 2^31 - 1 ns), so the absolute times of pending events are kept as their low 32 bits: equality
+// with t and the distance from t are exact in 32-bit arithmetic.
 struct Ctx {
   DesSmem& S;
   uint64_t t, horizon, comm;
+  __device__ uint32_t t32() const { return (uint32_t)t; }
   uint64_t dig;  // this lane's partial digest
   bool fifo;     // FIFO_DIRECT: no eps, no kappa, no buckets, arrival order
   bool want_dig; // the caller asked for digests (out_digest != NULL); otherwise events are not recorded
@@ -166,7 +169,7 @@ struct Ctx {
       if (i >= EVCAP) { fprintf(stderr, "simulate: event buffer overflow (%u, kind %u)\n", i, kind); abort(); }
 #endif
       evb[i] = make_uint4((uint32_t)t, (uint32_t)(t >> 32),
-                          kind | ((uint32_t)S.cLocal[c] << 8) | (ev_byte(cb) << 16) | (ev_byte(seg) << 24),
+                          kind | (c << 8) | (ev_byte(cb) << 16) | (ev_byte(seg) << 24),
                           ev_byte(unit) | (ev_byte(bk) << 8));
     }
   }
@@ -179,44 +182,45 @@ struct Ctx {
   __device__ void flush(uint32_t lane) {
     __syncwarp();
     const uint32_t n = S.evN;
-    for (uint32_t i = lane; i < n; i += 32) dig += fnv_record(evb[i]);
+    for (uint32_t i = lane; i < n; i += 32) {
+      uint4 e = evb[i];
+      e.z = (e.z & 0xffff00ffu) | ((uint32_t)S.cLocal[(e.z >> 8) & 0xffu] << 8);  // rank -> set-local chain
+      dig += fnv_record(e);
+    }
     __syncwarp();
     if (lane == 0) S.evN = 0;
     __syncwarp();
   }
-  // executor x has phase-A work due now (a zero-length eps leaves it due right after it starts)
-  __device__ bool exec_due(uint32_t x) const {
-    const uint32_t ph = S.exPhase[x];
-    return ((ph == P_CPU || ph == P_EPS_SPIN) && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == t);
-  }
-  // executor x starts segment exSeg[x] of its job's callback
-  __device__ void begin_segment(uint32_t x) {
+  // executor x starts segment exSeg[x] of its job's callback; true: it has phase-A work due now (a
+  // zero-length eps; CPU segments are never zero-length)
+  __device__ bool begin_segment(uint32_t x) {
     const uint32_t c = S.exChain[x], sl = S.exSlot[x];
     const uint32_t j = S.cCb0[c] + S.ref(c, sl).cb;
     const uint32_t g = S.bSeg0[j] + S.exSeg[x];
     if (S.gKind[g] == 0) {
       S.exPhase[x] = P_CPU;
       S.exRem[x] = S.gW[g];
-    } else {
-      const uint32_t eps = fifo ? 0u : S.uEps[S.gUnit[g]];
-      if (S.xWait[x]) { S.exPhase[x] = P_EPS_SPIN; S.exRem[x] = eps; }
-      else { S.exPhase[x] = P_EPS_SUSP; S.exTimer[x] = t + eps; }
+      return false;
     }
+    const uint32_t eps = fifo ? 0u : S.uEps[S.gUnit[g]];
+    if (S.xWait[x]) { S.exPhase[x] = P_EPS_SPIN; S.exRem[x] = eps; }
+    else { S.exPhase[x] = P_EPS_SUSP; S.exTimer[x] = t32() + eps; }
+    return eps == 0;
   }
-  // executor x finished the current segment (D12, D13, D16)
-  __device__ void advance_segment(uint32_t x) {
+  // executor x finished the current segment (D12, D13, D16); true: it has phase-A work due now
+  __device__ bool advance_segment(uint32_t x) {
     const uint32_t c = S.exChain[x], sl = S.exSlot[x];
     InstRef I = S.ref(c, sl);
     const uint32_t j = S.cCb0[c] + I.cb;
     ev(EV_SEG_DONE, c, I.cb, S.exSeg[x], FULL, FULL);
     S.exSeg[x]++;
-    if (S.exSeg[x] < S.bNseg[j]) { begin_segment(x); return; }
+    if (S.exSeg[x] < S.bNseg[j]) return begin_segment(x);
     ev(EV_CB_DONE, c, I.cb, FULL, FULL, FULL);
     if (I.cb + 1u < S.cNcb[c]) {
       const uint32_t nx = S.bExec[j + 1];
       I.cb++;
       if (nx == x) I.state = I_READY;
-      else { I.state = I_TRANSIT; I.ready_at = t + comm; }
+      else { I.state = I_TRANSIT; I.ready_at = t32() + (uint32_t)comm; }
     } else {
       const uint64_t resp = t - (S.cPhase[c] + (uint64_t)I.k * S.cT[c]);  // D16
       atomicMax(&S.maxResp[c], (unsigned long long)resp);
@@ -227,6 +231,7 @@ struct Ctx {
     }
     S.exPhase[x] = P_NONE;
     S.exChain[x] = 0xff;
+    return false;
   }
 };
 
@@ -415,13 +420,22 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     uint32_t seq = 0;     // warp-uniform
     bool on_core = false; // lane = canonical executor
     uint32_t drops = 0;
-    uint64_t steps = 0;
+    uint32_t steps = 0;  // STEP_CAP < 2^32
     int32_t stop = PAAM_SIM_OK;  // warp-uniform: why the run stopped early (PAAM_SIM_BACKLOG / _STEPCAP)
     bool backlog = false;         // lane = chain: a release found every instance slot live
     const bool is_chain = lane < nch, is_exec = lane < nex, is_unit = lane < n_unit;
     // this lane's unit / executor / chain has an event due at the current t (set by the time advance from
     // the lane's own minima; a repeated pass of phase A runs with all three set)
     bool due_u = true, due_x = true, due_c = true;
+    // lane-owned static facts of the set, kept in registers
+    const uint32_t same_core = is_exec ? S.xSameCore[lane] : 0u;  // executors on this executor's core
+    const uint32_t run_phases =  // phases (other than idle) in which this executor wants its core (D5)
+        (1u << P_CPU) | (1u << P_EPS_SPIN) | ((is_exec && S.xWait[lane]) ? (1u << P_WAIT) : 0u);
+    const bool preemptive = is_unit && S.uN[lane] > 1;  // a unit of a multi-bucket accelerator (D9)
+    bool may_transit = false;  // chain lane: a callback of the chain is followed by one on another executor
+    if (is_chain)
+      for (uint32_t j = S.cCb0[lane]; j + 1 < (uint32_t)S.cCb0[lane] + S.cNcb[lane]; j++)
+        may_transit |= S.bExec[j] != S.bExec[j + 1];
 
     for (;;) {
       // ===================== settle time t (D15) =====================
@@ -435,14 +449,15 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         while (run_a) {
           if (C.want_dig && C.must_flush()) C.flush(lane);
           // (1) units.  Only a unit whose phase end or completion is due at t has anything to do here.
-          if (is_unit && due_u) {
+          if (is_unit && due_u && S.unState[lane] != U_IDLE && S.unEnd[lane] == C.t32()) {
             const uint32_t u = lane;
-            if ((S.unState[u] == U_SWOUT || S.unState[u] == U_SWIN) && S.unEnd[u] == C.t) {
-              if (S.unState[u] == U_SWOUT) S.unState[u] = U_IDLE;
-              else { S.unState[u] = U_RUN; S.unRem[u] = S.ref(S.unChain[u], S.unSlot[u]).rem; S.uDirty[u] = 1; }
-             
-            }
-            if (S.unState[u] == U_RUN && S.unRem[u] == 0) {
+            const uint32_t us = S.unState[u];
+            if (us == U_SWOUT) S.unState[u] = U_IDLE;
+            else if (us == U_SWIN) {
+              S.unState[u] = U_RUN;
+              S.unEnd[u] = C.t32() + S.ref(S.unChain[u], S.unSlot[u]).rem;  // > t: the rest of the request
+              S.uDirty[u] = 1;
+            } else if (us == U_RUN) {  // due: the request completes now
               const uint32_t c = S.unChain[u], sl = S.unSlot[u];
               InstRef I = S.ref(c, sl);
               const uint32_t j = S.cCb0[c] + I.cb;
@@ -453,18 +468,18 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               I.wunit = NOQ;
               S.uQ[u]--;
               S.unState[u] = U_IDLE;
-              C.advance_segment(x);
-             
+              C.advance_segment(x);  // the next segment is a CPU one or none: never due now
             }
           }
           __syncwarp();
           // (2) executors: CPU / eps completions; enqueues sequenced by (chain, instance) (D7)
-          bool enq = false, adv = false;
+          bool enq = false;
           uint32_t enq_key = 0xffffffffu;
+          bool again_x = false;  // an executor (2) advanced is due again (its next segment is a zero-length eps)
           if (is_exec && due_x) {  // (1) leaves no executor due: a callback's next segment is never zero-length
             const uint32_t x = lane, ph = S.exPhase[x];
-            if (ph == P_CPU && S.exRem[x] == 0) { C.advance_segment(x); adv = true; }
-            else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t)) {
+            if (ph == P_CPU && S.exRem[x] == 0) again_x = C.advance_segment(x);
+            else if ((ph == P_EPS_SPIN && S.exRem[x] == 0) || (ph == P_EPS_SUSP && S.exTimer[x] == C.t32())) {
               S.exPhase[x] = P_WAIT;
               enq = true;
               enq_key = ((uint32_t)S.cLocal[S.exChain[x]] << 24) | (S.ref(S.exChain[x], S.exSlot[x]).k & 0xffffffu);
@@ -472,8 +487,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             }
           }
           // (2) served every executor that was due, and advance_segment(x) changes executor x only, so
-          // only an executor (2) advanced can be due again (its next segment may be zero-length)
-          const bool again_x = adv && C.exec_due(lane);  // final for this pass: (3)/(4) leave executors alone
+          // only an executor (2) advanced can be due again; (3)/(4) leave executors alone
           const uint32_t enq_mask = __ballot_sync(FULL, enq);
           if (enq_mask) {
             uint32_t pos = 0;
@@ -500,10 +514,11 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           // (3) comm arrivals, (4) releases (D2, D14)
           if (is_chain && due_c) {
             const uint32_t c = lane;
-            for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
-              const uint32_t q = slot_of(tm);
-              if (S.iw[c][q].ready_at == C.t) { byte_of(S.iState[c], q) = I_READY; }
-            }
+            if (may_transit)
+              for (uint32_t tm = slots_eq(S.iState[c], I_TRANSIT); tm; tm &= tm - 1) {
+                const uint32_t q = slot_of(tm);
+                if (S.iw[c][q].ready_at == C.t32()) { byte_of(S.iState[c], q) = I_READY; }
+              }
             const uint64_t r = next_rel;
             if (r == C.t && r < horizon) {
               if (S.cCls[c] == 1)
@@ -544,6 +559,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         const uint32_t has_ready = __reduce_or_sync(FULL, ready_x);
         const uint32_t want = __ballot_sync(FULL, is_exec && on_core && S.exPhase[lane] == P_NONE && ((has_ready >> lane) & 1u));
         uint32_t wm = want;
+        uint32_t hr = has_ready;  // (6) needs the chains' offers after (5)
+        if (wm) {
         while (wm) {
           const uint32_t x = __ffs(wm) - 1;
           wm &= wm - 1;
@@ -565,8 +582,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             S.exSlot[x] = (uint8_t)best;
             S.exSeg[x] = 0;
             C.ev(EV_CB_START, c, I.cb, 0, FULL, FULL);
-            C.begin_segment(x);
-            dueB |= C.exec_due(x);
+            dueB |= C.begin_segment(x);
             // this chain no longer offers that instance
             ready_x = 0;
             {
@@ -577,19 +593,19 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           }
           __syncwarp();
         }
-        // (6) core dispatch (D5): highest process priority runnable executor per core.  ready_x is
+        hr = __reduce_or_sync(FULL, ready_x);
+        }
+        // (6) core dispatch (D5): highest process priority runnable executor per core.  ready_x (hr) is
         // current: (5) recomputed it on every chain lane whose instance it started.
         {
-          const uint32_t hr = __reduce_or_sync(FULL, ready_x);
           bool run = false;
           if (is_exec) {
             const uint32_t ph = S.exPhase[lane];
-            run = ph == P_NONE ? ((hr >> lane) & 1u) : (ph == P_CPU || ph == P_EPS_SPIN) ? true
-                : ph == P_WAIT ? (S.xWait[lane] != 0) : false;
+            run = ph == P_NONE ? ((hr >> lane) & 1u) : ((run_phases >> ph) & 1u);
           }
           const uint32_t R = __ballot_sync(FULL, run);
-          const uint32_t cand = is_exec ? (R & S.xSameCore[lane]) : 0u;
-          const bool oc = cand && (__ffs(cand) - 1 == lane);
+          const uint32_t cand = R & same_core;  // same_core = 0 on a lane that is no executor
+          const bool oc = cand != 0 && (cand & (0u - cand)) == (1u << lane);  // the lowest is this lane
           // an executor that just got its core while idle with ready work is the only thing another
           // phase-B pass could act on ((5) serves every wanting executor once per pass; (7) units are
           // independent of each other)
@@ -607,7 +623,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             // check would repeat its last, negative, outcome)
             const uint32_t ust = S.unState[lane], q = S.uQ[lane];
             cand = fifo ? (ust == U_IDLE && q > 0)
-                        : ((ust == U_IDLE && q > 0) || (ust == U_RUN && S.uN[lane] > 1 && q > 1 && S.uDirty[lane]));
+                        : ((ust == U_IDLE && q > 0) || (ust == U_RUN && preemptive && q > 1 && S.uDirty[lane]));
             S.uDirty[lane] = 0;
           }
           umask = __ballot_sync(FULL, cand);
@@ -632,7 +648,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               S.unSlot[u] = (uint8_t)fslot;
               I.started = 1;
               S.unState[u] = U_RUN;
-              S.unRem[u] = S.gW[S.bSeg0[j] + seg];
+              S.unEnd[u] = C.t32() + S.gW[S.bSeg0[j] + seg];
               C.ev(EV_ACC_START, lane, I.cb, seg, u, 0u);
             }
             __syncwarp();
@@ -674,13 +690,13 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               S.unSlot[u] = (uint8_t)bslot;
               if (I.started) {  // D10: switch back in
                 S.unState[u] = U_SWIN;
-                S.unEnd[u] = C.t + S.uKap[u];
+                S.unEnd[u] = C.t32() + S.uKap[u];
                 dueB |= S.uKap[u] == 0;
                 C.ev(EV_ACC_RESUME, wc, I.cb, seg, u, wbkt);
               } else {
                 I.started = 1;
                 S.unState[u] = U_RUN;
-                S.unRem[u] = S.gW[S.bSeg0[j] + seg];
+                S.unEnd[u] = C.t32() + S.gW[S.bSeg0[j] + seg];
                 C.ev(EV_ACC_START, wc, I.cb, seg, u, wbkt);
               }
             }
@@ -693,9 +709,9 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             if (wbkt > rbkt) {
               if (lane == 0) {
                 C.ev(EV_ACC_PREEMPT, rc, R.cb, rseg, u, rbkt);
-                R.rem = S.unRem[u];
+                R.rem = S.unEnd[u] - C.t32();  // > 0: a request completing now finished in (1)
                 S.unState[u] = U_SWOUT;
-                S.unEnd[u] = C.t + S.uKap[u];
+                S.unEnd[u] = C.t32() + S.uKap[u];
                 dueB |= S.uKap[u] == 0;
               }
             }
@@ -713,25 +729,21 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       // Every pending event lies less than 2^31 ns ahead (a period, eps, kappa, comm or remaining
       // work, each < 2^31 - 1 ns), so the next event is found as a 32-bit distance from t.
       uint32_t nd_c = 0xffffffffu, nd_x = 0xffffffffu, nd_u = 0xffffffffu;  // none
-      bool run_x = false, run_u = false;  // executor / unit whose remaining work shrinks with time
+      bool run_x = false;  // executor whose remaining work shrinks with time
       if (is_chain) {
         const uint64_t r = next_rel;
         if (r < horizon) nd_c = (uint32_t)(r - C.t);
-        for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
-          nd_c = min(nd_c, (uint32_t)(S.iw[lane][slot_of(tm)].ready_at - C.t));
+        if (may_transit)
+          for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
+            nd_c = min(nd_c, S.iw[lane][slot_of(tm)].ready_at - C.t32());
       }
       if (is_exec) {
         const uint32_t ph = S.exPhase[lane];
         run_x = (ph == P_CPU || ph == P_EPS_SPIN) && on_core;
         if (run_x) nd_x = S.exRem[lane];
-        if (ph == P_EPS_SUSP) nd_x = (uint32_t)(S.exTimer[lane] - C.t);
+        if (ph == P_EPS_SUSP) nd_x = S.exTimer[lane] - C.t32();
       }
-      if (is_unit) {
-        const uint32_t us = S.unState[lane];
-        run_u = us == U_RUN;
-        if (run_u) nd_u = S.unRem[lane];
-        if (us == U_SWOUT || us == U_SWIN) nd_u = (uint32_t)(S.unEnd[lane] - C.t);
-      }
+      if (is_unit && S.unState[lane] != U_IDLE) nd_u = S.unEnd[lane] - C.t32();
       const uint32_t nd = __reduce_min_sync(FULL, min(nd_c, min(nd_x, nd_u)));
       if (nd == 0xffffffffu) break;
       // with comm = 0 a callback completing at t makes its successor arrive at t (D13), so every chain
@@ -742,7 +754,6 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       if (++steps > STEP_CAP) { stop = PAAM_SIM_STEPCAP; break; }
       const uint64_t nt = C.t + nd;
       if (run_x) S.exRem[lane] -= nd;
-      if (run_u) S.unRem[lane] -= nd;
       C.t = nt;
       __syncwarp();
     }
