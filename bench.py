@@ -10,9 +10,10 @@ recipe on 2M sets.
 
 Extra legs in the same JSON line: the kernel's per-launch time (roofline: HBM, issue and ALU views),
 the split entry points (paam_repack + paam_analyze) for reference, verdict_only (PAAM_FLAG_VERDICT_ONLY),
-e2e (the same metric from pinned host buffers through paam_pack_analyze with every WCRT copied back,
-H2D / D2H inside the timed region) and e2e_verdict_only, e2e_device_generate (paam_sweep: device
-generation included), des (config-5 leg: paam_simulate on 1M sets, 10 s horizon, sim <= bound
+e2e (the same metric from pinned host buffers through paam_pack_analyze32 -- the compact batch, 32-bit
+times and one byte per segment -- with every WCRT copied back, H2D / D2H inside the timed region),
+e2e_u64 (the same through paam_pack_analyze on the u64 batch), e2e_verdict_only, e2e_device_generate
+(paam_sweep: device generation included), des (config-5 leg: paam_simulate on 1M sets, 10 s horizon, sim <= bound
 census, misses / drops / stopped runs, with and without digests), cpu_baseline (the oracle).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -197,6 +198,10 @@ def workload_name(n: int) -> str:
             f"{n} sets/GPU, seed {SEED}, rank r owns [r*{n}, (r+1)*{n}) -- N=8 is config 4 (16M sets)")
 
 
+def batch32_bytes(b32) -> int:
+    return int(sum(a.nbytes for k, a in b32.arrays.items() if a is not None and not k.endswith("_pinned")))
+
+
 def batch_bytes(c) -> int:
     n, ch, cb, sg, ex, ac = c.n_sets, c.n_chains, c.n_cbs, c.n_segs, c.n_execs, c.n_accels
     return (3 * 4 * (n + 1) + ch * (8 + 8 + 4 + 1) + 4 * (ch + 1) + cb * 2 + 4 * (cb + 1) + sg * (1 + 8 + 1 + 1)
@@ -357,7 +362,7 @@ def run_ours(args):
     # ---- e2e: the same metric through the C ABI with HOST buffers (copies inside the region) ------
     # Each step copies the pinned host batch in (chunked, overlapped with the kernel of earlier chunks)
     # and reads every WCRT, verdict and the bin counts back: the full output of the timed step.
-    e2e = e2e_vo = None
+    e2e = e2e_vo = e2e_u64 = None
     if not args.no_e2e:
         from gen.inputs import generate_host
 
@@ -395,17 +400,32 @@ def run_ours(args):
             for _ in range(args.steps):
                 e2e_step(batch, with_wcrt)
             return max_over_ranks(time.perf_counter() - t0, world)
-        e2e_s = timed(hb, True)
-        if not np.array_equal(wcrt_h.numpy(), wcrt.cpu().numpy()):
-            raise RuntimeError("e2e WCRTs differ from the device-resident run")
+        ref_w = wcrt.cpu().numpy()
+        d2h_full = 8 * hb.c.n_chains + n + 8 * 2 * gp.n_bins
+        u64_s = timed(hb, True)
+        if not np.array_equal(wcrt_h.numpy(), ref_w):
+            raise RuntimeError("e2e (u64 batch) WCRTs differ from the device-resident run")
+        e2e_u64 = {"value": world * n * args.steps / u64_s, "unit": "chain-sets/s",
+                   "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": d2h_full,
+                   "ms_per_step": 1e3 * u64_s / args.steps,
+                   "note": "paam_pack_analyze from pinned host buffers (u64 CSR batch, chunked H2D overlapped with "
+                           "the kernel) + D2H of every WCRT, verdict and bin count; host wall clock, max over ranks"}
+        # the compact batch (paam_batch32: the same sets in 32-bit times and one byte per segment), pinned
+        hb32 = paam.Batch32.from_host(host, pin=True)
+        hvb32 = paam.Batch32.from_host(dict(host, flags=paam.PAAM_FLAG_VERDICT_ONLY), pin=True)
+        wcrt_h.zero_()
+        e2e_s = timed(hb32, True)
+        if not np.array_equal(wcrt_h.numpy(), ref_w):
+            raise RuntimeError("e2e (compact batch) WCRTs differ from the device-resident run")
         e2e = {"value": world * n * args.steps / e2e_s, "unit": "chain-sets/s",
-               "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": 8 * hb.c.n_chains + n + 8 * 2 * gp.n_bins,
+               "h2d_bytes_per_step": batch32_bytes(hb32), "d2h_bytes_per_step": d2h_full,
                "ms_per_step": 1e3 * e2e_s / args.steps,
-               "note": "paam_pack_analyze from pinned host buffers (u64 CSR batch, chunked H2D overlapped with the "
-                       "kernel) + D2H of every WCRT, verdict and bin count; host wall clock, max over ranks"}
-        vo_s = timed(hvb, False)
+               "note": "paam_pack_analyze32 from pinned host buffers (the compact batch: 32-bit times, one byte per "
+                       "segment; chunked H2D overlapped with the kernel) + D2H of every WCRT, verdict and bin count; "
+                       "host wall clock, max over ranks.  e2e_u64: the same through the u64 batch"}
+        vo_s = timed(hvb32, False)
         e2e_vo = {"value": world * n * args.steps / vo_s, "unit": "chain-sets/s",
-                  "h2d_bytes_per_step": batch_bytes(hb.c), "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
+                  "h2d_bytes_per_step": batch32_bytes(hb32), "d2h_bytes_per_step": n + 8 * 2 * gp.n_bins,
                   "ms_per_step": 1e3 * vo_s / args.steps,
                   "note": "as e2e with PAAM_FLAG_VERDICT_ONLY: verdicts and bins only"}
         hsets.free()
@@ -518,6 +538,7 @@ def run_ours(args):
            "split_path": split, "bins": bins.cpu().tolist()}
     if e2e:
         out["e2e"] = e2e
+        out["e2e_u64"] = e2e_u64
         out["e2e_verdict_only"] = e2e_vo
     if e2e_gen:
         out["e2e_device_generate"] = e2e_gen

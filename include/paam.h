@@ -217,16 +217,58 @@ int paam_analyze(const paam_sets* sets, uint32_t n, uint64_t* out_wcrt, uint8_t*
  *   out_wcrt as in paam_analyze (may be NULL).  Device pointers only. */
 int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_t* out_wcrt, paam_stream_t stream);
 
-/* paam_pack_analyze -- steps 2-6 in one call, pipelined: the batch is cut into chunks whose
- * pack_kernel and analyze_kernel launches overlap on two internal streams (chunk i's analysis
- * runs while chunk i+1 is packed), joined back into `stream`.  A host batch is copied to the device
- * chunk by chunk on a third internal stream, each chunk's copy overlapping the kernels of the
- * previous chunks; with pinned host memory the copies are asynchronous, so the caller must not
- * modify the batch until `stream` has completed.  Same results as paam_repack followed by
- * paam_analyze; `sets` must have capacity for batch->n_sets (from paam_pack).  out_status is in the
- * batch's memory space; a host out_status makes the call synchronise `stream` (as paam_repack). */
+/* paam_pack_analyze -- steps 2-6 in one call: one fused kernel validates and derives each set and
+ * solves its fixed points with the derived record on chip (no record is written), followed by the
+ * exact u64 kernel for the sets it hands over (a time >= 2^31 - 1 ns).  A host batch is copied to the
+ * device in chunks on an internal stream, each chunk's copy overlapping the kernel of the previous
+ * chunk; with pinned host memory the copies are asynchronous, so the caller must not modify the batch
+ * until `stream` has completed.  Same results as paam_repack followed by paam_analyze; `sets` must
+ * have capacity for batch->n_sets (from paam_pack).  out_status is in the batch's memory space; a host
+ * out_status makes the call synchronise `stream` (as paam_repack).  The handle keeps the batch for a
+ * later paam_analyze / paam_admit / paam_simulate (which then pack it first). */
 int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
                       uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream);
+
+/* Compact batch: paam_batch with 32-bit times and one byte per segment, 1.4 KB instead of 2.3 KB per
+ * config-3 set, for host batches whose transfer bounds the call (the H2D copy of a host batch runs at
+ * the PCIe rate).  Layout and meaning as paam_batch, except:
+ *   chain_T, chain_D, seg_wcet, accel_eps, accel_kappa   uint32_t ns (a time below 2^32 ns; times
+ *                                                        >= 2^31 - 1 ns take the exact u64 path);
+ *   seg_meta   kind | accel << 1 | unit << 3 (kind 0 CPU / 1 ACCEL, set-local accelerator < 4,
+ *              unit < 8; for a CPU segment accel and unit are ignored) -- replaces seg_kind,
+ *              seg_accel and seg_unit;
+ *   cb_exec    uint8_t.
+ * Every value a paam_batch can express inside these ranges means the same; results are identical to
+ * paam_pack_analyze on the equivalent paam_batch. */
+typedef struct {
+  uint32_t n_sets;
+  int32_t mem; /* PAAM_MEM_HOST | PAAM_MEM_DEVICE */
+  uint32_t n_chains, n_cbs, n_segs, n_execs, n_accels, n_bins;
+  const uint32_t *set_chain_off, *set_exec_off, *set_accel_off; /* [n_sets+1] */
+  const uint32_t *chain_T, *chain_D;
+  const uint32_t *chain_prio;
+  const uint8_t *chain_class;
+  const uint32_t *chain_cb_off; /* [n_chains+1] */
+  const uint8_t *cb_exec;
+  const uint32_t *cb_seg_off;   /* [n_cbs+1] */
+  const uint8_t *seg_meta;
+  const uint32_t *seg_wcet;
+  const uint8_t *exec_core;
+  const uint32_t *exec_prio;
+  const uint8_t *exec_wait;
+  const uint8_t *accel_buckets, *accel_units, *accel_server_core;
+  const uint32_t *accel_eps, *accel_kappa;
+  const uint32_t *set_bin;
+  uint64_t comm_cost;
+  uint32_t flags;
+  uint32_t _pad;
+} paam_batch32;
+
+/* paam_pack_analyze32 -- paam_pack_analyze on a compact batch (same outputs, same errors).  The handle
+ * keeps no batch a later paam_analyze / paam_admit / paam_simulate could pack: those return
+ * PAAM_EINVAL until a paam_pack / paam_repack / paam_pack_analyze. */
+int paam_pack_analyze32(const paam_batch32* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
+                        uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream);
 
 /* paam_simulate -- §8(a) steps 7-8.  Discrete-event simulation of every set (DESIGN.md App. A,
  * rules D1-D17: PiCAS executors, fixed-priority cores, PAAM bucket queues with cross-bucket

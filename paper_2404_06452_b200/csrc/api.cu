@@ -27,6 +27,7 @@ struct paam_sets {
   int device;             // the CUDA device the handle lives on (made current by every call)
   void* sim_scratch;      // paam_simulate's event buffers (grown on demand)
   size_t sim_scratch_bytes;
+  bool c32;               // dev is a compact batch (paam_pack_analyze32): nothing can pack it into records
   bool rec_valid;         // rec holds the records of `dev` (false after the fused paam_pack_analyze, which writes
                           // none: the next paam_analyze / paam_admit / paam_simulate packs them first)
 };
@@ -62,22 +63,25 @@ inline int use_device(const paam_sets* s) {
 struct Field { const void** ptr; size_t elems, size; };
 
 // The array fields of a batch with their element counts (order of include/paam.h).
-int batch_fields(paam_batch* b, Field* f) {
+// c32: b carries a compact batch (paam_batch32 pointers: 4-byte times, 1-byte cb_exec, seg_kind = the
+// packed segment byte, no seg_accel / seg_unit).
+int batch_fields(paam_batch* b, Field* f, bool c32 = false) {
   const size_t nn = (size_t)b->n_sets + 1;
+  const size_t tz = c32 ? 4 : 8, sa = c32 ? 0 : b->n_segs;
   Field t[] = {
       {(const void**)&b->set_chain_off, nn, 4}, {(const void**)&b->set_exec_off, nn, 4},
       {(const void**)&b->set_accel_off, nn, 4},
-      {(const void**)&b->chain_T, b->n_chains, 8}, {(const void**)&b->chain_D, b->n_chains, 8},
+      {(const void**)&b->chain_T, b->n_chains, tz}, {(const void**)&b->chain_D, b->n_chains, tz},
       {(const void**)&b->chain_prio, b->n_chains, 4}, {(const void**)&b->chain_class, b->n_chains, 1},
       {(const void**)&b->chain_cb_off, (size_t)b->n_chains + 1, 4},
-      {(const void**)&b->cb_exec, b->n_cbs, 2}, {(const void**)&b->cb_seg_off, (size_t)b->n_cbs + 1, 4},
-      {(const void**)&b->seg_kind, b->n_segs, 1}, {(const void**)&b->seg_wcet, b->n_segs, 8},
-      {(const void**)&b->seg_accel, b->n_segs, 1}, {(const void**)&b->seg_unit, b->n_segs, 1},
+      {(const void**)&b->cb_exec, b->n_cbs, c32 ? 1u : 2u}, {(const void**)&b->cb_seg_off, (size_t)b->n_cbs + 1, 4},
+      {(const void**)&b->seg_kind, b->n_segs, 1}, {(const void**)&b->seg_wcet, b->n_segs, tz},
+      {(const void**)&b->seg_accel, sa, 1}, {(const void**)&b->seg_unit, sa, 1},
       {(const void**)&b->exec_core, b->n_execs, 1}, {(const void**)&b->exec_prio, b->n_execs, 4},
       {(const void**)&b->exec_wait, b->n_execs, 1},
       {(const void**)&b->accel_buckets, b->n_accels, 1}, {(const void**)&b->accel_units, b->n_accels, 1},
-      {(const void**)&b->accel_server_core, b->n_accels, 1}, {(const void**)&b->accel_eps, b->n_accels, 8},
-      {(const void**)&b->accel_kappa, b->n_accels, 8},
+      {(const void**)&b->accel_server_core, b->n_accels, 1}, {(const void**)&b->accel_eps, b->n_accels, tz},
+      {(const void**)&b->accel_kappa, b->n_accels, tz},
       {(const void**)&b->set_bin, b->set_bin ? (size_t)b->n_sets : 0, 4}};
   const int n = sizeof(t) / sizeof(t[0]);
   for (int i = 0; i < n; i++) f[i] = t[i];
@@ -121,13 +125,15 @@ int ensure_streams(paam_sets* sets) {
 int ensure_records(const paam_sets* cs, cudaStream_t st) {
   paam_sets* sets = const_cast<paam_sets*>(cs);
   if (sets->rec_valid) return PAAM_OK;
+  if (sets->c32)
+    return fail(PAAM_EINVAL, "the handle holds a compact batch (paam_pack_analyze32): paam_pack / paam_repack first");
   cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
   if (int rc = launch_pack(&sets->dev, sets->rec, nullptr, sets->wide_list, sets->tickets + 20, st)) return rc;
   sets->rec_valid = true;
   return PAAM_OK;
 }
 
-int check_batch(const paam_batch* b) {
+int check_batch(const paam_batch* b, bool c32 = false) {
   if (!b) return fail(PAAM_EINVAL, "NULL batch");
   if (b->mem != PAAM_MEM_HOST && b->mem != PAAM_MEM_DEVICE) return fail(PAAM_EINVAL, "batch.mem must be HOST or DEVICE");
   if (b->comm_cost >= LIMW) return fail(PAAM_EINVAL, "batch.comm_cost must be < 2^48 ns");
@@ -136,7 +142,7 @@ int check_batch(const paam_batch* b) {
   if (b->set_bin && b->n_bins == 0) return fail(PAAM_EINVAL, "set_bin given with n_bins == 0");
   paam_batch c = *b;
   Field f[32];
-  const int nf = batch_fields(&c, f);
+  const int nf = batch_fields(&c, f, c32);
   for (int i = 0; i < nf; i++)
     if (f[i].elems && !*f[i].ptr && f[i].ptr != (const void**)&c.set_bin)
       return fail(PAAM_EINVAL, "NULL array in a batch with a non-zero count");
@@ -199,6 +205,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
   sets->comm = batch->comm_cost;
   sets->flags = batch->flags;
   sets->rec_valid = true;
+  sets->c32 = false;
   return PAAM_OK;
 }
 
@@ -285,9 +292,12 @@ extern "C" int paam_simulate(const paam_sets* sets, uint32_t n, uint64_t horizon
                          &ms->sim_scratch, &ms->sim_scratch_bytes, (cudaStream_t)stream);
 }
 
-extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
-                                 uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream) {
-  int rc = check_batch(batch);
+namespace paam {
+namespace {
+// paam_pack_analyze on a u64 batch or (c32) on a compact batch carried in a paam_batch
+int pack_analyze_impl(const paam_batch* batch, bool c32, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
+                      uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream) {
+  int rc = check_batch(batch, c32);
   if (rc) return rc;
   if (!sets) return fail(PAAM_EINVAL, "NULL handle");
   if (batch->n_sets > sets->cap) return fail(PAAM_EINVAL, "paam_pack_analyze: handle capacity too small");
@@ -300,16 +310,17 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   const uint32_t n = batch->n_sets;
   const int64_t* bins = batch->set_bin ? out_bins : nullptr;
   paam_batch d = *batch;  // the batch the kernel reads (host: pointers into the staging buffer)
+  d._pad = 0;
   int32_t* status_dev = out_status;
   if (!host) {
     // steps 2-6 in one kernel (fused.cu): the derived records stay on chip
     cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
     if ((rc = launch_fused(&d, sets->wide_list, sets->tickets + 20, status_dev, out_wcrt, out_sched,
-                           const_cast<int64_t*>(bins), st)))
+                           const_cast<int64_t*>(bins), st, c32)))
       return rc;
     // the sets it handed over (a time >= 2^31 - 1 ns): exact u64 path
     if ((rc = launch_wide(&d, sets->wide_list, sets->tickets + 20, status_dev, out_wcrt, out_sched,
-                          const_cast<int64_t*>(bins), nullptr, st)))
+                          const_cast<int64_t*>(bins), nullptr, st, c32)))
       return rc;
   } else {
     // Host batch: K chunks; chunk i's slice of every array is copied H2D on side[2] while the kernel of
@@ -322,7 +333,7 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
     const int K = n < 4096 ? 1 : KH;
     if ((rc = ensure_streams(sets))) return rc;
     Field f[32];
-    const int nf = batch_fields(&d, f);
+    const int nf = batch_fields(&d, f, c32);
     size_t foff[32];
     // The chunk copies read the host CSR offsets at chunk boundaries: they must be monotone and within
     // the declared totals (include/paam.h), else a copy range would be wrong or out of bounds.
@@ -368,7 +379,7 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
                                {lo, hi}};
       Field hf[32];
       paam_batch hcopy = *batch;
-      batch_fields(&hcopy, hf);
+      batch_fields(&hcopy, hf, c32);
       for (int k = 0; k < nf; k++) {  // one cudaMemcpyAsync per array slice (no batched-copy APIs)
         if (!f[k].elems || r[k][1] <= r[k][0]) continue;
         const size_t sz = f[k].size;
@@ -387,10 +398,11 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
       cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), sets->side[0]);
       if ((rc = launch_fused(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
                              out_sched ? out_sched + lo : nullptr,
-                             const_cast<int64_t*>(bins), sets->side[0])))
+                             const_cast<int64_t*>(bins), sets->side[0], c32)))
         return rc;
       if ((rc = launch_wide(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
-                            out_sched ? out_sched + lo : nullptr, const_cast<int64_t*>(bins), nullptr, sets->side[0])))
+                            out_sched ? out_sched + lo : nullptr, const_cast<int64_t*>(bins), nullptr, sets->side[0],
+                            c32)))
         return rc;
     }
     cudaEventRecord(sets->ev[9], sets->side[0]);
@@ -411,7 +423,42 @@ extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32
   sets->comm = batch->comm_cost;
   sets->flags = batch->flags;
   sets->rec_valid = false;  // the fused kernel wrote no records
+  sets->c32 = c32;
   return PAAM_OK;
+}
+}  // namespace
+}  // namespace paam
+
+extern "C" int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
+                                 uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream) {
+  return pack_analyze_impl(batch, false, sets, out_status, out_wcrt, out_sched, out_bins, stream);
+}
+
+extern "C" int paam_pack_analyze32(const paam_batch32* b32, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
+                                   uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream) {
+  if (!b32) return fail(PAAM_EINVAL, "NULL batch");
+  // the compact arrays travel in a paam_batch (the kernels read them through ld_time / ld_seg)
+  paam_batch b{};
+  b.n_sets = b32->n_sets; b.mem = b32->mem;
+  b.n_chains = b32->n_chains; b.n_cbs = b32->n_cbs; b.n_segs = b32->n_segs;
+  b.n_execs = b32->n_execs; b.n_accels = b32->n_accels; b.n_bins = b32->n_bins;
+  b.set_chain_off = b32->set_chain_off; b.set_exec_off = b32->set_exec_off; b.set_accel_off = b32->set_accel_off;
+  b.chain_T = reinterpret_cast<const uint64_t*>(b32->chain_T);
+  b.chain_D = reinterpret_cast<const uint64_t*>(b32->chain_D);
+  b.chain_prio = b32->chain_prio; b.chain_class = b32->chain_class; b.chain_cb_off = b32->chain_cb_off;
+  b.cb_exec = reinterpret_cast<const uint16_t*>(b32->cb_exec);
+  b.cb_seg_off = b32->cb_seg_off;
+  b.seg_kind = b32->seg_meta;
+  b.seg_wcet = reinterpret_cast<const uint64_t*>(b32->seg_wcet);
+  b.seg_accel = nullptr; b.seg_unit = nullptr;
+  b.exec_core = b32->exec_core; b.exec_prio = b32->exec_prio; b.exec_wait = b32->exec_wait;
+  b.accel_buckets = b32->accel_buckets; b.accel_units = b32->accel_units;
+  b.accel_server_core = b32->accel_server_core;
+  b.accel_eps = reinterpret_cast<const uint64_t*>(b32->accel_eps);
+  b.accel_kappa = reinterpret_cast<const uint64_t*>(b32->accel_kappa);
+  b.set_bin = b32->set_bin;
+  b.comm_cost = b32->comm_cost; b.flags = b32->flags; b._pad = 0;
+  return pack_analyze_impl(&b, true, sets, out_status, out_wcrt, out_sched, out_bins, stream);
 }
 
 extern "C" int paam_sets_info(const paam_sets* sets, uint32_t* n_sets, uint32_t* n_chains, uint32_t* n_bins) {

@@ -33,6 +33,30 @@ constexpr uint32_t SAT = 0x7FFFFFFFu;
 constexpr uint64_t LIM = 0x7FFFFFFFull;  // the u32 kernels take the sets whose every time is < LIM (A14)
 
 __device__ __forceinline__ uint32_t sadd(uint32_t a, uint32_t b) { return min(a + b, SAT); }  // a,b <= SAT
+
+// Raw-batch loads for the u64 batch (C32 = false) or the compact batch (C32 = true, paam_batch32): a
+// compact batch travels in a paam_batch whose pointers are paam_batch32's -- the times uint32_t,
+// cb_exec uint8_t, seg_kind the packed segment byte kind | accel << 1 | unit << 3 (seg_accel / seg_unit
+// unused).
+template <bool C32>
+__device__ __forceinline__ uint64_t ld_time(const uint64_t* p, size_t i) {
+  if constexpr (C32) return reinterpret_cast<const uint32_t*>(p)[i];
+  else return p[i];
+}
+template <bool C32>
+__device__ __forceinline__ uint32_t ld_cb_exec(const paam_batch& b, size_t j) {
+  if constexpr (C32) return reinterpret_cast<const uint8_t*>(b.cb_exec)[j];
+  else return b.cb_exec[j];
+}
+template <bool C32>
+__device__ __forceinline__ void ld_seg(const paam_batch& b, size_t g, uint32_t& kind, uint32_t& accel, uint32_t& unit) {
+  if constexpr (C32) {
+    const uint32_t m = b.seg_kind[g];
+    kind = m & 1u; accel = (m >> 1) & 3u; unit = m >> 3;
+  } else {
+    kind = b.seg_kind[g]; accel = b.seg_accel[g]; unit = b.seg_unit[g];
+  }
+}
 __device__ __forceinline__ uint32_t smul(uint32_t a, uint32_t b) {
   const uint64_t p = (uint64_t)a * b;
   return p > SAT ? SAT : (uint32_t)p;
@@ -155,11 +179,12 @@ int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
                    cudaStream_t st, int32_t* out_fail = nullptr);
 // §8(a) steps 2-6 in one kernel (fused.cu): no record is written
+// c32: b carries a compact batch (paam_batch32, see ld_time)
 int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
-                 uint8_t* out_sched, int64_t* out_bins, cudaStream_t st);
+                 uint8_t* out_sched, int64_t* out_bins, cudaStream_t st, bool c32 = false);
 // the exact u64 path over the sets listed by the u32 kernels (wide.cu); out_fail: admission decisions
 int launch_wide(const paam_batch* b, const uint32_t* list, const uint32_t* count, int32_t* status, uint64_t* out_wcrt,
-                uint8_t* out_sched, int64_t* out_bins, int32_t* out_fail, cudaStream_t st);
+                uint8_t* out_sched, int64_t* out_bins, int32_t* out_fail, cudaStream_t st, bool c32 = false);
 // scratch / scratch_bytes: the caller's device scratch for the DES event buffers (grown on demand)
 int launch_simulate(const paam_batch* b, const Record* rec, uint32_t n, uint64_t horizon, uint64_t seed,
                     uint64_t first_index, uint32_t sim_flags, const paam_sim_out* out, unsigned int* ticket,

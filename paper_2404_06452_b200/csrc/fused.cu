@@ -271,6 +271,8 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
 #ifndef FUSED_MINB
 #define FUSED_MINB 4  // 4 blocks of 8 warps (7 KB of shared memory per warp): 32 warps, 64 registers
 #endif
+// C32: b carries a compact batch (paam_batch32; common.cuh ld_time)
+template <bool C32>
 __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     fused_kernel(paam_batch b, uint32_t* __restrict__ wide_list, uint32_t* __restrict__ wide_count,
                  int32_t* __restrict__ status_out, uint64_t* __restrict__ out_wcrt,
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       bool erange = false, edang = false, eaccel = false, eshape = false, edup = false, edl = false, ecore = false;
       bool wide = false;  // a time in [2^31 - 1, 2^48) ns: the set goes to the u64 path
       if (lane < (int)nch) {
-        const uint64_t T64 = b.chain_T[c0 + lane], D64 = b.chain_D[c0 + lane];
+        const uint64_t T64 = ld_time<C32>(b.chain_T, c0 + lane), D64 = ld_time<C32>(b.chain_D, c0 + lane);
         erange |= (T64 == 0 || T64 >= LIMW || D64 >= LIMW);
         wide |= (T64 >= LIM || D64 >= LIM);  // exact only on the u64 path (wide.cu)
         T = (uint32_t)min(T64, (uint64_t)SAT);
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       }
       if (lane < (int)nac) {
         const uint32_t n = b.accel_buckets[a0 + lane], u = b.accel_units[a0 + lane];
-        const uint64_t e = b.accel_eps[a0 + lane], kp = b.accel_kappa[a0 + lane];
+        const uint64_t e = ld_time<C32>(b.accel_eps, a0 + lane), kp = ld_time<C32>(b.accel_kappa, a0 + lane);
         erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= LIMW || kp >= LIMW);
         wide |= (e >= LIM || kp >= LIM);
         s.aN[lane] = n;
@@ -379,8 +381,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       // ---- segments: lane per segment, staged with their per-segment validation
       #pragma unroll 2  // two passes' loads in flight
       for (uint32_t i = lane; i < nseg; i += 32) {
-        const uint64_t w = b.seg_wcet[sg0 + i];
-        const uint32_t kind = b.seg_kind[sg0 + i], a = b.seg_accel[sg0 + i], u = b.seg_unit[sg0 + i];
+        const uint64_t w = ld_time<C32>(b.seg_wcet, sg0 + i);
+        uint32_t kind, a, u;
+        ld_seg<C32>(b, sg0 + i, kind, a, u);
         erange |= (w >= LIMW);
         wide |= (w >= LIM);
         eshape |= (kind > 1) || (w == 0);
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         const uint32_t j = pass * 32 + lane;
         uint32_t exec = 0xffffffffu, E = 0, na = 0, fa = 0, fu = 0, fw = 0;
         if (j < ncb) {
-          exec = b.cb_exec[cb0 + j];
+          exec = ld_cb_exec<C32>(b, cb0 + j);
           uint32_t so = b.cb_seg_off[cb0 + j], se = b.cb_seg_off[cb0 + j + 1];
           edang |= (se == so) || (exec >= nex);
           if (so < sg0 || se < so || se > sg1) { malformed = true; so = se = sg0; }
@@ -852,25 +855,34 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
 }  // namespace
 
 #ifndef PAAM_WARP_EMU
-int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
-                 uint8_t* out_sched, int64_t* out_bins,
-                 cudaStream_t st) {
-  if (b->n_sets == 0) return PAAM_OK;
+namespace {
+template <bool C32>
+int launch_fused_t(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
+                   uint8_t* out_sched, int64_t* out_bins, cudaStream_t st) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   constexpr size_t SMEM = FW * sizeof(FSmem);
-  static const cudaError_t attr = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(fused_kernel<C32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
   if (attr != cudaSuccess) return fail_cuda(attr, "fused_kernel: shared memory attribute");
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel, FW * 32, SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<C32>, FW * 32, SMEM);
   if (per_sm < 1) per_sm = 1;
   const uint32_t need = (b->n_sets + FW - 1) / FW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  fused_kernel<<<grid, FW * 32, SMEM, st>>>(*b, wide_list, wide_count, status, out_wcrt, out_sched, out_bins);
+  fused_kernel<C32><<<grid, FW * 32, SMEM, st>>>(*b, wide_list, wide_count, status, out_wcrt, out_sched, out_bins);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "fused_kernel launch");
+}
+}  // namespace
+
+int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
+                 uint8_t* out_sched, int64_t* out_bins, cudaStream_t st, bool c32) {
+  if (b->n_sets == 0) return PAAM_OK;
+  return c32 ? launch_fused_t<true>(b, wide_list, wide_count, status, out_wcrt, out_sched, out_bins, st)
+             : launch_fused_t<false>(b, wide_list, wide_count, status, out_wcrt, out_sched, out_bins, st);
 }
 #endif  // PAAM_WARP_EMU
 

@@ -55,7 +55,9 @@ struct WSet {
   uint64_t sE[MAXS], smaxE[MAXS], seps[MAXS], sbase3[MAXS], sS[MAXS], sR[MAXS], sHs[MAXS];
 };
 
-// Validation in the order of include/paam.h; returns PAAM_SET_* and fills the set.
+// Validation in the order of include/paam.h; returns PAAM_SET_* and fills the set.  C32: b
+// carries a compact batch (common.cuh ld_time).
+template <bool C32>
 __device__ int w_load(const paam_batch& b, uint32_t set, WSet& s, uint32_t& nch, uint32_t& ncb, uint32_t& nq,
                       uint32_t& nex, uint32_t& nac, uint32_t& nsub) {
   const uint32_t c0 = b.set_chain_off[set], c1 = b.set_chain_off[set + 1];
@@ -78,7 +80,7 @@ __device__ int w_load(const paam_batch& b, uint32_t set, WSet& s, uint32_t& nch,
   uint32_t units_total = 0;
   for (uint32_t a = 0; a < nac; a++) {
     const uint32_t n = b.accel_buckets[a0 + a], u = b.accel_units[a0 + a];
-    const uint64_t e = b.accel_eps[a0 + a], k = b.accel_kappa[a0 + a];
+    const uint64_t e = ld_time<C32>(b.accel_eps, a0 + a), k = ld_time<C32>(b.accel_kappa, a0 + a);
     erange |= (n < 1 || n > 32 || u < 1 || u > 8 || e >= W_LIM || k >= W_LIM);
     s.nb[a] = n; s.nu[a] = u; s.ub[a] = units_total; s.server[a] = b.accel_server_core[a0 + a];
     s.eps[a] = e; s.keff[a] = n > 1 ? k : 0;  // A6
@@ -86,7 +88,7 @@ __device__ int w_load(const paam_batch& b, uint32_t set, WSet& s, uint32_t& nch,
   }
   erange |= units_total > MAXU;
   for (uint32_t c = 0; c < nch; c++) {
-    s.T[c] = b.chain_T[c0 + c]; s.D[c] = b.chain_D[c0 + c]; s.prio[c] = b.chain_prio[c0 + c];
+    s.T[c] = ld_time<C32>(b.chain_T, c0 + c); s.D[c] = ld_time<C32>(b.chain_D, c0 + c); s.prio[c] = b.chain_prio[c0 + c];
     s.cls[c] = b.chain_class[c0 + c];
     erange |= (s.T[c] == 0 || s.T[c] >= W_LIM || s.D[c] >= W_LIM);
     const uint32_t o = b.chain_cb_off[c0 + c] - cbA, e = b.chain_cb_off[c0 + c + 1] - cbA;
@@ -100,15 +102,16 @@ __device__ int w_load(const paam_batch& b, uint32_t set, WSet& s, uint32_t& nch,
   }
   for (uint32_t j = 0; j < ncb; j++) {
     const uint32_t so = b.cb_seg_off[cbA + j], se = b.cb_seg_off[cbA + j + 1];
-    const uint32_t x = b.cb_exec[cbA + j];
+    const uint32_t x = ld_cb_exec<C32>(b, cbA + j);
     edang |= (se == so) || (x >= nex);
     s.exec[j] = (uint8_t)min(x, 255u);
     s.seg0[j] = nq; s.nseg[j] = 0;
     uint64_t E = 0;
     uint32_t prev = 0xffffffffu;
     for (uint32_t g = so; g < se; g++) {
-      const uint32_t kind = b.seg_kind[g], a = b.seg_accel[g], u = b.seg_unit[g];
-      const uint64_t w = b.seg_wcet[g];
+      uint32_t kind, a, u;
+      ld_seg<C32>(b, g, kind, a, u);
+      const uint64_t w = ld_time<C32>(b.seg_wcet, g);
       erange |= w >= W_LIM;
       eshape |= (kind > 1) || (w == 0) || (kind == prev);
       prev = kind;
@@ -172,6 +175,7 @@ __device__ uint64_t w_lemma2(const WSet& s, uint32_t q, uint32_t nch) {
   return W_SAT;
 }
 
+template <bool C32>
 __global__ void __launch_bounds__(128) wide_kernel(paam_batch b, const uint32_t* __restrict__ list,
                                                    const uint32_t* __restrict__ count, int32_t* __restrict__ status_out,
                                                    uint64_t* __restrict__ out_wcrt, uint8_t* __restrict__ out_sched,
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(128) wide_kernel(paam_batch b, const uint32_t*
     if (set >= b.n_sets) continue;  // paam_analyze / paam_admit of the first n sets only
     WSet s;
     uint32_t nch, ncb, nq, nex, nac, nsub;
-    const int st = w_load(b, set, s, nch, ncb, nq, nex, nac, nsub);
+    const int st = w_load<C32>(b, set, s, nch, ncb, nq, nex, nac, nsub);
     const uint32_t c0 = b.set_chain_off[set], m = b.set_chain_off[set + 1] - c0;
     if (status_out) status_out[set] = st;
     uint32_t sched = 0;
@@ -377,9 +381,10 @@ __global__ void __launch_bounds__(128) wide_kernel(paam_batch b, const uint32_t*
 #ifndef PAAM_WARP_EMU
 // The wide sets listed in list[0 .. *count) (count is device memory, written by the u32 kernels).
 int launch_wide(const paam_batch* b, const uint32_t* list, const uint32_t* count, int32_t* status, uint64_t* out_wcrt,
-                uint8_t* out_sched, int64_t* out_bins, int32_t* out_fail, cudaStream_t st) {
+                uint8_t* out_sched, int64_t* out_bins, int32_t* out_fail, cudaStream_t st, bool c32) {
   if (b->n_sets == 0) return PAAM_OK;
-  wide_kernel<<<148, 128, 0, st>>>(*b, list, count, status, out_wcrt, out_sched, out_bins, out_fail);
+  if (c32) wide_kernel<true><<<148, 128, 0, st>>>(*b, list, count, status, out_wcrt, out_sched, out_bins, out_fail);
+  else wide_kernel<false><<<148, 128, 0, st>>>(*b, list, count, status, out_wcrt, out_sched, out_bins, out_fail);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "wide_kernel launch");

@@ -34,12 +34,30 @@ BATCH_ARRAYS = [
     ("accel_eps", np.uint64), ("accel_kappa", np.uint64),
     ("set_bin", np.uint32),
 ]
+# paam_batch32 (the compact batch) array fields, in declaration order.
+BATCH32_ARRAYS = [
+    ("set_chain_off", np.uint32), ("set_exec_off", np.uint32), ("set_accel_off", np.uint32),
+    ("chain_T", np.uint32), ("chain_D", np.uint32), ("chain_prio", np.uint32), ("chain_class", np.uint8),
+    ("chain_cb_off", np.uint32), ("cb_exec", np.uint8), ("cb_seg_off", np.uint32),
+    ("seg_meta", np.uint8), ("seg_wcet", np.uint32),
+    ("exec_core", np.uint8), ("exec_prio", np.uint32), ("exec_wait", np.uint8),
+    ("accel_buckets", np.uint8), ("accel_units", np.uint8), ("accel_server_core", np.uint8),
+    ("accel_eps", np.uint32), ("accel_kappa", np.uint32),
+    ("set_bin", np.uint32),
+]
 
 
 class PaamBatch(ctypes.Structure):
     _fields_ = ([("n_sets", ctypes.c_uint32), ("mem", ctypes.c_int32)] +
                 [(k, ctypes.c_uint32) for k in ("n_chains", "n_cbs", "n_segs", "n_execs", "n_accels", "n_bins")] +
                 [(name, ctypes.c_void_p) for name, _ in BATCH_ARRAYS] +
+                [("comm_cost", ctypes.c_uint64), ("flags", ctypes.c_uint32), ("_pad", ctypes.c_uint32)])
+
+
+class PaamBatch32(ctypes.Structure):
+    _fields_ = ([("n_sets", ctypes.c_uint32), ("mem", ctypes.c_int32)] +
+                [(k, ctypes.c_uint32) for k in ("n_chains", "n_cbs", "n_segs", "n_execs", "n_accels", "n_bins")] +
+                [(name, ctypes.c_void_p) for name, _ in BATCH32_ARRAYS] +
                 [("comm_cost", ctypes.c_uint64), ("flags", ctypes.c_uint32), ("_pad", ctypes.c_uint32)])
 
 
@@ -100,6 +118,7 @@ def lib():
         L.paam_analyze.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp, _vp]
         L.paam_admit.argtypes = [_vp, ctypes.c_uint32, _vp, _vp, _vp]
         L.paam_pack_analyze.argtypes = [ctypes.POINTER(PaamBatch), _vp, _vp, _vp, _vp, _vp, _vp]
+        L.paam_pack_analyze32.argtypes = [ctypes.POINTER(PaamBatch32), _vp, _vp, _vp, _vp, _vp, _vp]
         L.paam_simulate.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                     ctypes.c_uint32, ctypes.POINTER(PaamSimOut), _vp]
         L.paam_sets_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
@@ -198,6 +217,95 @@ class Batch:
         return Batch(arrays, h.c.n_sets, PAAM_MEM_DEVICE, h.c.n_bins, h.c.comm_cost, h.c.flags, tot)
 
 
+def compact_dict(d: dict) -> dict:
+    """The paam_batch32 arrays of a host dict batch (BATCH_ARRAYS names): 32-bit times, one packed byte
+    kind | accel << 1 | unit << 3 per segment, 8-bit callback executors.  Input marshalling only; raises
+    ValueError if a value does not fit the compact layout (include/paam.h paam_batch32)."""
+    out = {k: d[k] for k in ("n_sets",) if k in d}
+    for k in ("n_bins", "comm_cost", "flags"):
+        if k in d:
+            out[k] = d[k]
+    for name, dt in BATCH32_ARRAYS:
+        if name == "seg_meta":
+            kind = np.asarray(d["seg_kind"], np.uint64)
+            acc = np.asarray(d["seg_accel"], np.uint64)
+            unit = np.asarray(d["seg_unit"], np.uint64)
+            acc = np.where(kind == 1, acc, 0)
+            unit = np.where(kind == 1, unit, 0)
+            if (kind > 1).any() or (acc > 3).any() or (unit > 7).any():
+                raise ValueError("segment kind / accelerator / unit out of the compact range")
+            out[name] = (kind | (acc << 1) | (unit << 3)).astype(np.uint8)
+            continue
+        a = d.get(name)
+        if a is None:
+            out[name] = None
+            continue
+        a = np.asarray(a)
+        if a.size and int(a.max()) > np.iinfo(dt).max:
+            raise ValueError(f"{name}: a value does not fit {np.dtype(dt).name}")
+        out[name] = np.ascontiguousarray(a, dtype=dt)
+    return out
+
+
+class Batch32:
+    """A paam_batch32 (compact batch) plus the buffers it points to (host numpy or device torch)."""
+
+    def __init__(self, arrays: dict, n_sets: int, mem: int, n_bins=0, comm_cost=100_000, flags=0, totals=None):
+        self.arrays = arrays
+        b = PaamBatch32()
+        b.n_sets, b.mem, b.n_bins = n_sets, mem, n_bins
+        for k, v in (totals or {}).items():
+            setattr(b, k, v)
+        for name, _ in BATCH32_ARRAYS:
+            a = arrays.get(name)
+            if a is None:
+                setattr(b, name, None)
+            elif mem == PAAM_MEM_HOST:
+                setattr(b, name, a.ctypes.data if a.size else None)
+            else:
+                setattr(b, name, a.data_ptr() if a.numel() else None)
+        b.comm_cost, b.flags = comm_cost, flags
+        self.c = b
+
+    @property
+    def n_sets(self):
+        return self.c.n_sets
+
+    @staticmethod
+    def from_host(d: dict, pin=False) -> "Batch32":
+        """Host compact batch from a host dict batch (BATCH_ARRAYS names); pin: page-locked copies."""
+        c = compact_dict(d)
+        arrays = {}
+        for name, _ in BATCH32_ARRAYS:
+            a = c.get(name)
+            if a is not None and pin:
+                import torch
+                t = torch.from_numpy(a).pin_memory()
+                arrays[name + "_pinned"] = t
+                a = t.numpy()
+            arrays[name] = a
+        tot = dict(n_chains=int(c["set_chain_off"][-1]), n_cbs=int(c["chain_cb_off"][-1]),
+                   n_segs=int(c["cb_seg_off"][-1]), n_execs=int(c["set_exec_off"][-1]),
+                   n_accels=int(c["set_accel_off"][-1]))
+        n_bins = int(d.get("n_bins", 0))
+        if not n_bins:
+            arrays["set_bin"] = None
+        return Batch32(arrays, int(d["n_sets"]), PAAM_MEM_HOST, n_bins, int(d.get("comm_cost", 100_000)),
+                       int(d.get("flags", 0)), tot)
+
+    @staticmethod
+    def from_host_to_device(d: dict, device="cuda") -> "Batch32":
+        """A device compact batch (torch tensors) from a host dict batch."""
+        import torch
+        h = Batch32.from_host(d)
+        arrays = {}
+        for name, _ in BATCH32_ARRAYS:
+            a = h.arrays.get(name)
+            arrays[name] = None if a is None else torch.from_numpy(a.view(np.uint8).copy()).to(device)
+        tot = {k: getattr(h.c, k) for k in ("n_chains", "n_cbs", "n_segs", "n_execs", "n_accels")}
+        return Batch32(arrays, h.c.n_sets, PAAM_MEM_DEVICE, h.c.n_bins, h.c.comm_cost, h.c.flags, tot)
+
+
 class Raw:
     """Device raw batch produced by paam_generate (§8(a) step 1)."""
 
@@ -291,8 +399,12 @@ class Sets:
         ptr = lambda t: None if t is None else t.data_ptr()
         st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
                                              else out_status.data_ptr())
-        check(lib().paam_pack_analyze(ctypes.byref(batch.c), self.h, st, ptr(out_wcrt), ptr(out_sched),
-                                      ptr(out_bins), _stream_ptr(stream)), "paam_pack_analyze")
+        if isinstance(batch, Batch32):
+            check(lib().paam_pack_analyze32(ctypes.byref(batch.c), self.h, st, ptr(out_wcrt), ptr(out_sched),
+                                            ptr(out_bins), _stream_ptr(stream)), "paam_pack_analyze32")
+        else:
+            check(lib().paam_pack_analyze(ctypes.byref(batch.c), self.h, st, ptr(out_wcrt), ptr(out_sched),
+                                          ptr(out_bins), _stream_ptr(stream)), "paam_pack_analyze")
         self._refresh()
 
     def analyze(self, out_wcrt=None, out_sched=None, out_bins=None, n=None, stream=None):

@@ -450,3 +450,85 @@ def test_wide_time_sets_admission_and_des_status():
     assert wide.sum() > 50
     assert (s[wide] == paam.PAAM_SIM_WIDE).all()
     assert (s[~wide] != paam.PAAM_SIM_WIDE).all()
+
+
+def gpu_compact_path(batch, device=False):
+    """paam_pack_analyze32 on the compact form of `batch` (host or device), through a handle whose capacity
+    comes from paam_pack of the u64 batch; returns (wcrt, sched, status, bins) as paam.analyze."""
+    n = batch["n_sets"]
+    dev = torch.device("cuda")
+    sets = paam.Sets(paam.Batch.from_host(batch))
+    b32 = paam.Batch32.from_host_to_device(batch) if device else paam.Batch32.from_host(batch)
+    status = (torch.full((max(n, 1),), -9, dtype=torch.int32, device=dev) if device
+              else np.full(max(n, 1), -9, np.int32))
+    nch = int(batch["set_chain_off"][-1])
+    wcrt = torch.full((max(nch, 1),), -5, dtype=torch.int64, device=dev)
+    sched = torch.full((max(n, 1),), 7, dtype=torch.uint8, device=dev)
+    nb = int(batch.get("n_bins", 0))
+    bins = torch.zeros(max(2 * nb, 1), dtype=torch.int64, device=dev)
+    sets.pack_analyze(b32, wcrt, sched, bins if nb else None, out_status=status)
+    torch.cuda.synchronize()
+    st = status if isinstance(status, np.ndarray) else status.cpu().numpy()
+    out = (wcrt.cpu().numpy().view(np.uint64)[:nch], sched.cpu().numpy()[:n], st[:n], bins.cpu().numpy()[:2 * nb])
+    sets.free()
+    return out
+
+
+def mutate_invalid_compact(s: System, rng):
+    """Break one validation rule that the compact batch can express (or none)."""
+    k = rng.randrange(8)
+    if k == 0 and len(s.chains) > 1:
+        s.chains[1].prio = s.chains[0].prio
+    elif k == 1:
+        s.chains[0].D = s.chains[0].T + 1
+        s.chains[0].cls = CRITICAL
+    elif k == 2:
+        s.chains[0].cbs[0].exec = 31
+    elif k == 3:
+        s.chains[0].cbs[0].segs.append(Seg(1, 1, 3, 0))  # undeclared accelerator
+    elif k == 4:
+        s.chains[0].cbs[0].segs[0].wcet = 0
+    elif k == 5:
+        s.execs[0] = (10, 1, 0)  # server core of accelerator 0
+    elif k == 6:
+        s.chains[0].cbs[0].segs.append(Seg(s.chains[0].cbs[0].segs[-1].kind, 1))
+    return s
+
+
+@pytest.mark.parametrize("flags", [0, 1, 3])
+def test_compact_batch_gives_the_u64_batch_results(flags):
+    """paam_pack_analyze32 (the compact batch: u32 times, one byte per segment) is bit-exact with the
+    oracle on the same sets: valid and invalid ones, times on both sides of 2^31 - 1 ns (the wide ones take
+    the u64 kernel through the compact loads), host and device batches, the generated config-3 workload."""
+    rng = random.Random(300 + flags)
+    systems = []
+    for i in range(1200):
+        s = random_small_system(rng, max_chains=6, tmax=120)
+        if i % 4 == 1:  # the largest time scaled to just below 2^32 ns: wide, still representable in 32 bits
+            top = max([c.T for c in s.chains] + [c.D for c in s.chains] + [g.wcet for c in s.chains for x in c.cbs
+                       for g in x.segs] + [e for a in s.accels for e in a[3:5]] + [1])
+            s = _scaled(s, ((1 << 32) - 1) // top)
+        systems.append(mutate_invalid_compact(s, rng) if i % 3 == 0 else s)
+    for i, s in enumerate(systems):
+        s.bin = i % 5
+    b = flatten(systems, comm_cost=3, flags=flags, n_bins=5)
+    assert int(b["chain_T"].max()) < (1 << 32) and (b["chain_T"] >= (1 << 31) - 1).any()
+    assert_same(b, gpu_compact_path(b), fused_too=False)
+    assert_same(b, gpu_compact_path(b, device=True), fused_too=False)
+    g = generate_host(config3_params(), 4, 0, 20_000)
+    assert_same(g, gpu_compact_path(g), fused_too=False)
+
+
+def test_compact_batch_handle_refuses_a_later_pack():
+    """After paam_pack_analyze32 the handle holds no batch paam_analyze could pack: PAAM_EINVAL, until a
+    paam_repack of a u64 batch."""
+    b = flatten([app_b_two_chains()], comm_cost=0)
+    sets = paam.Sets(paam.Batch.from_host(b))
+    sets.pack_analyze(paam.Batch32.from_host(b))
+    with pytest.raises(paam.PaamError, match="compact"):
+        sets.analyze(torch.empty(2, dtype=torch.int64, device="cuda"))
+    sets.repack(paam.Batch.from_host(b))
+    w = torch.empty(2, dtype=torch.int64, device="cuda")
+    sets.analyze(w)
+    torch.cuda.synchronize()
+    assert w.cpu().tolist() == GOLD["two_chains_one_executor"]["R"]

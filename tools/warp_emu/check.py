@@ -12,16 +12,34 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 from gen.inputs import MS, config2_params, config3_params, flatten, generate_host, make_params  # noqa
 from oracle import oracle as O  # noqa
-from paper_2404_06452_b200.paam import Batch  # noqa  (only for the batch struct marshalling)
+from paper_2404_06452_b200.paam import Batch, PaamBatch, compact_dict  # noqa  (only for the batch struct marshalling)
 
 L = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("PAAM_EMU_LIB", "libpaam_emu.so")))
 vp = ctypes.c_void_p
 L.emu_pack.argtypes = [vp, vp, vp, vp, vp]
-L.emu_wide.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+L.emu_wide.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int]
 L.emu_analyze.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp]
 L.emu_simulate.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, vp]
 L.emu_record_bytes.restype = ctypes.c_uint32
-L.emu_fused.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+L.emu_fused.argtypes = [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int]
+
+
+def compact_struct(hb):
+    """A paam_batch carrying the compact (paam_batch32) arrays of host batch hb, as paam_pack_analyze32
+    builds it; returns (struct, arrays kept alive), or None if hb does not fit the compact layout."""
+    d = {name: hb.arrays.get(name) for name in hb.arrays}
+    d.update(n_sets=hb.c.n_sets, n_bins=hb.c.n_bins, comm_cost=hb.c.comm_cost, flags=hb.c.flags)
+    try:
+        c = compact_dict(d)
+    except ValueError:
+        return None
+    b = PaamBatch()
+    ctypes.memmove(ctypes.addressof(b), ctypes.addressof(hb.c), ctypes.sizeof(b))
+    ptr = lambda a: None if a is None or a.size == 0 else a.ctypes.data
+    for name in ("chain_T", "chain_D", "cb_exec", "seg_wcet", "accel_eps", "accel_kappa"):
+        setattr(b, name, ptr(c[name]))
+    b.seg_kind, b.seg_accel, b.seg_unit = ptr(c["seg_meta"]), None, None
+    return b, c
 
 
 def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
@@ -32,8 +50,8 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     wl = np.zeros(max(n, 1), np.uint32)  # sets handed over to the u64 path (wide.cu)
     wc = np.zeros(1, np.uint32)
     L.emu_pack(ctypes.addressof(hb.c), rec.ctypes.data, st.ctypes.data, wl.ctypes.data, wc.ctypes.data)
-    L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, st.ctypes.data, None, None, None, None)
-    wide = lambda w_, s_, b_: L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, None, w_, s_, b_, None)
+    L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, st.ctypes.data, None, None, None, None, 0)
+    wide = lambda w_, s_, b_: L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, None, w_, s_, b_, None, 0)
     nch = max(hb.c.n_chains, 1)
     w = np.zeros(nch, np.uint64)
     sc = np.zeros(max(n, 1), np.uint8)
@@ -56,19 +74,34 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     fb = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
     fl, fc = np.zeros(max(n, 1), np.uint32), np.zeros(1, np.uint32)
     L.emu_fused(ctypes.addressof(hb.c), fl.ctypes.data, fc.ctypes.data, fst.ctypes.data, fw.ctypes.data, fs.ctypes.data,
-                fb.ctypes.data if hb.c.set_bin else None)
+                fb.ctypes.data if hb.c.set_bin else None, 0)
     L.emu_wide(ctypes.addressof(hb.c), fl.ctypes.data, fc.ctypes.data, fst.ctypes.data, fw.ctypes.data, fs.ctypes.data,
-               fb.ctypes.data if hb.c.set_bin else None, None)
+               fb.ctypes.data if hb.c.set_bin else None, None, 0)
+    # the same through the compact batch (paam_pack_analyze32's kernels), when the batch fits it
+    cs = compact_struct(hb)
+    if cs is not None:
+        cst = np.full(max(n, 1), -9, np.int32)
+        cw = np.zeros(nch, np.uint64)
+        csc = np.zeros(max(n, 1), np.uint8)
+        cbn = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
+        cl, cc = np.zeros(max(n, 1), np.uint32), np.zeros(1, np.uint32)
+        L.emu_fused(ctypes.addressof(cs[0]), cl.ctypes.data, cc.ctypes.data, cst.ctypes.data, cw.ctypes.data,
+                    csc.ctypes.data, cbn.ctypes.data if hb.c.set_bin else None, 1)
+        L.emu_wide(ctypes.addressof(cs[0]), cl.ctypes.data, cc.ctypes.data, cst.ctypes.data, cw.ctypes.data,
+                   csc.ctypes.data, cbn.ctypes.data if hb.c.set_bin else None, None, 1)
+        out_c = dict(c_status=cst[:n], c_wcrt=cw[:hb.c.n_chains], c_sched=csc[:n], c_bins=cbn[:2 * hb.c.n_bins])
+    else:
+        out_c = {}
     vb = Batch.from_host(dict(batch, flags=batch.get("flags", 0) | 0x4))
     fsv = np.zeros(max(n, 1), np.uint8)
     fbv = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
     fc[0] = 0
     L.emu_fused(ctypes.addressof(vb.c), fl.ctypes.data, fc.ctypes.data, None, None, fsv.ctypes.data,
-                fbv.ctypes.data if hb.c.set_bin else None)
+                fbv.ctypes.data if hb.c.set_bin else None, 0)
     L.emu_wide(ctypes.addressof(vb.c), fl.ctypes.data, fc.ctypes.data, None, None, fsv.ctypes.data,
-               fbv.ctypes.data if hb.c.set_bin else None, None)
+               fbv.ctypes.data if hb.c.set_bin else None, None, 0)
     out.update(f_status=fst[:n], f_wcrt=fw[:hb.c.n_chains], f_sched=fs[:n], f_bins=fb[:2 * hb.c.n_bins],
-               f_sched_v=fsv[:n], f_bins_v=fbv[:2 * hb.c.n_bins])
+               f_sched_v=fsv[:n], f_bins_v=fbv[:2 * hb.c.n_bins], **out_c)
     if horizon is not None:
         from paper_2404_06452_b200.paam import PaamSimOut
         a = {k: np.zeros(nch, np.uint64) for k in ("resp", "count", "misses", "drops")}
@@ -99,7 +132,12 @@ def compare(batch, horizon=None, seed=0, first=0, label="", fifo=False):
         bad = np.nonzero(ow != e["f_wcrt"])[0][:5]
         print(f"  FUSED MISMATCH status o={ost[:8]} f={e['f_status'][:8]} wcrt bad {bad} o={ow[bad]} f={e['f_wcrt'][bad]}")
     ok = ok and okf
-    msg = [f"{label}: analyze {'OK' if ok else 'MISMATCH'}"]
+    if "c_wcrt" in e:  # the compact batch gives the u64 batch's results
+        okc = all(np.array_equal(e["f_" + k], e["c_" + k]) for k in ("status", "wcrt", "sched", "bins"))
+        if not okc:
+            print(f"  COMPACT MISMATCH status f={e['f_status'][:8]} c={e['c_status'][:8]}")
+        ok = ok and okc
+    msg = [f"{label}: analyze {'OK' if ok else 'MISMATCH'}" + (" (+compact)" if "c_wcrt" in e else "")]
     if not ok:
         bad = np.nonzero(ow != e["wcrt"])[0][:5]
         msg.append(f"  status o={ost[:8]} e={e['status'][:8]} wcrt bad idx {bad} o={ow[bad]} e={e['wcrt'][bad]}")
