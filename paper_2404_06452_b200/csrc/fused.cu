@@ -368,11 +368,13 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         s.xWait[lane] = (uint8_t)w;
       }
       __syncwarp();
+      uint32_t units_pack;  // byte a: the units of accelerator a (a < nac <= 4; u <= 255 as loaded)
       {
         const uint32_t u = lane < (int)nac ? s.aUnits[lane] : 0u;
         const uint32_t ub = f_scan_excl(u, lane);
         if (lane < (int)nac) s.aUbase[lane] = ub;
         n_unit = __reduce_add_sync(FULL, u);
+        units_pack = __reduce_or_sync(FULL, lane < 4 ? u << (8 * lane) : 0u);
       }
       const uint64_t cstart_bit = (lane < (int)nch && cbo < 64) ? (1ull << cbo) : 0ull;
       cstart = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(cstart_bit >> 32)) << 32) |
@@ -387,12 +389,13 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         erange |= (w >= LIMW);
         wide |= (w >= LIM);
         eshape |= (kind > 1) || (w == 0);
-        if (kind == 1) {
-          if (a >= nac) eaccel = true;
-          else edang |= (u >= s.aUnits[a]);
-        }
+        const bool isacc = kind == 1u;
+        eaccel |= isacc && a >= nac;
+        edang |= isacc && a < nac && u >= ((units_pack >> ((a & 3u) << 3)) & 0xffu);
         s.gW[i] = (uint32_t)min(w, (uint64_t)SAT);
-        s.gMeta[i] = (uint8_t)(min(kind, 1u) | (min(a, 3u) << 1) | (min(u, 7u) << 3));
+        // kind bit: an ACCEL segment (an undefined kind is ESHAPE, counted as no accelerator segment); the
+        // accelerator / unit bits are read only for valid sets, where they fit
+        s.gMeta[i] = (uint8_t)((kind == 1u ? 1u : 0u) | (a << 1) | (u << 3));
       }
       __syncwarp();
       // ---- callbacks: lane per callback, walking its staged segments
@@ -438,6 +441,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       }
       n_sub = __popcll(runstart);
       __syncwarp();
+      if (runstart & ~cstart)  // some chain changes executor: A13 (no return to an executor it left)
       #pragma unroll 1
       for (uint32_t j = lane; j < ncb; j += 32) {  // A13
         if (((runstart >> j) & 1ull) && !((cstart >> j) & 1ull)) {

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
             prev_kind = kind;
             if (kind == 0) {
               E = sadd(E, w);
-            } else {
+            } else if (kind == 1) {  // an undefined kind (ESHAPE) is no accelerator segment
               if (na == 0) { fa = s.gAcc[k]; fu = s.gUnit[k]; fw = w; }
               na++;
             }

@@ -532,3 +532,21 @@ def test_compact_batch_handle_refuses_a_later_pack():
     sets.analyze(w)
     torch.cuda.synchronize()
     assert w.cpu().tolist() == GOLD["two_chains_one_executor"]["R"]
+
+
+def test_invalid_segment_kind_is_not_counted_as_an_accelerator_segment():
+    """Validation counts ACCEL segments (kind == 1) against the 64-segment cap; a segment of an undefined
+    kind (2) is an ESHAPE error, never an accelerator segment (include/paam.h ERANGE / ESHAPE).  A set with
+    exactly 64 ACCEL segments plus one kind-2 segment is ESHAPE (not ERANGE), on every path."""
+    s = System()
+    a = s.accel(buckets=1, server_core=0)
+    x = s.executor(core=1)
+    s.chain(T=100 * MS, prio=1, cbs=[cb(x, cpu(1), acc(a, 1)) for _ in range(64)])
+    bad = System()
+    a = bad.accel(buckets=1, server_core=0)
+    x = bad.executor(core=1)
+    bad.chain(T=100 * MS, prio=1, cbs=[cb(x, cpu(1), acc(a, 1)) for _ in range(63)] + [cb(x, Seg(2, 1), acc(a, 1))])
+    b = flatten([s, bad], comm_cost=0)
+    _, _, st, _ = O.analyze(b)
+    assert st.tolist() == [0, 4]  # OK, ESHAPE
+    assert_same(b, gpu_host_path(b))
