@@ -198,25 +198,30 @@ __device__ PAAM_COLD uint32_t f_sound_blocking(const FSmem& s, uint32_t B, uint3
   return B;
 }
 
-// Eq.5 evaluation, as analyze.cu's eval_eq5 (see there), reading the shared period table.
+// Eq.5 evaluation, as analyze.cu's eval_eq5 (see there), reading the shared period table.  nxt: the
+// smallest R' > R at which one of the floor terms floor((R' - 1) / T) differs from its value at R (a term
+// with q = floor((R - 1) / T) changes at R' = (q + 1) T + 1); below it F and C are those at R, as long
+// as the interferers' H* are unchanged.
 template <bool WIDE>
 __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmask, uint32_t wsel, uint32_t umask,
                                        uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut, uint32_t xm,
                                        uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F, uint32_t& nH,
-                                       uint32_t& C) {
+                                       uint32_t& C, uint32_t& nxt) {
   const uint32_t h2 = (R - 1u) << 1;
   uint64_t acc = 0;
   uint32_t hi = 0;
+  uint32_t nx = 0xffffffffu;  // (q + 1) T + 1 < 2^32 for R, T < 2^31
   #pragma unroll 1
   for (uint32_t m = lmask; m;) {
     const uint32_t i = __ffs(m) - 1;
     const uint4 p = s.pTab[i];
-    if (p.x >= R) break;
+    if (p.x >= R) { nx = min(nx, p.x + 1u); break; }  // this and every later (longer) period: q = 0
     m &= m - 1;
 #ifdef PAAM_EMU_STATS
     atomicAdd(&emu_stats[3], 1ull);  // Lemma-3 floor terms
 #endif
     const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
+    nx = min(nx, (q + 1u) * p.x + 1u);
     uint32_t wu = p.w;
     if (wsel) {
       const uint32_t k = p.z & 0xffu;
@@ -246,6 +251,7 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
     const uint32_t X = sadd(s.sE[h], s.Hs[h]);
     const uint4 p = s.pTab[s.sPos[h]];
     const uint32_t q = p.x < R ? (__umulhi(h2, p.y) >> (p.z >> 8)) : 0u;
+    nx = min(nx, (q + 1u) * p.x + 1u);
     const uint64_t pr = (uint64_t)(q + 2u) * X;
     xs += pr;
     if (!WIDE) hi |= (uint32_t)(pr >> 32);
@@ -257,12 +263,18 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
       const uint4 p = s.pTab[s.sPos[h]];
       if (p.x < R) {
         const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
+        nx = min(nx, (q + 1u) * p.x + 1u);
         const uint64_t pr = (uint64_t)q * sadd(s.sE[h], s.sEps[h]);
         xs += pr;
         if (!WIDE) hi |= (uint32_t)(pr >> 32);
+      } else {
+        nx = min(nx, p.x + 1u);
       }
     }
+  } else if (xTmin != 0xffffffffu) {
+    nx = min(nx, xTmin + 1u);  // every such interferer has T >= R: q = 0 up to its T
   }
+  nxt = nx;
   const uint64_t f = (uint64_t)BE + nH + xs;
   F = (hi || f > cut) ? SAT : (uint32_t)f;
   if (F == SAT) nH = SAT;
@@ -768,14 +780,14 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
 #endif
       #pragma unroll 1
       for (;;) {
-        uint32_t F = R, nH = Hst;
+        uint32_t F = R, nH = Hst, nxt = 0u;
 #ifdef PAAM_EMU_STATS
         if (lane == 0) emu_stats[1]++;  // warp iterates
         if (dirty) atomicAdd(&emu_stats[2], 1ull);  // lane evaluations
 #endif
         if (dirty) {
-          if (wide) f_eval<true>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
-          else f_eval<false>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
+          if (wide) f_eval<true>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
+          else f_eval<false>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
         }
         const bool chg = dirty && (F != R || nH != Hst);
         const uint32_t cm = __ballot_sync(FULL, chg);
@@ -804,7 +816,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           s.Hs[lane] = nH;
         }
         __syncwarp();
-        dirty = act && R != SAT && (chg || (depm & cm) != 0u);
+        // A lane that moved to F below nxt has F(F) = F unless an interferer's H* changed: the floor terms,
+        // hence C and H*, are those of the evaluation just done, so it is not re-evaluated for itself.
+        dirty = act && R != SAT && ((chg && R >= nxt) || (depm & cm) != 0u);
         if (flags & PAAM_FLAG_VERDICT_ONLY) {
           if (__any_sync(FULL, critical && R == SAT)) { miss = true; break; }
         }
@@ -814,18 +828,16 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       if (!miss) {
         if (is_chain) { s.sum[lane] = 0; s.uns[lane] = 0; }
         __syncwarp();
-        if (act) {
-          if (R == SAT) s.uns[rk] = 1;
-          else atomicAdd(&s.sum[rk], (unsigned long long)R);
+        if (act) {  // per chain: sum of R, and (sub-chains | unschedulable ones << 16)
+          atomicAdd(&s.uns[rk], R == SAT ? 0x10001u : 1u);
+          if (R != SAT) atomicAdd(&s.sum[rk], (unsigned long long)R);
         }
         __syncwarp();
         bool ok = true;
         if (is_chain) {
           const uint32_t k = lane;
-          const uint32_t o = s.rCbo[k], nb = s.rNcb[k];
-          const uint64_t rng = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) << o;
-          const uint32_t nsc = __popcll(runstart & rng);
-          const uint64_t Rstar = s.uns[k] ? UNS : s.sum[k] + comm * (uint64_t)(nsc - 1);
+          const uint32_t u = s.uns[k], nsc = u & 0xffffu;  // nsc: the chain's executor crossings + 1 (A9)
+          const uint64_t Rstar = (u >> 16) ? UNS : s.sum[k] + comm * (uint64_t)(nsc - 1);
           if (out_wcrt) out_wcrt[c0 + s.rIdx[k]] = Rstar;
           const bool crit = s.rCls[k] == 0;
           ok = !crit || (Rstar != UNS && Rstar <= (uint64_t)s.rD[k]);
