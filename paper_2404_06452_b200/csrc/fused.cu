@@ -722,6 +722,13 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         s.sEps[lane] = eps;
         s.sPos[lane] = s.posOf[rk];
       }
+      // The set's CSR offsets and the prefetched next ones are not read again until step 5 / the end of the
+      // set: they rest in the dead LP-blocking scan buffer, which frees their registers for the solve.
+      uint32_t* const park = s.cmp;
+      if (lane == 0) {
+        park[0] = c0; park[1] = nc; park[2] = nx; park[3] = na_; park[4] = ncbo; park[5] = nsgo;
+        park[6] = pc; park[7] = px; park[8] = pa; park[9] = pcb; park[10] = psg;
+      }
       // ---- step 3: Lemma 2 (sound blocking: all segments up front) ------------------------------------
       __syncwarp();  // aBase / sE / sEps complete; maxA and pre2 are dead (H, Hs, sum, uns reuse them)
       if (!lazy_s)
@@ -838,12 +845,15 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           const uint32_t k = lane;
           const uint32_t u = s.uns[k], nsc = u & 0xffffu;  // nsc: the chain's executor crossings + 1 (A9)
           const uint64_t Rstar = (u >> 16) ? UNS : s.sum[k] + comm * (uint64_t)(nsc - 1);
-          if (out_wcrt) out_wcrt[c0 + s.rIdx[k]] = Rstar;
+          if (out_wcrt) out_wcrt[park[0] + s.rIdx[k]] = Rstar;
           const bool crit = s.rCls[k] == 0;
           ok = !crit || (Rstar != UNS && Rstar <= (uint64_t)s.rD[k]);
         }
         sched = __all_sync(FULL, ok) ? 1u : 0u;
       }
+      __syncwarp();
+      c0 = park[0]; nc = park[1]; nx = park[2]; na_ = park[3]; ncbo = park[4]; nsgo = park[5];
+      pc = park[6]; px = park[7]; pa = park[8]; pcb = park[9]; psg = park[10];
     }
     if (lane == 0) {
       if (out_sched) out_sched[set] = (uint8_t)sched;
@@ -858,7 +868,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       }
     }
     __syncwarp();
-    c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
+    c0 = nc; x0 = nx; a0 = na_; cb0 = ncbo; sg0 = nsgo;
     nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
   }
   if (blk_bins) {  // every warp of the block is done: one global atomic per non-zero counter
