@@ -659,7 +659,6 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           s.posOf[rank] = (uint8_t)ppos;
         }
       }
-      const bool wide = !__any_sync(FULL, is_chain && T < 64u);  // see analyze.cu eval_eq5
       __syncwarp();
 
       // ---- sub-chains (lane = sub-chain id, callback order): everything stays in registers -----------
@@ -793,8 +792,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         if (dirty) atomicAdd(&emu_stats[2], 1ull);  // lane evaluations
 #endif
         if (dirty) {
-          if (wide) f_eval<true>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
-          else f_eval<false>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
+          // one (checked) copy of the evaluation: the unchecked one for periods >= 64 ns saved one
+          // instruction per floor term but doubled the loop's code (instruction-cache stalls)
+          f_eval<false>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
         }
         const bool chg = dirty && (F != R || nH != Hst);
         const uint32_t cm = __ballot_sync(FULL, chg);
