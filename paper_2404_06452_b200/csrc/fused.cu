@@ -466,8 +466,15 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       {  // chain ranks and period positions (ascending T; equal periods by chain index), one pass
         uint32_t rk = 0, below = 0;
         const uint32_t Tme = lane < (int)nch ? T : 0xffffffffu;
+        uint32_t d = 0;
         #pragma unroll 1
-        for (uint32_t d = 0; d < nch; d++) {
+        for (; d + 1 < nch; d += 2) {  // two chains per trip: the four shuffles in flight together
+          const uint32_t p0 = __shfl_sync(FULL, prio, d), p1 = __shfl_sync(FULL, prio, d + 1);
+          const uint32_t t0 = __shfl_sync(FULL, Tme, d), t1 = __shfl_sync(FULL, Tme, d + 1);
+          rk += (uint32_t)(p0 > prio) + (uint32_t)(p1 > prio);
+          below += (uint32_t)(t0 < Tme) + (uint32_t)(t1 < Tme);
+        }
+        if (d < nch) {
           rk += (__shfl_sync(FULL, prio, d) > prio);
           below += (__shfl_sync(FULL, Tme, d) < Tme);
         }
