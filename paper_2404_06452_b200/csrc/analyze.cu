@@ -90,16 +90,21 @@ template <bool WIDE>
 __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uint32_t R, uint32_t lmask, uint32_t wsel,
                                          uint32_t umask, uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut,
                                          uint32_t xm, uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F,
-                                         uint32_t& nH, uint32_t& C) {
+                                         uint32_t& nH, uint32_t& C, uint32_t& nxt) {
+  // nxt: the smallest R' > R at which a floor term floor((R' - 1) / T) differs from its value at R (a term
+  // with q = floor((R - 1) / T) changes at (q + 1) T + 1 < 2^32); below it F and C are those at R while
+  // the interferers' H* are unchanged (fused.cu f_eval)
   const uint32_t h2 = (R - 1u) << 1;
   uint64_t acc = 0;
   uint32_t hi = 0;
+  uint32_t nx = 0xffffffffu;
   for (uint32_t m = lmask; m;) {
     const uint32_t i = __ffs(m) - 1;
     const uint4 p = r.pTab[i];  // {T, M, rank | L << 8, W[rank][0] + W[rank][1]}
-    if (p.x >= R) break;        // this and every later period: floor((R-1)/T) = 0
+    if (p.x >= R) { nx = min(nx, p.x + 1u); break; }  // this and every later period: floor((R-1)/T) = 0
     m &= m - 1;
     const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
+    nx = min(nx, (q + 1u) * p.x + 1u);
     uint32_t wu = p.w;
     if (wsel) {  // not both of units 0 and 1: one unit (wsel = unit + 1), or the general unit union
       const uint32_t k = p.z & 0xffu;
@@ -127,6 +132,7 @@ __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uin
     const uint32_t X = sadd(r.sE[h], w.Hs[h]);
     const uint4 p = r.pTab[w.sPos[h]];
     const uint32_t q = p.x < R ? (__umulhi(h2, p.y) >> (p.z >> 8)) : 0u;
+    nx = min(nx, (q + 1u) * p.x + 1u);
     const uint64_t pr = (uint64_t)(q + 2u) * X;
     xs += pr;
     if (!WIDE) hi |= (uint32_t)(pr >> 32);
@@ -137,12 +143,18 @@ __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uin
       const uint4 p = r.pTab[w.sPos[h]];
       if (p.x < R) {
         const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
+        nx = min(nx, (q + 1u) * p.x + 1u);
         const uint64_t pr = (uint64_t)q * sadd(r.sE[h], r.sEps[h]);
         xs += pr;
         if (!WIDE) hi |= (uint32_t)(pr >> 32);
+      } else {
+        nx = min(nx, p.x + 1u);
       }
     }
+  } else if (xTmin != 0xffffffffu) {
+    nx = min(nx, xTmin + 1u);
   }
+  nxt = nx;
   const uint64_t f = (uint64_t)BE + nH + xs;
   F = (hi || f > cut) ? SAT : (uint32_t)f;  // above the cutoff: UNSCHED (A4)
   if (F == SAT) nH = SAT;                   // dependants become UNSCHED as well (A8)
@@ -303,7 +315,6 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const uint32_t depm = hpm | (hppm & spin_mask);  // X_h = E_h + H*_h (hp, spinning hpp: P:1132)
       const uint32_t xm = hpm | hppm;                   // every CPU interferer (Eq.5 sums)
       const bool critical = act && ((r.cMisc[rk] >> 8) & 0xffu) == 0;
-      const bool wide = (r.hflags & REC_WIDE_OK) != 0u;  // set-uniform: unchecked 64-bit mu sums
       bool sexact = !lazy_s;
       // period positions of the chains (pTab is in ascending period order)
       if (lane < (int)nch) w.posOf[r.pTab[lane].z & 0xffu] = (uint8_t)lane;
@@ -349,11 +360,9 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       bool dirty = act;  // must be evaluated this iterate (own R or a dependency's H* changed)
       bool miss = false;
       for (;;) {
-        uint32_t F = R, nH = Hst;
-        if (dirty) {
-          if (wide) eval_eq5<true>(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
-          else eval_eq5<false>(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C);
-        }
+        uint32_t F = R, nH = Hst, nxt = 0u;
+        if (dirty)  // one checked copy (the unchecked one doubled the loop's code)
+          eval_eq5<false>(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
         const bool chg = dirty && (F != R || nH != Hst);
         const uint32_t cm = __ballot_sync(FULL, chg);
         if (!cm) {
@@ -381,7 +390,8 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
           w.Hs[lane] = nH;
         }
         __syncwarp();
-        dirty = act && R != SAT && (chg || (depm & cm) != 0u);
+        // a lane that moved below nxt has F(F) = F unless an interferer's H* changed (fused.cu)
+        dirty = act && R != SAT && ((chg && R >= nxt) || (depm & cm) != 0u);
         if (flags & PAAM_FLAG_VERDICT_ONLY) {  // R_c > D_c of a CRITICAL chain => R* > D
           if (__any_sync(FULL, critical && R == SAT)) { miss = true; break; }
         }

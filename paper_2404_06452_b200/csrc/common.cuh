@@ -118,7 +118,6 @@ constexpr int MAXA = 64;   // accelerator segments
 constexpr int MAXU = 8;    // accelerator units (all accelerators of the set)
 constexpr int MAXX = 32;   // executors
 constexpr int MAXCB = 64;  // callbacks
-constexpr uint32_t REC_WIDE_OK = 1u;  // Record::hflags
 constexpr uint64_t LIMW = 1ull << 48;   // every input time must be < LIMW (else PAAM_SET_ERANGE); times >= LIM go
                                         // to the exact u64 path (wide.cu)
 constexpr int32_t REC_STATUS_WIDE = 0x100;  // internal status: handed over to wide.cu
@@ -130,7 +129,7 @@ struct __align__(16) Record {
   uint32_t chain_base;  // global index of the set's first chain (out_wcrt position)
   uint32_t bin;         // utilisation bin (0 when the batch has none)
   uint32_t n_out;       // chains of the set in the batch (== n_chain when valid)
-  uint32_t hflags;      // REC_WIDE_OK: every period >= 64 ns (unchecked 64-bit mu sums cannot overflow)
+  uint32_t hflags;      // reserved (0)
   uint32_t pad_[2];
   // chains by rank (rank 0 = highest priority)
   uint32_t cCut[MAXC];   // cutoff min(D, T) (A4, A12)

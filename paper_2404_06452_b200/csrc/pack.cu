@@ -580,8 +580,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       }
       if (is_chain) r->pTab[pos] = uint4{Tk, M, (uint32_t)lane | (L << 8), sadd(s.W[lane][0], s.W[lane][1])};
       // every period >= 64 ns: q * W < 2^62 / 64, so 64 such products cannot overflow a u64 sum
-      const bool wide_ok = !__any_sync(FULL, is_chain && Tk < 64u);
-      if (lane == 0) r->hflags = wide_ok ? REC_WIDE_OK : 0u;
+      if (lane == 0) r->hflags = 0u;
     }
     // ---- accelerator segments (rank order) ------------------------------------------------------------
     for (uint32_t q = lane; q < n_aseg; q += 32) {
