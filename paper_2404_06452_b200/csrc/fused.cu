@@ -21,7 +21,16 @@ namespace paam {
 
 namespace {
 
-constexpr int FW = 8;  // warps per block
+// Block shape, measured (tools/fused_variants.sh, 2M config-3 sets): 2 blocks of 16 warps per SM beat 4 of
+// 8 (8.02 vs 8.24 ms) and 8 of 4 (8.78 ms); one segment-staging pass per loop trip beats two (-0.05 ms).
+#ifndef F_WARPS
+#define F_WARPS 16
+#endif
+constexpr int FW = F_WARPS;  // warps per block
+#ifndef F_SEG_UNROLL
+#define F_SEG_UNROLL 1
+#endif
+constexpr int kFSegUnroll = F_SEG_UNROLL;  // segment-staging passes per loop trip
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t MAXSEG = 192;
 constexpr int F_WARP_BINS = 32;
@@ -281,7 +290,7 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
 }
 
 #ifndef FUSED_MINB
-#define FUSED_MINB 4  // 4 blocks of 8 warps (7 KB of shared memory per warp): 32 warps, 64 registers
+#define FUSED_MINB 2  // 2 blocks of 16 warps (7 KB of shared memory per warp): 32 warps, 64 registers
 #endif
 // C32: b carries a compact batch (paam_batch32; common.cuh ld_time)
 template <bool C32>
@@ -393,7 +402,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
                __reduce_or_sync(FULL, (uint32_t)cstart_bit);
       __syncwarp();
       // ---- segments: lane per segment, staged with their per-segment validation
-      #pragma unroll 2  // two passes' loads in flight
+      #pragma unroll kFSegUnroll
       for (uint32_t i = lane; i < nseg; i += 32) {
         const uint64_t w = ld_time<C32>(b.seg_wcet, sg0 + i);
         uint32_t kind, a, u;
