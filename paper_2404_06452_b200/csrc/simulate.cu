@@ -33,7 +33,12 @@ namespace paam {
 
 namespace {
 
-constexpr int SW = 4;      // warps per block
+// Block shape, measured (tools/des_variants.sh, 1M config-5 sets): 16 blocks of 2 warps per SM beat 8 of 4
+// (317.5k vs 312k sets/s with digests), 4 of 8 (296k) and 32 of 1 (278k).
+#ifndef SIM_WARPS
+#define SIM_WARPS 2
+#endif
+constexpr int SW = SIM_WARPS;  // warps per block
 constexpr int QCAP = PAAM_SIM_QCAP;  // instance slots per chain; one more live instance stops the run
 constexpr int MAXG = 192;  // segments per set
 constexpr uint32_t FULL = 0xffffffffu;
@@ -236,7 +241,7 @@ struct Ctx {
 };
 
 #ifndef SIM_MINB
-#define SIM_MINB 8  // measured: 8 blocks of 4 warps (64 registers) beat 6, 7 and 9
+#define SIM_MINB 16  // 16 blocks of 2 warps: 32 warps per SM (shared memory bounds it at 33)
 #endif
 __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch b, const Record* __restrict__ recs, uint32_t n,
                                                            uint64_t horizon, uint64_t seed, uint64_t first_index,
