@@ -31,6 +31,10 @@ constexpr int FW = F_WARPS;  // warps per block
 #define F_SEG_UNROLL 1
 #endif
 constexpr int kFSegUnroll = F_SEG_UNROLL;  // segment-staging passes per loop trip
+#ifndef F_CB_UNROLL
+#define F_CB_UNROLL 1
+#endif
+constexpr int kFCbUnroll = F_CB_UNROLL;  // a callback's segments per trip of its walk
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t MAXSEG = 192;
 constexpr int F_WARP_BINS = 32;
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
           edang |= (se == so) || (exec >= nex);
           if (so < sg0 || se < so || se > sg1) { malformed = true; so = se = sg0; }
           uint32_t prev_kind = 0xffffffffu;
-          #pragma unroll 1
+          #pragma unroll kFCbUnroll
           for (uint32_t k = so - sg0; k < se - sg0; k++) {
             const uint32_t meta = s.gMeta[k], kind = meta & 1u, w = s.gW[k];
             eshape |= (kind == prev_kind);
