@@ -25,7 +25,10 @@ namespace paam {
 
 namespace {
 
-constexpr int WARPS = 4;
+#ifndef PACK_WARPS
+#define PACK_WARPS 4
+#endif
+constexpr int WARPS = PACK_WARPS;
 #ifndef PACK_SEG_UNROLL
 #define PACK_SEG_UNROLL 1
 #endif
