@@ -22,7 +22,7 @@ struct paam_sets {
   cudaStream_t side[3];  // internal streams of paam_pack_analyze: pack, analyze, H2D copies (created on first use)
   cudaEvent_t ev[17], evc[8];  // evc: chunk copies done
   unsigned int* tickets;  // work-distribution counters: pipeline chunks [0, 16), analyze 16, admit 17, simulate 18,
-                          // 20: number of wide sets listed (wide.cu)
+                          // 20: number of wide sets listed (wide.cu), 21: fused_kernel's work ticket
   uint32_t* wide_list;    // [cap] the sets handed over to the u64 path by the last pack / fused launch
   int device;             // the CUDA device the handle lives on (made current by every call)
   void* sim_scratch;      // paam_simulate's event buffers (grown on demand)
@@ -314,7 +314,7 @@ int pack_analyze_impl(const paam_batch* batch, bool c32, paam_sets* sets, int32_
   int32_t* status_dev = out_status;
   if (!host) {
     // steps 2-6 in one kernel (fused.cu): the derived records stay on chip
-    cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
+    cudaMemsetAsync(sets->tickets + 20, 0, 2 * sizeof(unsigned int), st);  // wide count, work ticket
     if ((rc = launch_fused(&d, sets->wide_list, sets->tickets + 20, status_dev, out_wcrt, out_sched,
                            const_cast<int64_t*>(bins), st, c32)))
       return rc;
@@ -395,7 +395,7 @@ int pack_analyze_impl(const paam_batch* batch, bool c32, paam_sets* sets, int32_
       view.set_exec_off += lo;
       view.set_accel_off += lo;
       if (view.set_bin) view.set_bin += lo;
-      cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), sets->side[0]);
+      cudaMemsetAsync(sets->tickets + 20, 0, 2 * sizeof(unsigned int), sets->side[0]);  // wide count, work ticket
       if ((rc = launch_fused(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
                              out_sched ? out_sched + lo : nullptr,
                              const_cast<int64_t*>(bins), sets->side[0], c32)))

@@ -178,7 +178,8 @@ int launch_analyze(const Record* rec, uint32_t n, uint64_t comm, uint32_t flags,
                    uint64_t* out_wcrt, uint8_t* out_sched, int64_t* out_bins, unsigned int* ticket,
                    cudaStream_t st, int32_t* out_fail = nullptr);
 // §8(a) steps 2-6 in one kernel (fused.cu): no record is written
-// c32: b carries a compact batch (paam_batch32, see ld_time)
+// c32: b carries a compact batch (paam_batch32, see ld_time).  wide_count[1] is the kernel's work ticket:
+// the caller zeroes wide_count[0..1] on the stream before the launch.
 int launch_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_count, int32_t* status, uint64_t* out_wcrt,
                  uint8_t* out_sched, int64_t* out_bins, cudaStream_t st, bool c32 = false);
 // the exact u64 path over the sets listed by the u32 kernels (wide.cu); out_fail: admission decisions

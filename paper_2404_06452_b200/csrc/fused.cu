@@ -27,6 +27,9 @@ namespace {
 #define F_WARPS 16
 #endif
 constexpr int FW = F_WARPS;  // warps per block
+#ifndef F_CHUNK
+#define F_CHUNK 8  // sets per work ticket (0: fixed per-warp ranges)
+#endif
 #ifndef F_SEG_UNROLL
 #define F_SEG_UNROLL 1
 #endif
@@ -300,6 +303,7 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
 template <bool C32>
 __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     fused_kernel(paam_batch b, uint32_t* __restrict__ wide_list, uint32_t* __restrict__ wide_count,
+                 unsigned int* __restrict__ work_ticket,
                  int32_t* __restrict__ status_out, uint64_t* __restrict__ out_wcrt,
                  uint8_t* __restrict__ out_sched, int64_t* __restrict__ out_bins) {
 #ifdef PAAM_WARP_EMU
@@ -322,11 +326,23 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     __syncthreads();
   }
   const uint64_t comm = b.comm_cost;
-  // Blocked assignment (as pack.cu): warp w owns the contiguous sets [lo, hi); each set's start
-  // offsets are the previous set's end offsets, whose dependent loads are pipelined one set ahead.
+  // Dynamic assignment: a warp takes F_CHUNK consecutive sets per ticket (a set's cost varies with its
+  // chains and iterates, so fixed per-warp ranges leave the slowest warp ~8% behind the mean); within a
+  // chunk each set's start offsets are the previous set's end offsets, whose dependent loads are
+  // pipelined one set ahead.
+#if F_CHUNK
+  #pragma unroll 1
+  for (;;) {
+  uint32_t tk = 0;
+  if (lane == 0) tk = atomicAdd(work_ticket, (unsigned)F_CHUNK);
+  const uint32_t lo = __shfl_sync(FULL, tk, 0);
+  if (lo >= b.n_sets) break;
+  const uint32_t hi = min(lo + (uint32_t)F_CHUNK, b.n_sets);
+#else
   const uint32_t nwarps = gridDim.x * FW, wid = blockIdx.x * FW + (threadIdx.x >> 5);
   const uint32_t lo = (uint32_t)((uint64_t)b.n_sets * wid / nwarps);
   const uint32_t hi = (uint32_t)((uint64_t)b.n_sets * (wid + 1) / nwarps);
+#endif
   uint32_t c0 = 0, x0 = 0, a0 = 0, cb0 = 0, sg0 = 0;
   uint32_t nc = 0, nx = 0, na_ = 0, ncbo = 0, nsgo = 0;
   if (lo < hi) {
@@ -891,6 +907,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
     c0 = nc; x0 = nx; a0 = na_; cb0 = ncbo; sg0 = nsgo;
     nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
   }
+#if F_CHUNK
+  }
+#endif
   if (blk_bins) {  // every warp of the block is done: one global atomic per non-zero counter
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < 2 * n_bins; i += FW * 32)
@@ -917,7 +936,9 @@ int launch_fused_t(const paam_batch* b, uint32_t* wide_list, uint32_t* wide_coun
   const uint32_t need = (b->n_sets + FW - 1) / FW;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  fused_kernel<C32><<<grid, FW * 32, SMEM, st>>>(*b, wide_list, wide_count, status, out_wcrt, out_sched, out_bins);
+  // the work ticket is the counter after wide_count (the callers zero both)
+  fused_kernel<C32><<<grid, FW * 32, SMEM, st>>>(*b, wide_list, wide_count, wide_count + 1, status, out_wcrt, out_sched,
+                                                  out_bins);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "fused_kernel launch");

@@ -536,7 +536,7 @@ struct paam_sweeper {
   uint32_t chunk;
   paam_raw raw[2];          // capacity-laid-out raw batches (ping-pong)
   uint32_t* wide[2];        // sets of the chunk handed over to the u64 path (wide.cu), one list per buffer
-  unsigned int* tickets;    // their counts, one per buffer
+  unsigned int* tickets;    // per buffer: the wide-list count and fused_kernel's work ticket
   cudaStream_t sg, sa;      // generation / pack + analysis
   cudaEvent_t start, gen_done[2], ana_done[2], join[2];
   int device;
@@ -553,7 +553,7 @@ extern "C" int paam_sweep_create(uint32_t chunk, paam_sweeper** out) {
     h->raw[i].device = h->device;
     e = cudaMalloc((void**)&h->wide[i], sizeof(uint32_t) * (size_t)chunk);
   }
-  if (e == cudaSuccess) e = cudaMalloc((void**)&h->tickets, sizeof(unsigned int) * 2);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->tickets, sizeof(unsigned int) * 4);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sg, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sa, cudaStreamNonBlocking);
   cudaEvent_t* evs[7] = {&h->start, &h->gen_done[0], &h->gen_done[1], &h->ana_done[0], &h->ana_done[1], &h->join[0], &h->join[1]};
@@ -594,11 +594,11 @@ extern "C" int paam_sweep(paam_sweeper* h, const paam_gen_params* params, uint64
     if (int rc = generate_into(&h->raw[bi], p, seed, first_index + lo, cnt, comm_cost, flags, h->sg, h->chunk)) return rc;
     cudaEventRecord(h->gen_done[bi], h->sg);
     cudaStreamWaitEvent(h->sa, h->gen_done[bi], 0);
-    cudaMemsetAsync(h->tickets + bi, 0, sizeof(unsigned int), h->sa);
-    if (int rc = launch_fused(&h->raw[bi].b, h->wide[bi], h->tickets + bi, nullptr, nullptr,
+    cudaMemsetAsync(h->tickets + 2 * bi, 0, 2 * sizeof(unsigned int), h->sa);  // wide count, work ticket
+    if (int rc = launch_fused(&h->raw[bi].b, h->wide[bi], h->tickets + 2 * bi, nullptr, nullptr,
                               out_sched ? out_sched + lo : nullptr, p.n_bins ? out_bins : nullptr, h->sa))  // steps 2-6
       return rc;
-    if (int rc = launch_wide(&h->raw[bi].b, h->wide[bi], h->tickets + bi, nullptr, nullptr,
+    if (int rc = launch_wide(&h->raw[bi].b, h->wide[bi], h->tickets + 2 * bi, nullptr, nullptr,
                              out_sched ? out_sched + lo : nullptr, p.n_bins ? out_bins : nullptr, nullptr, h->sa))
       return rc;
     cudaEventRecord(h->ana_done[bi], h->sa);

@@ -72,7 +72,7 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     fw = np.zeros(nch, np.uint64)
     fs = np.zeros(max(n, 1), np.uint8)
     fb = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
-    fl, fc = np.zeros(max(n, 1), np.uint32), np.zeros(1, np.uint32)
+    fl, fc = np.zeros(max(n, 1), np.uint32), np.zeros(2, np.uint32)  # wide count, work ticket
     L.emu_fused(ctypes.addressof(hb.c), fl.ctypes.data, fc.ctypes.data, fst.ctypes.data, fw.ctypes.data, fs.ctypes.data,
                 fb.ctypes.data if hb.c.set_bin else None, 0)
     L.emu_wide(ctypes.addressof(hb.c), fl.ctypes.data, fc.ctypes.data, fst.ctypes.data, fw.ctypes.data, fs.ctypes.data,
@@ -84,7 +84,7 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
         cw = np.zeros(nch, np.uint64)
         csc = np.zeros(max(n, 1), np.uint8)
         cbn = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
-        cl, cc = np.zeros(max(n, 1), np.uint32), np.zeros(1, np.uint32)
+        cl, cc = np.zeros(max(n, 1), np.uint32), np.zeros(2, np.uint32)
         L.emu_fused(ctypes.addressof(cs[0]), cl.ctypes.data, cc.ctypes.data, cst.ctypes.data, cw.ctypes.data,
                     csc.ctypes.data, cbn.ctypes.data if hb.c.set_bin else None, 1)
         L.emu_wide(ctypes.addressof(cs[0]), cl.ctypes.data, cc.ctypes.data, cst.ctypes.data, cw.ctypes.data,
@@ -95,7 +95,7 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     vb = Batch.from_host(dict(batch, flags=batch.get("flags", 0) | 0x4))
     fsv = np.zeros(max(n, 1), np.uint8)
     fbv = np.zeros(max(2 * hb.c.n_bins, 1), np.int64)
-    fc[0] = 0
+    fc[:] = 0
     L.emu_fused(ctypes.addressof(vb.c), fl.ctypes.data, fc.ctypes.data, None, None, fsv.ctypes.data,
                 fbv.ctypes.data if hb.c.set_bin else None, 0)
     L.emu_wide(ctypes.addressof(vb.c), fl.ctypes.data, fc.ctypes.data, None, None, fsv.ctypes.data,

@@ -4,7 +4,7 @@ extern "C" void emu_fused(const paam_batch* b, uint32_t* wide_list, uint32_t* wi
                           uint8_t* sched, int64_t* bins, int c32) {
   gridDim.x = 1;
   emu::launch_block(0, paam::FW * 32, [&]() {
-    if (c32) paam::fused_kernel<true>(*b, wide_list, wide_count, status, wcrt, sched, bins);
-    else paam::fused_kernel<false>(*b, wide_list, wide_count, status, wcrt, sched, bins);
+    if (c32) paam::fused_kernel<true>(*b, wide_list, wide_count, wide_count + 1, status, wcrt, sched, bins);
+    else paam::fused_kernel<false>(*b, wide_list, wide_count, wide_count + 1, status, wcrt, sched, bins);
   });
 }
