@@ -127,7 +127,7 @@ int ensure_records(const paam_sets* cs, cudaStream_t st) {
   if (sets->rec_valid) return PAAM_OK;
   if (sets->c32)
     return fail(PAAM_EINVAL, "the handle holds a compact batch (paam_pack_analyze32): paam_pack / paam_repack first");
-  cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
+  cudaMemsetAsync(sets->tickets + 20, 0, 2 * sizeof(unsigned int), st);  // wide count, work ticket
   if (int rc = launch_pack(&sets->dev, sets->rec, nullptr, sets->wide_list, sets->tickets + 20, st)) return rc;
   sets->rec_valid = true;
   return PAAM_OK;
@@ -186,7 +186,7 @@ extern "C" int paam_repack(const paam_batch* batch, paam_sets* sets, int32_t* ou
       status_dev = sets->dstatus;
     }
   }
-  cudaMemsetAsync(sets->tickets + 20, 0, sizeof(unsigned int), st);
+  cudaMemsetAsync(sets->tickets + 20, 0, 2 * sizeof(unsigned int), st);  // wide count, work ticket
   rc = launch_pack(&d, sets->rec, status_dev, sets->wide_list, sets->tickets + 20, st);
   if (rc) return rc;
   // the wide sets (a time >= 2^31 - 1 ns): validated on the u64 path (statuses only here)

@@ -171,6 +171,7 @@ int fail_cuda(cudaError_t e, const char* what);
 int fail(int code, const char* what);
 
 // launchers (defined in the kernel files)
+// wide_count[1] is the kernel's work ticket: the caller zeroes wide_count[0..1] before the launch
 int launch_pack(const paam_batch* dev_batch_fields, Record* rec, int32_t* status, uint32_t* wide_list,
                 uint32_t* wide_count, cudaStream_t st);
 // ticket: one device counter (zeroed by the launcher on `st`) for dynamic work distribution

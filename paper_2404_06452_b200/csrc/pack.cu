@@ -130,24 +130,32 @@ __device__ PAAM_COLD void wfd_units(Scratch& s, uint32_t nac, uint32_t ncb, uint
   }
 }
 
+#ifndef P_CHUNK
+#define P_CHUNK 8  // sets per work ticket
+#endif
 #ifndef PACK_MINB
 #define PACK_MINB 8
 #endif
 __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch b, Record* __restrict__ recs,
                                                           int32_t* __restrict__ status_out,
                                                           uint32_t* __restrict__ wide_list,
-                                                          uint32_t* __restrict__ wide_count) {
+                                                          uint32_t* __restrict__ wide_count,
+                                                          unsigned int* __restrict__ work_ticket) {
   __shared__ Scratch smem[WARPS];
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   Scratch& s = smem[threadIdx.x >> 5];
   const bool sound = (b.flags & PAAM_FLAG_BLOCKING_SOUND) != 0;  // record fields of the sound B_c (A10)
-  // Blocked assignment: warp w owns the contiguous sets [lo, hi).  Consecutive sets are adjacent in
-  // every CSR array, so the next set's start offsets are this set's end offsets: after the first set
-  // no dependent offset loads remain, and the next set's lines are often already in L2.
-  const uint32_t nwarps = gridDim.x * WARPS, wid = blockIdx.x * WARPS + (threadIdx.x >> 5);
-  const uint32_t lo = (uint32_t)((uint64_t)b.n_sets * wid / nwarps);
-  const uint32_t hi = (uint32_t)((uint64_t)b.n_sets * (wid + 1) / nwarps);
+  // Dynamic assignment: a warp takes P_CHUNK consecutive sets per ticket (as fused_kernel).  Consecutive
+  // sets are adjacent in every CSR array, so the next set's start offsets are this set's end offsets:
+  // after a chunk's first set no dependent offset loads remain.
+  #pragma unroll 1
+  for (;;) {
+  uint32_t tk = 0;
+  if (lane == 0) tk = atomicAdd(work_ticket, (unsigned)P_CHUNK);
+  const uint32_t lo = __shfl_sync(0xffffffffu, tk, 0);
+  if (lo >= b.n_sets) break;
+  const uint32_t hi = min(lo + (uint32_t)P_CHUNK, b.n_sets);
   uint32_t c0 = 0, x0 = 0, a0 = 0, cb0 = 0, sg0 = 0;      // start offsets of the current set
   uint32_t nc = 0, nx = 0, na_ = 0, ncbo = 0, nsgo = 0;  // end offsets of the current set (prefetched)
   if (lo < hi) {
@@ -600,6 +608,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     c0 = c1; x0 = x1; a0 = a1; cb0 = cb1; sg0 = sg1;
     nc = pc; nx = px; na_ = pa; ncbo = pcb; nsgo = psg;
   }
+  }
 }
 
 }  // namespace
@@ -616,7 +625,7 @@ int launch_pack(const paam_batch* b, Record* rec, int32_t* status, uint32_t* wid
   const uint32_t need = (b->n_sets + WARPS - 1) / WARPS;
   const uint32_t cap = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t grid = need < cap ? need : cap;
-  pack_kernel<<<grid, WARPS * 32, 0, st>>>(*b, rec, status, wide_list, wide_count);
+  pack_kernel<<<grid, WARPS * 32, 0, st>>>(*b, rec, status, wide_list, wide_count, wide_count + 1);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PAAM_OK : fail_cuda(e, "pack_kernel launch");

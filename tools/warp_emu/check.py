@@ -48,7 +48,7 @@ def emu_run(batch, horizon=None, seed=0, first=0, fifo=False):
     rec = np.zeros((max(n, 1), L.emu_record_bytes()), np.uint8)
     st = np.zeros(max(n, 1), np.int32)
     wl = np.zeros(max(n, 1), np.uint32)  # sets handed over to the u64 path (wide.cu)
-    wc = np.zeros(1, np.uint32)
+    wc = np.zeros(2, np.uint32)  # wide count, work ticket
     L.emu_pack(ctypes.addressof(hb.c), rec.ctypes.data, st.ctypes.data, wl.ctypes.data, wc.ctypes.data)
     L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, st.ctypes.data, None, None, None, None, 0)
     wide = lambda w_, s_, b_: L.emu_wide(ctypes.addressof(hb.c), wl.ctypes.data, wc.ctypes.data, None, w_, s_, b_, None, 0)
