@@ -530,16 +530,16 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         }
       }
       erange |= (n_aseg > MAXA) || (n_unit > MAXU);
-      if (__any_sync(FULL, malformed)) st = PAAM_SET_EDANGLING;
-      else if (__any_sync(FULL, erange)) st = PAAM_SET_ERANGE;
-      else if (__any_sync(FULL, wide)) st = REC_STATUS_WIDE;  // handed over: wide.cu validates and analyses it
-      else if (__any_sync(FULL, edang)) st = PAAM_SET_EDANGLING;
-      else if (__any_sync(FULL, eaccel)) st = PAAM_SET_EACCEL;
-      else if (__any_sync(FULL, eshape)) st = PAAM_SET_ESHAPE;
-      else if (n_sub > MAXS) st = PAAM_SET_ERANGE;
-      else if (__any_sync(FULL, edup)) st = PAAM_SET_EDUPPRIO;
-      else if (__any_sync(FULL, edl)) st = PAAM_SET_EDEADLINE;
-      else if (__any_sync(FULL, ecore)) st = PAAM_SET_ECORE;
+      {  // the rules in order (include/paam.h): one OR-reduction, the first failing rule decides
+        const uint32_t mine = (malformed ? 1u : 0u) | (erange ? 2u : 0u) | (wide ? 4u : 0u) | (edang ? 8u : 0u) |
+                              (eaccel ? 16u : 0u) | (eshape ? 32u : 0u) | (edup ? 128u : 0u) | (edl ? 256u : 0u) |
+                              (ecore ? 512u : 0u);
+        const uint32_t err = __reduce_or_sync(FULL, mine) | (n_sub > MAXS ? 64u : 0u);
+        if (err) {
+          const uint32_t i = __ffs(err) - 1;  // nibble i: the status of rule i (rule 2 = the u64 handover)
+          st = i == 2 ? REC_STATUS_WIDE : (int)((0x7651432012ull >> (4 * i)) & 0xfu);
+        }
+      }
     }
     if (!st2) { pcb = b.chain_cb_off[pc]; st2 = true; }
     if (st == REC_STATUS_WIDE) {  // every output of a handed-over set is wide_kernel's
