@@ -496,7 +496,7 @@ def run_ours(args):
             "algorithmic_bytes": alg_bytes, "bytes_per_set": alg_bytes / n,
             "peak_of": "measured (MEASURED_PEAKS.json hbm_gbs)" if pk else "fallback (B200_PROFILING.md)",
             "ncu_issue": issue.get("fused_kernel"),
-            "note": "one launch per step; per-launch CUDA events on the bench stream. The kernel is issue-bound "
+            "note": "two launches per step, fused_kernel and wide_kernel (whose list is empty for config 3); per-launch CUDA events on the bench stream. The kernel is issue-bound "
                     "(see issue): its HBM traffic is the raw batch once, the derived records stay on chip"}
     # issue roofline: warp-instructions per set (ncu) x sets/s vs 148 SMs x 4 schedulers x clock
     iss = issue.get("fused_kernel") or {}
