@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     cb0 = b.chain_cb_off[c0]; ncbo = b.chain_cb_off[nc];
     sg0 = b.cb_seg_off[cb0]; nsgo = b.cb_seg_off[ncbo];
   }
+  #pragma unroll 1
   for (uint32_t set = lo; set < hi; set++) {
     Record* r = recs + set;
     const uint32_t c1 = nc, x1 = nx, a1 = na_, cb1 = ncbo, sg1 = nsgo;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
 #ifndef PAAM_WARP_EMU
 #pragma unroll kStageUnroll
 #endif
+      #pragma unroll 1
       for (uint32_t i = lane; i < nseg; i += 32) {
         const uint64_t w = b.seg_wcet[sg0 + i];
         const uint32_t kind = b.seg_kind[sg0 + i], a = b.seg_accel[sg0 + i], u = b.seg_unit[sg0 + i];
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       // ---- callbacks: two passes of 32 lanes; each lane walks its segments ----------------------
       uint32_t prev_exec = 0xffffffffu;
       bool malformed = false;  // a callback's segment range leaves the set's: EDANGLING before segment checks
+      #pragma unroll 1
       for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
         const uint32_t j = pass * 32 + lane;
         uint32_t exec = 0xffffffffu, E = 0, na = 0, fa = 0, fu = 0, fw = 0;  // fa/fu/fw: first ACCEL segment
@@ -305,15 +308,18 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       n_sub = __popcll(runstart);
       __syncwarp();
       // A13: a chain never re-enters an executor it left
+      #pragma unroll 1
       for (uint32_t j = lane; j < ncb; j += 32) {
         if (((runstart >> j) & 1ull) && !((cstart >> j) & 1ull)) {
           const uint32_t first = 63 - __clzll(cstart & ((2ull << j) - 1));  // chain's first callback
+          #pragma unroll 1
           for (uint32_t i = first; i + 1 < j; i++) eshape |= (s.bExec[i] == s.bExec[j]);
         }
       }
       // chain ranks and duplicate priorities
       {
         uint32_t rk = 0;
+        #pragma unroll 1
         for (uint32_t d = 0; d < nch; d++) rk += (__shfl_sync(FULL, prio, d) > prio);
         rank = rk;
         const uint32_t valid = nch >= 32 ? FULL : (1u << nch) - 1u;
@@ -333,6 +339,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         }
         if (lane < nex) {
           s.xPPrank[lane] = (uint8_t)pr;
+          #pragma unroll 1
           for (uint32_t a = 0; a < nac; a++) ecore |= (xcore == s.aServer[a]);
         }
       }
@@ -384,6 +391,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     // per-callback first accelerator segment (exclusive scan over the callback order)
     {
       uint32_t carry = 0;
+      #pragma unroll 1
       for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
         const uint32_t j = pass * 32 + lane;
         const uint32_t na = j < ncb ? s.bNa[j] : 0u;
@@ -407,6 +415,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       if (k < nch) { s.rA0[k] = f; s.rNa[k] = (uint8_t)na; }
     }
     // sub-chain id of every callback
+    #pragma unroll 1
     for (uint32_t j = lane; j < ncb; j += 32) {
       const uint32_t sid = __popcll(runstart & ((2ull << j) - 1)) - 1;
       s.bSub[j] = (uint8_t)sid;
@@ -414,6 +423,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     }
     __syncwarp();
     // ---- accelerator segments: A*, unit, rank; written in rank order --------------------------------
+    #pragma unroll 1
     for (uint32_t pass = 0; pass * 32 < ncb; pass++) {
       const uint32_t j = pass * 32 + lane;
       if (j < ncb && s.bNa[j]) {
@@ -433,6 +443,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
           put(s.bFa[j], s.bFu[j], s.bFw[j]);
         } else {
           const uint32_t so = b.cb_seg_off[cb0 + j] - sg0, se = b.cb_seg_off[cb0 + j + 1] - sg0;
+          #pragma unroll 1
           for (uint32_t k = so; k < se; k++)  // the staged segments are intact until WFD / W
             if (s.gKind[k] == 1) put(s.gAcc[k], s.gUnit[k], s.gW[k]);
         }
@@ -443,11 +454,13 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     __syncwarp();
     // ---- per chain (lane = rank): W[k][u], max A*[u][k], accelerator use mask ------------------------
     uint32_t use = 0;
+    #pragma unroll 1
     for (uint32_t u = 0; u < n_unit; u++) s.maxA[u][lane] = 0;
     if (is_chain) {
       const uint32_t k = lane;
       reinterpret_cast<uint4*>(s.W[k])[0] = uint4{0u, 0u, 0u, 0u};
       reinterpret_cast<uint4*>(s.W[k])[1] = uint4{0u, 0u, 0u, 0u};
+      #pragma unroll 1
       for (uint32_t q = s.rA0[k]; q < s.rA0[k] + s.rNa[k]; q++) {
         const uint32_t u = s.qUnit[q], a = s.qAstar[q];
         use |= 1u << s.qAcc[q];
@@ -458,6 +471,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     __syncwarp();
     if (!st3) { psg = b.cb_seg_off[pcb]; st3 = true; }
     // ---- buckets (A5) and LP blocking per (unit, rank) ---------------------------------
+    #pragma unroll 1
     for (uint32_t a = 0; a < nac; a++) {
       const uint32_t U = __ballot_sync(FULL, (use >> a) & 1u);
       const uint32_t ma = __popc(U), n = s.aN[a];
@@ -469,6 +483,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       // users of a form aligned blocks of g consecutive positions, one block per bucket: the user at
       // position p is in bucket n - 1 - p / g (A5)
       const uint32_t blk_end = min(((((uint32_t)lane * ginv) >> 16) + 1) * g, ma);
+      #pragma unroll 1
       for (uint32_t u = s.aUbase[a]; u < s.aUbase[a] + s.aUnits[a]; u++) {
         if (user) s.cmp[p] = s.maxA[u][lane];
         __syncwarp();
@@ -488,6 +503,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       }
     }
     // 2 * sum_{k < r} W[k][u]: the "+1 +1" of mu summed over the HP chains (exact, saturating)
+    #pragma unroll 1
     for (uint32_t u = 0; u < n_unit; u++) {
       const uint32_t w = is_chain ? s.W[lane][u] : 0u;
       const uint32_t incl = scan_sat_incl(w, lane);
@@ -507,6 +523,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       s_rank = s.rank_of[c];
       s_key = ((uint32_t)s.xCore[s_exec] << 16) | ((uint32_t)s.xPPrank[s_exec] << 8) | s_rank;
       uint32_t mE = 0;
+      #pragma unroll 1
       for (uint32_t j = s_j0; j < s_j0 + s_nj; j++) { mE = max(mE, s.bE[j]); s_E = sadd(s_E, s.bE[j]); }
       s.sMaxE[lane] = mE;
       s.sRank[lane] = (uint8_t)s_rank;
@@ -515,6 +532,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
     // canonical order (A7): per core, process priority desc, chain rank asc
     {
       uint32_t pos = 0;
+      #pragma unroll 1
       for (uint32_t l = 0; l < n_sub; l++) pos += (__shfl_sync(FULL, s_key, l) < s_key);
       if ((uint32_t)lane < n_sub) s.sCanon[lane] = (uint8_t)pos;
     }
@@ -530,6 +548,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       const uint32_t qn = s.bA0[s_j0 + s_nj] - s.bA0[s_j0];
       const uint32_t E = s_E;
       uint32_t eps = 0, base3 = 0, umask = 0, slb = 0;
+      #pragma unroll 1
       for (uint32_t q = qa; q < qa + qn; q++) {
         const uint32_t u = s.qUnit[q];
         eps = sadd(eps, s.aEps[s.qAcc[q]]);
@@ -539,6 +558,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         umask |= 1u << u;
       }
       uint32_t a2 = base3;  // Eq.4 with every mu = 2 (the union of hps over the sub-chain's units, A1)
+      #pragma unroll 1
       for (uint32_t um = umask; um; um &= um - 1) a2 = sadd(a2, s.pre2[__ffs(um) - 1][s_rank]);
       uint32_t hp = 0, lp = 0, hpp = 0, B = 0;
       uint32_t m = same_exec & ~(1u << lane);
@@ -581,10 +601,12 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       r->cD[k] = s.rD[k];
       r->cM[k] = M;
       r->cMisc[k] = L | ((uint32_t)s.rCls[k] << 8) | ((uint32_t)s.rIdx[k] << 16) | (nsub << 24);
+      #pragma unroll 1
       for (uint32_t u = 0; u < n_unit; u++) r->W[k][u] = s.W[k][u];
     }
     {  // period order (ascending T, ties by rank)
       uint32_t pos = 0;
+      #pragma unroll 1
       for (uint32_t j = 0; j < nch; j++) {
         const uint32_t Tj = __shfl_sync(FULL, Tk, j);
         pos += (Tj < Tk) || (Tj == Tk && j < (uint32_t)lane);
@@ -594,6 +616,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
       if (lane == 0) r->hflags = 0u;
     }
     // ---- accelerator segments (rank order) ------------------------------------------------------------
+    #pragma unroll 1
     for (uint32_t q = lane; q < n_aseg; q += 32) {
       const uint32_t u = s.qUnit[q], rk = s.qRank[q];
       r->aBase2[q] = sadd(sadd(s.qAstar[q], s.maxA[u][rk]), s.pre2[u][rk]);
