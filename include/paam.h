@@ -224,8 +224,12 @@ int paam_admit(const paam_sets* sets, uint32_t n, int32_t* out_decision, uint64_
  * chunk; with pinned host memory the copies are asynchronous, so the caller must not modify the batch
  * until `stream` has completed.  Same results as paam_repack followed by paam_analyze; `sets` must
  * have capacity for batch->n_sets (from paam_pack).  out_status is in the batch's memory space; a host
- * out_status makes the call synchronise `stream` (as paam_repack).  The handle keeps the batch for a
- * later paam_analyze / paam_admit / paam_simulate (which then pack it first). */
+ * out_status makes the call synchronise `stream` (as paam_repack).  With a host batch, out_wcrt and
+ * out_sched may be host memory too (pinned for asynchrony): the kernels write a device staging copy and
+ * each chunk's WCRTs and verdicts are copied back as soon as its kernels finish, overlapping the next
+ * chunk's H2D; they are complete when `stream` is.  With a device batch they must be device memory
+ * (PAAM_EINVAL otherwise).  out_bins is always device memory (accumulated).  The handle keeps the batch
+ * for a later paam_analyze / paam_admit / paam_simulate (which then pack it first). */
 int paam_pack_analyze(const paam_batch* batch, paam_sets* sets, int32_t* out_status, uint64_t* out_wcrt,
                       uint8_t* out_sched, int64_t* out_bins, paam_stream_t stream);
 

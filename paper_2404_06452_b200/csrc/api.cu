@@ -25,6 +25,8 @@ struct paam_sets {
                           // 20: number of wide sets listed (wide.cu), 21: fused_kernel's work ticket
   uint32_t* wide_list;    // [cap] the sets handed over to the u64 path by the last pack / fused launch
   int device;             // the CUDA device the handle lives on (made current by every call)
+  void* ostage;           // device staging of host outputs of paam_pack_analyze (WCRTs, then verdicts)
+  size_t ostage_bytes;
   void* sim_scratch;      // paam_simulate's event buffers (grown on demand)
   size_t sim_scratch_bytes;
   bool c32;               // dev is a compact batch (paam_pack_analyze32): nothing can pack it into records
@@ -107,6 +109,25 @@ int ensure_dstatus(paam_sets* sets, uint32_t n) {
   const cudaError_t e = cudaMalloc((void**)&sets->dstatus, sizeof(int32_t) * (n ? n : 1));
   if (e != cudaSuccess) return fail_cuda(e, "status cudaMalloc");
   sets->dstatus_cap = n;
+  return PAAM_OK;
+}
+// Is p host memory (pinned or pageable)?  Device and managed pointers are not.
+bool is_host_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // pageable memory on old drivers reports an error: clear it
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+int ensure_ostage(paam_sets* sets, size_t bytes) {
+  if (sets->ostage_bytes >= bytes) return PAAM_OK;
+  if (sets->ostage) cudaFree(sets->ostage);
+  sets->ostage = nullptr;
+  sets->ostage_bytes = 0;
+  const cudaError_t e = cudaMalloc(&sets->ostage, bytes);
+  if (e != cudaSuccess) return fail_cuda(e, "output staging cudaMalloc");
+  sets->ostage_bytes = bytes;
   return PAAM_OK;
 }
 int ensure_streams(paam_sets* sets) {
@@ -312,6 +333,9 @@ int pack_analyze_impl(const paam_batch* batch, bool c32, paam_sets* sets, int32_
   paam_batch d = *batch;  // the batch the kernel reads (host: pointers into the staging buffer)
   d._pad = 0;
   int32_t* status_dev = out_status;
+  const bool wcrt_host = out_wcrt && is_host_ptr(out_wcrt), sched_host = out_sched && is_host_ptr(out_sched);
+  if (!host && (wcrt_host || sched_host))
+    return fail(PAAM_EINVAL, "paam_pack_analyze: host out_wcrt / out_sched need a host batch");
   if (!host) {
     // steps 2-6 in one kernel (fused.cu): the derived records stay on chip
     cudaMemsetAsync(sets->tickets + 20, 0, 2 * sizeof(unsigned int), st);  // wide count, work ticket
@@ -360,6 +384,16 @@ int pack_analyze_impl(const paam_batch* batch, bool c32, paam_sets* sets, int32_
       if ((rc = ensure_dstatus(sets, n))) return rc;
       status_dev = sets->dstatus;
     }
+    // Host outputs: the kernels write a device staging copy and each chunk's WCRTs / verdicts go back on
+    // side[1] as soon as the chunk's kernels are done, overlapping the next chunk's H2D (PCIe is duplex).
+    uint64_t* wcrt_dev = out_wcrt;
+    uint8_t* sched_dev = out_sched;
+    if (wcrt_host || sched_host) {
+      const size_t wb = wcrt_host ? align256(sizeof(uint64_t) * (size_t)batch->n_chains) : 0;
+      if ((rc = ensure_ostage(sets, wb + (sched_host ? (size_t)n : 0) + 1))) return rc;
+      if (wcrt_host) wcrt_dev = (uint64_t*)sets->ostage;
+      if (sched_host) sched_dev = (uint8_t*)sets->ostage + wb;
+    }
     cudaEventRecord(sets->ev[16], st);
     for (int i = 0; i < 3; i++) cudaStreamWaitEvent(sets->side[i], sets->ev[16], 0);
     for (int i = 0; i < K; i++) {
@@ -396,19 +430,33 @@ int pack_analyze_impl(const paam_batch* batch, bool c32, paam_sets* sets, int32_
       view.set_accel_off += lo;
       if (view.set_bin) view.set_bin += lo;
       cudaMemsetAsync(sets->tickets + 20, 0, 2 * sizeof(unsigned int), sets->side[0]);  // wide count, work ticket
-      if ((rc = launch_fused(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
-                             out_sched ? out_sched + lo : nullptr,
+      if ((rc = launch_fused(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, wcrt_dev,
+                             sched_dev ? sched_dev + lo : nullptr,
                              const_cast<int64_t*>(bins), sets->side[0], c32)))
         return rc;
-      if ((rc = launch_wide(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, out_wcrt,
-                            out_sched ? out_sched + lo : nullptr, const_cast<int64_t*>(bins), nullptr, sets->side[0],
+      if ((rc = launch_wide(&view, sets->wide_list, sets->tickets + 20, status_dev ? status_dev + lo : nullptr, wcrt_dev,
+                            sched_dev ? sched_dev + lo : nullptr, const_cast<int64_t*>(bins), nullptr, sets->side[0],
                             c32)))
         return rc;
+      if (wcrt_host || sched_host) {
+        cudaEventRecord(sets->ev[i], sets->side[0]);
+        cudaStreamWaitEvent(sets->side[1], sets->ev[i], 0);
+        if (wcrt_host && ch > cl &&
+            (e = cudaMemcpyAsync(out_wcrt + cl, wcrt_dev + cl, sizeof(uint64_t) * (ch - cl), cudaMemcpyDeviceToHost,
+                                 sets->side[1])) != cudaSuccess)
+          return fail_cuda(e, "paam_pack_analyze: WCRT D2H");
+        if (sched_host && hi > lo &&
+            (e = cudaMemcpyAsync(out_sched + lo, sched_dev + lo, hi - lo, cudaMemcpyDeviceToHost, sets->side[1])) !=
+                cudaSuccess)
+          return fail_cuda(e, "paam_pack_analyze: verdict D2H");
+      }
     }
     cudaEventRecord(sets->ev[9], sets->side[0]);
     cudaEventRecord(sets->ev[10], sets->side[2]);
+    cudaEventRecord(sets->ev[11], sets->side[1]);
     cudaStreamWaitEvent(st, sets->ev[9], 0);
     cudaStreamWaitEvent(st, sets->ev[10], 0);
+    cudaStreamWaitEvent(st, sets->ev[11], 0);
     if (out_status) {  // host status, as paam_repack: copied back, the call synchronises
       if ((e = cudaMemcpyAsync(out_status, status_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return fail_cuda(e, "paam_pack_analyze: status D2H");
@@ -478,6 +526,7 @@ extern "C" void paam_free(paam_sets* sets) {
   if (sets->stage) cudaFree(sets->stage);
   if (sets->dstatus) cudaFree(sets->dstatus);
   if (sets->sim_scratch) cudaFree(sets->sim_scratch);
+  if (sets->ostage) cudaFree(sets->ostage);
   if (sets->side[0]) {
     for (int i = 0; i < 3; i++) cudaStreamDestroy(sets->side[i]);
     for (int i = 0; i < 17; i++) cudaEventDestroy(sets->ev[i]);

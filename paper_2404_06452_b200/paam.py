@@ -394,9 +394,11 @@ class Sets:
                                _stream_ptr(stream)), "paam_admit")
 
     def pack_analyze(self, batch, out_wcrt=None, out_sched=None, out_bins=None, out_status=None, stream=None):
-        """Pipelined repack + analyze (paam_pack_analyze).  Outputs: device tensors or None; out_status in
-        the batch's memory space (numpy array for a host batch, device tensor for a device batch)."""
-        ptr = lambda t: None if t is None else t.data_ptr()
+        """Pipelined repack + analyze (paam_pack_analyze).  Outputs: device tensors or None; for a host batch
+        out_wcrt / out_sched may also be host memory (numpy arrays or pinned CPU tensors), copied back chunk
+        by chunk; out_status in the batch's memory space (numpy array for a host batch, device tensor for a
+        device batch)."""
+        ptr = lambda t: None if t is None else (t.ctypes.data if isinstance(t, np.ndarray) else t.data_ptr())
         st = None if out_status is None else (out_status.ctypes.data if isinstance(out_status, np.ndarray)
                                              else out_status.data_ptr())
         if isinstance(batch, Batch32):

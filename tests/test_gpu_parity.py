@@ -550,3 +550,32 @@ def test_invalid_segment_kind_is_not_counted_as_an_accelerator_segment():
     _, _, st, _ = O.analyze(b)
     assert st.tolist() == [0, 4]  # OK, ESHAPE
     assert_same(b, gpu_host_path(b))
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_outputs_of_a_host_batch(pinned):
+    """A host batch may write its WCRTs and verdicts straight into host memory (pageable numpy or pinned
+    tensors): the library copies each chunk back as its kernels finish; the results equal the oracle's,
+    for the u64 and the compact batch.  Host outputs with a device batch are refused."""
+    p = config3_params()
+    g = generate_host(p, 4, 0, 20_000)
+    ow, osch, _, ob = O.analyze(g, nthreads=NPROC)
+    hb = paam.Batch.from_host(g)
+    sets = paam.Sets(hb)
+    for batch in (hb, paam.Batch32.from_host(g)):
+        if pinned:
+            w = torch.zeros(hb.c.n_chains, dtype=torch.int64, pin_memory=True)
+            sc = torch.zeros(g["n_sets"], dtype=torch.uint8, pin_memory=True)
+        else:
+            w = np.zeros(hb.c.n_chains, np.uint64)
+            sc = np.zeros(g["n_sets"], np.uint8)
+        bins = torch.zeros(2 * p.n_bins, dtype=torch.int64, device="cuda")
+        sets.pack_analyze(batch, w, sc, bins)
+        torch.cuda.synchronize()
+        wn = w.numpy().view(np.uint64) if pinned else w
+        scn = sc.numpy() if pinned else sc
+        assert np.array_equal(wn, ow) and np.array_equal(scn, osch)
+        assert np.array_equal(bins.cpu().numpy(), ob)
+    db = paam.Batch.from_host_to_device(g)
+    with pytest.raises(paam.PaamError, match="host batch"):
+        sets.pack_analyze(db, np.zeros(hb.c.n_chains, np.uint64), None, None)
