@@ -422,6 +422,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
           evbuf + ((size_t)blockIdx.x * SW + (threadIdx.x >> 5)) * EVCAP};
     uint32_t next_k = 0;  // lane = rank
     uint64_t next_rel = (uint32_t)lane < nch ? S.cPhase[lane] : NONE64;  // release time of instance next_k (D2)
+    bool rel_live = (uint32_t)lane < nch && next_rel < horizon;  // a release is pending (below the horizon)
+    uint32_t rel32 = (uint32_t)next_rel;                          // its low 32 bits (< 2^31 ahead of t)
     uint32_t seq = 0;     // warp-uniform
     bool on_core = false; // lane = canonical executor
     uint32_t drops = 0;
@@ -524,8 +526,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
                 const uint32_t q = slot_of(tm);
                 if (S.iw[c][q].ready_at == C.t32()) { byte_of(S.iState[c], q) = I_READY; }
               }
-            const uint64_t r = next_rel;
-            if (r == C.t && r < horizon) {
+            if (rel_live && rel32 == C.t32()) {
               if (S.cCls[c] == 1)
                 for (uint32_t dm = slots_eq(S.iState[c], I_READY) & slots_eq(S.iCb[c], 0); dm; dm &= dm - 1) {
                   byte_of(S.iState[c], slot_of(dm)) = I_FREE;
@@ -543,7 +544,8 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               }
               next_k++;
               next_rel += S.cT[c];
-             
+              rel_live = next_rel < horizon;
+              rel32 = (uint32_t)next_rel;
             }
           }
           __syncwarp();
@@ -736,8 +738,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
       uint32_t nd_c = 0xffffffffu, nd_x = 0xffffffffu, nd_u = 0xffffffffu;  // none
       bool run_x = false;  // executor whose remaining work shrinks with time
       if (is_chain) {
-        const uint64_t r = next_rel;
-        if (r < horizon) nd_c = (uint32_t)(r - C.t);
+        if (rel_live) nd_c = rel32 - C.t32();
         if (may_transit)
           for (uint32_t tm = slots_eq(S.iState[lane], I_TRANSIT); tm; tm &= tm - 1)
             nd_c = min(nd_c, S.iw[lane][slot_of(tm)].ready_at - C.t32());
