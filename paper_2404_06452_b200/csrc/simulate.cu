@@ -88,6 +88,7 @@ struct DesSmem {
   uint8_t bSeg0[MAXCB];
   uint32_t gW[MAXG];
   uint8_t gKind[MAXG], gUnit[MAXG], gBkt[MAXG];
+  uint8_t cuBkt[MAXC][MAXU];  // bucket of chain rank k on unit u (per chain and accelerator)
   uint32_t xSameCore[MAXX];
   uint8_t xWait[MAXX];
   uint32_t uEps[MAXU], uKap[MAXU], uN[MAXU];
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         const uint32_t gsz = ma ? (ma + nb - 1) / nb : 1u;
         bk[a] = nb - 1 - __popc(U & lt) / gsz;
       }
-      if (lane < nch)
+      if (lane < nch) {
         for (uint32_t j = S.cCb0[lane]; j < S.cCb0[lane] + S.cNcb[lane]; j++)
           for (uint32_t g = S.bSeg0[j]; g < S.bSeg0[j] + S.bNseg[j]; g++)
             if (S.gKind[g] == 1) {
@@ -402,6 +403,12 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
               for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= S.gUnit[g]) a = q;
               S.gBkt[g] = (sim_flags & PAAM_SIM_FIFO_DIRECT) ? (uint8_t)0 : (uint8_t)bk[a];
             }
+        for (uint32_t u = 0; u < MAXU; u++) {
+          uint32_t a = 0;
+          for (uint32_t q = 1; q < nac; q++) if (ubase[q] <= u) a = q;
+          S.cuBkt[lane][u] = (sim_flags & PAAM_SIM_FIFO_DIRECT) ? (uint8_t)0 : (uint8_t)bk[a];
+        }
+      }
     }
     // dynamic state
     if (lane < MAXC) {
@@ -676,10 +683,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             }
             if (bslot >= 0) {
               InstRef I = S.ref(lane, bslot);
-              const uint32_t g = S.bSeg0[S.cCb0[lane] + I.cb];  // bucket is per (chain, accelerator)
-              uint32_t bkt = 0;
-              for (uint32_t gg = g; gg < g + S.bNseg[S.cCb0[lane] + I.cb]; gg++)
-                if (S.gKind[gg] == 1 && S.gUnit[gg] == u) bkt = S.gBkt[gg];
+              const uint32_t bkt = S.cuBkt[lane][u];  // the bucket is per (chain, accelerator)
               key = 1u + ((bkt << 6) | ((uint32_t)I.started << 5) | (31u - lane));
             }
           }
