@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
     if (is_chain)
       for (uint32_t j = S.cCb0[lane]; j + 1 < (uint32_t)S.cCb0[lane] + S.cNcb[lane]; j++)
         may_transit |= S.bExec[j] != S.bExec[j + 1];
+    const uint32_t one_x = is_chain ? 1u << S.bExec[S.cCb0[lane]] : 0u;  // its executor, if it has only one
 
     for (;;) {
       // ===================== settle time t (D15) =====================
@@ -566,9 +567,14 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
         bool needB = false, dueB = false;  // another phase-B pass could act / B left phase-A work due now
         uint32_t ready_x = 0;  // lane = rank: executors where this chain has a READY instance
         if (is_chain) {
-          const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
-          for (uint32_t rm = slots_eq(S.iState[lane], I_READY); rm; rm &= rm - 1)
-            ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * slot_of(rm))) & 0xffu)];
+          const uint32_t rm0 = slots_eq(S.iState[lane], I_READY);
+          if (!may_transit) {
+            ready_x = rm0 ? one_x : 0u;  // every callback of the chain runs on one executor
+          } else {
+            const uint32_t cbw = S.iCb[lane], cb0 = S.cCb0[lane];
+            for (uint32_t rm = rm0; rm; rm &= rm - 1)
+              ready_x |= 1u << S.bExec[cb0 + ((cbw >> (8 * slot_of(rm))) & 0xffu)];
+          }
         }
         const uint32_t has_ready = __reduce_or_sync(FULL, ready_x);
         const uint32_t want = __ballot_sync(FULL, is_exec && on_core && S.exPhase[lane] == P_NONE && ((has_ready >> lane) & 1u));
@@ -600,9 +606,14 @@ __global__ void __launch_bounds__(SW * 32, SIM_MINB) simulate_kernel(paam_batch 
             // this chain no longer offers that instance
             ready_x = 0;
             {
-              const uint32_t cbw2 = S.iCb[c], cb0 = S.cCb0[c];
-              for (uint32_t rm = slots_eq(S.iState[c], I_READY); rm; rm &= rm - 1)
-                ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * slot_of(rm))) & 0xffu)];
+              const uint32_t rm0 = slots_eq(S.iState[c], I_READY);
+              if (!may_transit) {  // lane == c: this chain's own registers
+                ready_x = rm0 ? one_x : 0u;
+              } else {
+                const uint32_t cbw2 = S.iCb[c], cb0 = S.cCb0[c];
+                for (uint32_t rm = rm0; rm; rm &= rm - 1)
+                  ready_x |= 1u << S.bExec[cb0 + ((cbw2 >> (8 * slot_of(rm))) & 0xffu)];
+              }
             }
           }
           __syncwarp();
