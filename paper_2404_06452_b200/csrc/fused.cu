@@ -64,8 +64,8 @@ struct FSmem {
     };
     struct {  // chains by rank / period order (written after that pass)
       uint2 cML[MAXC];      // mu magic (M, L) by rank (Lemma 2)
-      uint8_t posOf[MAXC];  // period position of chain rank k
-      uint8_t sPos[MAXS];   // period position of sub-chain h's chain
+      uint8_t posOf[MAXC];  // pTab slot (31 - period position) of chain rank k
+      uint8_t sPos[MAXS];   // pTab slot of sub-chain h's chain
     };
   };
   // accelerator segments (rank order)
@@ -108,7 +108,7 @@ struct FSmem {
       uint8_t gMeta[MAXSEG];  // kind | accelerator << 1 | unit << 3 (the values of a valid set fit)
     };
     struct {  // what a lane reads of other lanes / chains
-      uint4 pTab[MAXC];  // period order: {T, M, rank | L << 8, W[rank][0] + W[rank][1]}
+      uint4 pTab[MAXC];  // period order: {T, M, L | rank << 8, W[rank][0] + W[rank][1]} (f_shr: L < 32)
       uint32_t sE[MAXS], sEps[MAXS];
       uint32_t aBase[MAXA];  // Lemma-2 start value A* + LPB + 2 sum_{k<r} W[k][u] of each segment
     };
@@ -180,9 +180,8 @@ __device__ PAAM_COLD uint32_t f_lemma2(const FSmem& s, uint32_t q) {
 #pragma unroll 1
     for (uint32_t k = 0; k < rk; k++) {
       const uint2 ml = s.cML[k];
-      const uint64_t p = (uint64_t)(__umulhi(h2, ml.x) >> ml.y) * s.W[k][u];
-      acc += p;
-      hi |= (uint32_t)(p >> 32);
+      acc += (uint64_t)(__umulhi(h2, ml.x) >> ml.y) * s.W[k][u];
+      hi |= (uint32_t)(acc >> 32);  // latched high word (f_eval: no wrap before a latch)
     }
     if (hi || acc > cut) break;
     const uint32_t g = (uint32_t)acc;
@@ -217,33 +216,47 @@ __device__ PAAM_COLD uint32_t f_sound_blocking(const FSmem& s, uint32_t B, uint3
   return B;
 }
 
+// x >> (z mod 32) in one funnel shift (wrap mode): z = L | rank << 8 with L = ceil(log2 T) <= 31
+__device__ __forceinline__ uint32_t f_shr(uint32_t x, uint32_t z) { return __funnelshift_r(x, 0u, z); }
+// the index of the highest set bit of m != 0 in one FLO (31 - __clz(m) compiles to three instructions)
+__device__ __forceinline__ uint32_t f_hibit(uint32_t m) {
+#ifdef PAAM_WARP_EMU
+  return 31u - (uint32_t)__clz(m);
+#else
+  uint32_t i;
+  asm("bfind.u32 %0, %1;" : "=r"(i) : "r"(m));
+  return i;
+#endif
+}
+
 // Eq.5 evaluation, as analyze.cu's eval_eq5 (see there), reading the shared period table.  nxt: the
 // smallest R' > R at which one of the floor terms floor((R' - 1) / T) differs from its value at R (a term
 // with q = floor((R - 1) / T) changes at R' = (q + 1) T + 1); below it F and C are those at R, as long
-// as the interferers' H* are unchanged.
-template <bool WIDE>
-__device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmask, uint32_t wsel, uint32_t umask,
-                                       uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut, uint32_t xm,
-                                       uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F, uint32_t& nH,
-                                       uint32_t& C, uint32_t& nxt) {
-  const uint32_t h2 = (R - 1u) << 1;
+// as the interferers' H* are unchanged.  The loops track nm = nxt - 1 = min (q + 1) T (one multiply-add).
+// Overflow: every product is < 2^62 (q <= R - 1 < 2^31, every weight <= SAT), so a 64-bit sum that is
+// still < 2^32 cannot wrap in one addition; hi latches the sum's high word after each one, and any
+// nonzero latch saturates (every intermediate sum only grows until then): one multiply-add and one OR
+// per term.
+// Lemma 3's floor terms: W = the weight column of the chain (WSEL false: the table's own
+// two-unit sum; true: the sub-chain's units, wsel as in f_eval).
+template <bool WSEL>
+__device__ __forceinline__ uint64_t f_lemma3(const FSmem& s, uint32_t R, uint32_t h2, uint32_t lmask, uint32_t wsel,
+                                             uint32_t umask, uint32_t& hi, uint32_t& nm) {
   uint64_t acc = 0;
-  uint32_t hi = 0;
-  uint32_t nx = 0xffffffffu;  // (q + 1) T + 1 < 2^32 for R, T < 2^31
   #pragma unroll 1
   for (uint32_t m = lmask; m;) {
-    const uint32_t i = __ffs(m) - 1;
+    const uint32_t i = f_hibit(m);  // the shortest remaining period (pTab slot 31 - position)
     const uint4 p = s.pTab[i];
-    if (p.x >= R) { nx = min(nx, p.x + 1u); break; }  // this and every later (longer) period: q = 0
-    m &= m - 1;
+    if (p.x >= R) { nm = min(nm, p.x); break; }  // this and every later (longer) period: q = 0
+    m ^= 1u << i;
 #ifdef PAAM_EMU_STATS
     atomicAdd(&emu_stats[3], 1ull);  // Lemma-3 floor terms
 #endif
-    const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
-    nx = min(nx, (q + 1u) * p.x + 1u);
+    const uint32_t q = f_shr(__umulhi(h2, p.y), p.z);
+    nm = min(nm, q * p.x + p.x);
     uint32_t wu = p.w;
-    if (wsel) {
-      const uint32_t k = p.z & 0xffu;
+    if (WSEL) {
+      const uint32_t k = p.z >> 8;
       if (wsel <= MAXU) {
         wu = s.W[k][wsel - 1];
       } else {
@@ -252,28 +265,35 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
         for (uint32_t um = umask; um; um &= um - 1) wu = sadd(wu, s.W[k][__ffs(um) - 1]);
       }
     }
-    if (WIDE) {
-      acc += (uint64_t)q * wu;
-    } else {
-      const uint64_t pr = (uint64_t)q * wu;
-      acc += pr;
-      hi |= (uint32_t)(pr >> 32);
-    }
+    acc += (uint64_t)q * wu;
+    hi |= (uint32_t)(acc >> 32);
   }
+  return acc;
+}
+
+__device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmask, uint32_t wsel, uint32_t umask,
+                                       uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut, uint32_t xm,
+                                       uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F, uint32_t& nH,
+                                       uint32_t& C, uint32_t& nxt) {
+  const uint32_t h2 = (R - 1u) << 1;
+  uint32_t hi = 0;
+  uint32_t nm = 0xfffffffeu;  // (q + 1) T <= 2^32 - 4 for R, T < 2^31
+  uint64_t acc = wsel ? f_lemma3<true>(s, R, h2, lmask, wsel, umask, hi, nm)
+                      : f_lemma3<false>(s, R, h2, lmask, wsel, umask, hi, nm);
   acc += A2;
   C = (hi || acc > SAT) ? SAT : (uint32_t)acc;
   nH = sadd(min(S, C), eps);
   uint64_t xs = xs2;
+  uint32_t xhi = 0;
   #pragma unroll 1
   for (uint32_t m = depm; m; m &= m - 1) {
     const uint32_t h = __ffs(m) - 1;
     const uint32_t X = sadd(s.sE[h], s.Hs[h]);
     const uint4 p = s.pTab[s.sPos[h]];
-    const uint32_t q = p.x < R ? (__umulhi(h2, p.y) >> (p.z >> 8)) : 0u;
-    nx = min(nx, (q + 1u) * p.x + 1u);
-    const uint64_t pr = (uint64_t)(q + 2u) * X;
-    xs += pr;
-    if (!WIDE) hi |= (uint32_t)(pr >> 32);
+    const uint32_t q = p.x < R ? (f_shr(__umulhi(h2, p.y), p.z)) : 0u;
+    nm = min(nm, q * p.x + p.x);
+    xs += (uint64_t)(q + 2u) * X;
+    xhi |= (uint32_t)(xs >> 32);
   }
   if (R > xTmin) {
     #pragma unroll 1
@@ -281,21 +301,20 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
       const uint32_t h = __ffs(m) - 1;
       const uint4 p = s.pTab[s.sPos[h]];
       if (p.x < R) {
-        const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
-        nx = min(nx, (q + 1u) * p.x + 1u);
-        const uint64_t pr = (uint64_t)q * sadd(s.sE[h], s.sEps[h]);
-        xs += pr;
-        if (!WIDE) hi |= (uint32_t)(pr >> 32);
+        const uint32_t q = f_shr(__umulhi(h2, p.y), p.z);
+        nm = min(nm, q * p.x + p.x);
+        xs += (uint64_t)q * sadd(s.sE[h], s.sEps[h]);
+        xhi |= (uint32_t)(xs >> 32);
       } else {
-        nx = min(nx, p.x + 1u);
+        nm = min(nm, p.x);
       }
     }
   } else if (xTmin != 0xffffffffu) {
-    nx = min(nx, xTmin + 1u);  // every such interferer has T >= R: q = 0 up to its T
+    nm = min(nm, xTmin);  // every such interferer has T >= R: q = 0 up to its T
   }
-  nxt = nx;
+  nxt = nm + 1u;
   const uint64_t f = (uint64_t)BE + nH + xs;
-  F = (hi || f > cut) ? SAT : (uint32_t)f;
+  F = (hi || xhi || f > cut) ? SAT : (uint32_t)f;
   if (F == SAT) nH = SAT;
 }
 
@@ -706,8 +725,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         if (is_chain) {
           make_magic(T, &M, &L);
           s.cML[rank] = uint2{M, L};
-          s.pTab[ppos] = uint4{T, M, rank | (L << 8), sadd(s.W[rank][0], s.W[rank][1])};
-          s.posOf[rank] = (uint8_t)ppos;
+          // slot 31 - ppos: the shortest period is a mask's highest bit (f_lemma3 walks down from it)
+          s.pTab[31u - ppos] = uint4{T, M, L | (rank << 8), sadd(s.W[rank][0], s.W[rank][1])};
+          s.posOf[rank] = (uint8_t)(31u - ppos);
         }
       }
       __syncwarp();
@@ -801,7 +821,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       const uint32_t xm = hpm | hppm;
       const bool critical = act && s.rCls[rk] == 0;
       bool sexact = !lazy_s;
-      // ---- lmask: period positions of the chains of rank < rk (exclusive OR-scan over ranks)
+      // ---- lmask: pTab slots of the chains of rank < rk (exclusive OR-scan over ranks)
       uint32_t pb = is_chain ? (1u << s.posOf[lane]) : 0u;  // lane = rank
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -845,7 +865,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         if (dirty) {
           // one (checked) copy of the evaluation: the unchecked one for periods >= 64 ns saved one
           // instruction per floor term but doubled the loop's code (instruction-cache stalls)
-          f_eval<false>(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
+          f_eval(s, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
         }
         const bool chg = dirty && (F != R || nH != Hst);
         const uint32_t cm = __ballot_sync(FULL, chg);
