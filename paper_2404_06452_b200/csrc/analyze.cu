@@ -51,9 +51,9 @@ constexpr uint32_t FULL = 0xffffffffu;
 // Lemma 2 (Eq.3) for accelerator segment i: the least fixed point of
 // G(h) = aBase2 + sum_{k<r} floor((h-1)/T_k) * W[k][u] from aBase2, or SAT (UNB) once an iterate
 // exceeds the cutoff (A4).  aBase2 already holds A* + LPB + 2 sum_{k<r} W[k][u] (the "+2" of every mu),
-// so the start is G's value for floor(.) = 0, <= the least fixed point (A3).  Products are 64-bit; a
-// product >= 2^32 (high word != 0) is far above every cutoff, and without one the 64-bit sum of <= 31
-// products cannot overflow.
+// so the start is G's value for floor(.) = 0, <= the least fixed point (A3).  Products are 64-bit and
+// < 2^62; the sum's high word is latched after each addition (a sum >= 2^32 is far above every cutoff,
+// and one < 2^32 cannot wrap in one addition).
 __device__ __forceinline__ uint32_t lemma2(const Record& r, uint32_t i) {
   const uint32_t misc = r.aMisc[i];
   const uint32_t rk = misc & 0xffu, u = (misc >> 8) & 0xffu;
@@ -65,10 +65,8 @@ __device__ __forceinline__ uint32_t lemma2(const Record& r, uint32_t i) {
     uint32_t hi = 0;
 #pragma unroll 2
     for (uint32_t k = 0; k < rk; k++) {
-      const uint32_t q = __umulhi(h2, r.cM[k]) >> (r.cMisc[k] & 31u);
-      const uint64_t p = (uint64_t)q * r.W[k][u];
-      acc += p;
-      hi |= (uint32_t)(p >> 32);
+      acc += (uint64_t)f_shr(__umulhi(h2, r.cM[k]), r.cMisc[k]) * r.W[k][u];
+      hi |= (uint32_t)(acc >> 32);  // latched high word (eval_eq5)
     }
     if (hi || acc > cut) break;
     const uint32_t g = (uint32_t)acc;
@@ -78,36 +76,25 @@ __device__ __forceinline__ uint32_t lemma2(const Record& r, uint32_t i) {
   return SAT;
 }
 
-// One Eq.5 evaluation F_c(R) (Theorem 1, P:1126-1128) for R >= 1, with mu(R, T) = 2 + floor((R-1)/T)
-// (Eq.2): the mu = 2 parts come precomputed (A2 = base3 + 2 sum WU for Lemma 3, xs2 = 2 sum X_h of the
-// static interferers), and the floor parts are added only for periods T < R -- for the Lemma-3 chains
-// by walking their period positions (lmask) in ascending period order up to the first T >= R.
-// C = C_c(R) (Eq.4, union form A1), nH = H*_c(R) = min(S, C) + eps (Eq.1, P:1092), F = B + E + H* +
-// the hp / hpp interference (SAT = above the cutoff: UNSCHED, A4; then H* = SAT poisons dependants, A8).
-// WIDE: every period >= 64 ns, so q * W < 2^56 and the u64 sums of <= 64 products cannot overflow;
-// otherwise every product's high word is checked.
-template <bool WIDE>
-__device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uint32_t R, uint32_t lmask, uint32_t wsel,
-                                         uint32_t umask, uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut,
-                                         uint32_t xm, uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F,
-                                         uint32_t& nH, uint32_t& C, uint32_t& nxt) {
-  // nxt: the smallest R' > R at which a floor term floor((R' - 1) / T) differs from its value at R (a term
-  // with q = floor((R - 1) / T) changes at (q + 1) T + 1 < 2^32); below it F and C are those at R while
-  // the interferers' H* are unchanged (fused.cu f_eval)
-  const uint32_t h2 = (R - 1u) << 1;
+// Lemma 3's floor terms (Eq.4) for the periods T < R of lmask, walked from the shortest: bit
+// 31 - position of lmask is pTab[position] (ascending periods), so the highest bit comes first.  WSEL:
+// the weight is not the table's two-unit sum (see eval_eq5).  Overflow: every product is < 2^62 (q <=
+// R - 1 < 2^31, every weight <= SAT), so a sum still < 2^32 cannot wrap in one addition; hi latches the
+// sum's high word after each one and any nonzero latch saturates.  nm = min (q + 1) T (nxt - 1).
+template <bool WSEL>
+__device__ __forceinline__ uint64_t lemma3_terms(const Record& r, uint32_t R, uint32_t h2, uint32_t lmask,
+                                                 uint32_t wsel, uint32_t umask, uint32_t& hi, uint32_t& nm) {
   uint64_t acc = 0;
-  uint32_t hi = 0;
-  uint32_t nx = 0xffffffffu;
   for (uint32_t m = lmask; m;) {
-    const uint32_t i = __ffs(m) - 1;
-    const uint4 p = r.pTab[i];  // {T, M, rank | L << 8, W[rank][0] + W[rank][1]}
-    if (p.x >= R) { nx = min(nx, p.x + 1u); break; }  // this and every later period: floor((R-1)/T) = 0
-    m &= m - 1;
-    const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
-    nx = min(nx, (q + 1u) * p.x + 1u);
+    const uint32_t i = f_hibit(m);
+    const uint4 p = r.pTab[31u - i];  // {T, M, L | rank << 8, W[rank][0] + W[rank][1]}
+    if (p.x >= R) { nm = min(nm, p.x); break; }  // this and every later period: floor((R-1)/T) = 0
+    m ^= 1u << i;
+    const uint32_t q = f_shr(__umulhi(h2, p.y), p.z);
+    nm = min(nm, q * p.x + p.x);
     uint32_t wu = p.w;
-    if (wsel) {  // not both of units 0 and 1: one unit (wsel = unit + 1), or the general unit union
-      const uint32_t k = p.z & 0xffu;
+    if (WSEL) {  // not both of units 0 and 1: one unit (wsel = unit + 1), or the general unit union
+      const uint32_t k = p.z >> 8;
       if (wsel <= MAXU) {
         wu = r.W[k][wsel - 1];
       } else {
@@ -115,49 +102,64 @@ __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uin
         for (uint32_t um = umask; um; um &= um - 1) wu = sadd(wu, r.W[k][__ffs(um) - 1]);
       }
     }
-    if (WIDE) {
-      acc += (uint64_t)q * wu;
-    } else {
-      const uint64_t pr = (uint64_t)q * wu;
-      acc += pr;
-      hi |= (uint32_t)(pr >> 32);
-    }
+    acc += (uint64_t)q * wu;
+    hi |= (uint32_t)(acc >> 32);
   }
+  return acc;
+}
+
+// One Eq.5 evaluation F_c(R) (Theorem 1, P:1126-1128) for R >= 1, with mu(R, T) = 2 + floor((R-1)/T)
+// (Eq.2): the mu = 2 parts come precomputed (A2 = base3 + 2 sum WU for Lemma 3, xs2 = 2 sum X_h of the
+// static interferers), and the floor parts are added only for periods T < R -- for the Lemma-3 chains
+// by walking their period positions (lmask) in ascending period order up to the first T >= R.
+// C = C_c(R) (Eq.4, union form A1), nH = H*_c(R) = min(S, C) + eps (Eq.1, P:1092), F = B + E + H* +
+// the hp / hpp interference (SAT = above the cutoff: UNSCHED, A4; then H* = SAT poisons dependants, A8).
+__device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uint32_t R, uint32_t lmask, uint32_t wsel,
+                                         uint32_t umask, uint32_t A2, uint32_t S, uint32_t eps, uint32_t BE, uint32_t cut,
+                                         uint32_t xm, uint32_t depm, uint32_t xs2, uint32_t xTmin, uint32_t& F,
+                                         uint32_t& nH, uint32_t& C, uint32_t& nxt) {
+  // nxt: the smallest R' > R at which a floor term floor((R' - 1) / T) differs from its value at R (a term
+  // with q = floor((R - 1) / T) changes at (q + 1) T + 1 < 2^32); below it F and C are those at R while
+  // the interferers' H* are unchanged (fused.cu f_eval).  nm = nxt - 1.
+  const uint32_t h2 = (R - 1u) << 1;
+  uint32_t hi = 0;
+  uint32_t nm = 0xfffffffeu;
+  uint64_t acc = wsel ? lemma3_terms<true>(r, R, h2, lmask, wsel, umask, hi, nm)
+                      : lemma3_terms<false>(r, R, h2, lmask, wsel, umask, hi, nm);
   acc += A2;
   C = (hi || acc > SAT) ? SAT : (uint32_t)acc;  // C_c(R), Eq.4
   nH = sadd(min(S, C), eps);                     // H*_c(R), Eq.1
   uint64_t xs = xs2;  // CPU interference (hp, hpp): the mu = 2 part of the static interferers
+  uint32_t xhi = 0;   // latched, as hi
   for (uint32_t m = depm; m; m &= m - 1) {  // X_h = E_h + H*_h at h's current iterate (hp, spinning hpp)
     const uint32_t h = __ffs(m) - 1;
     const uint32_t X = sadd(r.sE[h], w.Hs[h]);
     const uint4 p = r.pTab[w.sPos[h]];
-    const uint32_t q = p.x < R ? (__umulhi(h2, p.y) >> (p.z >> 8)) : 0u;
-    nx = min(nx, (q + 1u) * p.x + 1u);
-    const uint64_t pr = (uint64_t)(q + 2u) * X;
-    xs += pr;
-    if (!WIDE) hi |= (uint32_t)(pr >> 32);
+    const uint32_t q = p.x < R ? f_shr(__umulhi(h2, p.y), p.z) : 0u;
+    nm = min(nm, q * p.x + p.x);
+    xs += (uint64_t)(q + 2u) * X;
+    xhi |= (uint32_t)(xs >> 32);
   }
   if (R > xTmin) {  // the floor terms of suspending hpp interferers with T_h < R: X_h = E_h + eps_h
     for (uint32_t m = xm & ~depm; m; m &= m - 1) {
       const uint32_t h = __ffs(m) - 1;
       const uint4 p = r.pTab[w.sPos[h]];
       if (p.x < R) {
-        const uint32_t q = __umulhi(h2, p.y) >> (p.z >> 8);
-        nx = min(nx, (q + 1u) * p.x + 1u);
-        const uint64_t pr = (uint64_t)q * sadd(r.sE[h], r.sEps[h]);
-        xs += pr;
-        if (!WIDE) hi |= (uint32_t)(pr >> 32);
+        const uint32_t q = f_shr(__umulhi(h2, p.y), p.z);
+        nm = min(nm, q * p.x + p.x);
+        xs += (uint64_t)q * sadd(r.sE[h], r.sEps[h]);
+        xhi |= (uint32_t)(xs >> 32);
       } else {
-        nx = min(nx, p.x + 1u);
+        nm = min(nm, p.x);
       }
     }
   } else if (xTmin != 0xffffffffu) {
-    nx = min(nx, xTmin + 1u);
+    nm = min(nm, xTmin);
   }
-  nxt = nx;
+  nxt = nm + 1u;
   const uint64_t f = (uint64_t)BE + nH + xs;
-  F = (hi || f > cut) ? SAT : (uint32_t)f;  // above the cutoff: UNSCHED (A4)
-  if (F == SAT) nH = SAT;                   // dependants become UNSCHED as well (A8)
+  F = (hi || xhi || f > cut) ? SAT : (uint32_t)f;  // above the cutoff: UNSCHED (A4)
+  if (F == SAT) nH = SAT;                          // dependants become UNSCHED as well (A8)
 }
 
 // L2 prefetch of the next record while the current one is analysed.  Measured: 2.74 -> 2.63 ms per 2M
@@ -329,11 +331,11 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       const bool critical = act && ((r.cMisc[rk] >> 8) & 0xffu) == 0;
       bool sexact = !lazy_s;
       // period positions of the chains (pTab is in ascending period order)
-      if (lane < (int)nch) w.posOf[r.pTab[lane].z & 0xffu] = (uint8_t)lane;
+      if (lane < (int)nch) w.posOf[r.pTab[lane].z >> 8] = (uint8_t)lane;
       __syncwarp();
       // lmask: period positions of the chains of rank < rk (Lemma-3 interferers, Eq.4), an exclusive
-      // OR-scan over ranks of 1 << position
-      uint32_t pb = lane < (int)nch ? (1u << w.posOf[lane]) : 0u;
+      // OR-scan over ranks of 1 << (31 - position)
+      uint32_t pb = lane < (int)nch ? (0x80000000u >> w.posOf[lane]) : 0u;  // bit 31 - position
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(FULL, pb, o);
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       for (;;) {
         uint32_t F = R, nH = Hst, nxt = 0u;
         if (dirty)  // one checked copy (the unchecked one doubled the loop's code)
-          eval_eq5<false>(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
+          eval_eq5(r, w, R, lmask, wsel, umask, A2, S, eps, BE, cut, xm, depm, xs2, xTmin, F, nH, C, nxt);
         const bool chg = dirty && (F != R || nH != Hst);
         const uint32_t cm = __ballot_sync(FULL, chg);
         if (!cm) {

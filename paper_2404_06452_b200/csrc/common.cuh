@@ -57,6 +57,19 @@ __device__ __forceinline__ void ld_seg(const paam_batch& b, size_t g, uint32_t& 
     kind = b.seg_kind[g]; accel = b.seg_accel[g]; unit = b.seg_unit[g];
   }
 }
+// x >> (z mod 32) in one funnel shift (wrap mode): a magic-division shift L = ceil(log2 T) <= 31 kept in
+// the low 5 bits of a packed word (pTab.z, cMisc)
+__device__ __forceinline__ uint32_t f_shr(uint32_t x, uint32_t z) { return __funnelshift_r(x, 0u, z); }
+// the index of the highest set bit of m != 0 in one FLO (31 - __clz(m) compiles to three instructions)
+__device__ __forceinline__ uint32_t f_hibit(uint32_t m) {
+#ifdef PAAM_WARP_EMU
+  return 31u - (uint32_t)__clz(m);
+#else
+  uint32_t i;
+  asm("bfind.u32 %0, %1;" : "=r"(i) : "r"(m));
+  return i;
+#endif
+}
 __device__ __forceinline__ uint32_t smul(uint32_t a, uint32_t b) {
   const uint64_t p = (uint64_t)a * b;
   return p > SAT ? SAT : (uint32_t)p;
@@ -138,7 +151,7 @@ struct __align__(16) Record {
   uint32_t cMisc[MAXC];  // L (5 bits) | class << 8 | local index << 16 | n_sub << 24
   // the chains in period order (ascending T, ties by rank): mu(R, T) = 2 + floor((R-1)/T), and the
   // floor is non-zero only for T < R, so an Eq.5 iterate walks this list up to the first T >= R.
-  // One 16-byte entry: {T, mu magic multiplier M, rank | L << 8, W[rank][0] + W[rank][1] (saturated)}
+  // One 16-byte entry: {T, mu magic multiplier M, L | rank << 8, W[rank][0] + W[rank][1] (saturated)}
   uint4 pTab[MAXC];
   // W[k][u]: sum of A* of chain rank k's segments on unit u (exact regrouping of Eq.3/Eq.4 sums);
   // rank-major so that lanes reading different units of one chain hit different banks

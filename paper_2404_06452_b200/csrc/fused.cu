@@ -216,19 +216,6 @@ __device__ PAAM_COLD uint32_t f_sound_blocking(const FSmem& s, uint32_t B, uint3
   return B;
 }
 
-// x >> (z mod 32) in one funnel shift (wrap mode): z = L | rank << 8 with L = ceil(log2 T) <= 31
-__device__ __forceinline__ uint32_t f_shr(uint32_t x, uint32_t z) { return __funnelshift_r(x, 0u, z); }
-// the index of the highest set bit of m != 0 in one FLO (31 - __clz(m) compiles to three instructions)
-__device__ __forceinline__ uint32_t f_hibit(uint32_t m) {
-#ifdef PAAM_WARP_EMU
-  return 31u - (uint32_t)__clz(m);
-#else
-  uint32_t i;
-  asm("bfind.u32 %0, %1;" : "=r"(i) : "r"(m));
-  return i;
-#endif
-}
-
 // Eq.5 evaluation, as analyze.cu's eval_eq5 (see there), reading the shared period table.  nxt: the
 // smallest R' > R at which one of the floor terms floor((R' - 1) / T) differs from its value at R (a term
 // with q = floor((R - 1) / T) changes at R' = (q + 1) T + 1); below it F and C are those at R, as long

@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(WARPS * 32, PACK_MINB) pack_kernel(paam_batch 
         const uint32_t Tj = __shfl_sync(FULL, Tk, j);
         pos += (Tj < Tk) || (Tj == Tk && j < (uint32_t)lane);
       }
-      if (is_chain) r->pTab[pos] = uint4{Tk, M, (uint32_t)lane | (L << 8), sadd(s.W[lane][0], s.W[lane][1])};
+      if (is_chain) r->pTab[pos] = uint4{Tk, M, L | ((uint32_t)lane << 8), sadd(s.W[lane][0], s.W[lane][1])};
       // every period >= 64 ns: q * W < 2^62 / 64, so 64 such products cannot overflow a u64 sum
       if (lane == 0) r->hflags = 0u;
     }
