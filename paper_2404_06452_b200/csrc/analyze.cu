@@ -165,8 +165,39 @@ __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uin
 // L2 prefetch of the next record while the current one is analysed.  Measured: 2.74 -> 2.63 ms per 2M
 // sets, but the whole 4.4 KB slot is fetched where the staging reads only its live vectors (DRAM 3.24 ->
 // 4.18 KB per set; restricting it to the live lines was slower, 2.82 ms), so it is off by default.
+// The record's 16-byte vectors and which of them are live (analyze_kernel stages only those): the
+// header's counts decide, per array, how many leading vectors are live (pack writes nothing past them,
+// and nothing in analyze reads past them).
+constexpr int REC_NV = sizeof(Record) / 16;
+constexpr int V_CH = offsetof(Record, cCut) / 16, V_P = offsetof(Record, pTab) / 16;
+constexpr int V_W = offsetof(Record, W) / 16;
+constexpr int V_SUB = offsetof(Record, sE) / 16, V_SEG = offsetof(Record, aBase2) / 16;
+constexpr int V_SND = offsetof(Record, aEps) / 16;  // aEps, aCbE: sound blocking only
+static_assert(V_CH == 2 && V_P - V_CH == 4 * MAXC / 4 && V_W - V_P == MAXC && V_SEG - V_SUB == 10 * MAXS / 4 &&
+                  V_SND - V_SEG == 2 * MAXA / 4 && REC_NV - V_SEG == 4 * MAXA / 4 && MAXU == 8 && MAXC == 32 &&
+                  MAXS == 32,
+              "live-vector map assumes the Record layout in common.cuh");
+__device__ __forceinline__ void rec_counts(uint32_t hdr, uint32_t& nc, uint32_t& vc, uint32_t& vs, uint32_t& va) {
+  nc = hdr & 0xffu;
+  vc = (nc + 3) >> 2;
+  vs = (((hdr >> 8) & 0xffu) + 3) >> 2;
+  va = (((hdr >> 16) & 0xffu) + 3) >> 2;
+}
+__device__ __forceinline__ bool rec_live(int i, uint32_t nc, uint32_t vc, uint32_t vs, uint32_t va, bool sound) {
+  return i < V_CH    ? true
+         : i < V_P   ? (uint32_t)((i - V_CH) & (MAXC / 4 - 1)) < vc
+         : i < V_W   ? (uint32_t)(i - V_P) < nc  // one period-table entry per vector
+         : i < V_SUB ? (uint32_t)((i - V_W) >> 1) < nc  // W row k = 2 vectors
+         : i < V_SEG ? (uint32_t)((i - V_SUB) & (MAXS / 4 - 1)) < vs
+         : i < REC_NV ? (uint32_t)((i - V_SEG) & (MAXA / 4 - 1)) < va && (i < V_SND || sound)
+                      : false;
+}
+
 #ifndef ANA_PF
-#define ANA_PF 0
+// L2 prefetch of the next record (one line per lane) while this one is solved: measured 2.625 -> 2.524 ms
+// per 2M sets; it also fetches the record's dead tails (tools/ana_pf_ab.sh; prefetching only the live
+// lines cost more instructions than it saved: 2.649 ms)
+#define ANA_PF 1
 #endif
 #ifndef ANA_MINB
 #define ANA_MINB 4
@@ -209,17 +240,9 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
     {
       const uint4* src = reinterpret_cast<const uint4*>(recs + set);
       uint4* dst = reinterpret_cast<uint4*>(&r);
-      constexpr int NV = sizeof(Record) / 16;
-      constexpr int V_CH = offsetof(Record, cCut) / 16, V_P = offsetof(Record, pTab) / 16;
-      constexpr int V_W = offsetof(Record, W) / 16;
-      constexpr int V_SUB = offsetof(Record, sE) / 16, V_SEG = offsetof(Record, aBase2) / 16;
-      constexpr int V_SND = offsetof(Record, aEps) / 16;  // aEps, aCbE: sound blocking only
-      static_assert(V_CH == 2 && V_P - V_CH == 4 * MAXC / 4 && V_W - V_P == MAXC && V_SEG - V_SUB == 10 * MAXS / 4 &&
-                        V_SND - V_SEG == 2 * MAXA / 4 && NV - V_SEG == 4 * MAXA / 4 && MAXU == 8 && MAXC == 32 &&
-                        MAXS == 32,
-                    "live-vector map assumes the Record layout in common.cuh");
-      const uint32_t nc = hdr & 0xffu, vc = (nc + 3) >> 2, vs = (((hdr >> 8) & 0xffu) + 3) >> 2;
-      const uint32_t va = (((hdr >> 16) & 0xffu) + 3) >> 2;
+      constexpr int NV = REC_NV;
+      uint32_t nc, vc, vs, va;
+      rec_counts(hdr, nc, vc, vs, va);
       // Predicated loads in groups of four, all issued before their stores (one round trip per group).
       constexpr int NK = (NV + 31) / 32;
 #pragma unroll
@@ -229,13 +252,7 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           const int i = lane + 32 * (k0 + k);
-          const bool live = i < V_CH    ? true
-                            : i < V_P   ? (uint32_t)((i - V_CH) & (MAXC / 4 - 1)) < vc
-                            : i < V_W   ? (uint32_t)(i - V_P) < nc  // one period-table entry per vector
-                            : i < V_SUB ? (uint32_t)((i - V_W) >> 1) < nc  // W row k = 2 vectors
-                            : i < V_SEG ? (uint32_t)((i - V_SUB) & (MAXS / 4 - 1)) < vs
-                            : i < NV    ? (uint32_t)((i - V_SEG) & (MAXA / 4 - 1)) < va && (i < V_SND || sound)
-                                        : false;
+          const bool live = rec_live(i, nc, vc, vs, va, sound);
           livem |= (uint32_t)live << k;
           v[k] = live ? __ldg(src + i) : uint4{0u, 0u, 0u, 0u};
         }
@@ -257,8 +274,9 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
     const uint32_t nhdr = nset < n ? __ldg(hdr_base + (size_t)nset * HDR_STRIDE) : 0u;
 #if ANA_PF && !defined(PAAM_WARP_EMU)
     if (nset < n) {  // the next record into L2, one 128-byte line per lane
-      const char* nr = reinterpret_cast<const char*>(recs + nset) + 128u * lane;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(nr));
+      const uintptr_t base = reinterpret_cast<uintptr_t>(recs + nset);
+      const uintptr_t la = (base & ~(uintptr_t)127) + 128u * lane;
+      if (la < base + sizeof(Record)) asm volatile("prefetch.global.L2 [%0];" ::"l"(la));
     }
 #endif
     __syncwarp();
