@@ -4,6 +4,7 @@ import csv, io, subprocess, sys
 from collections import defaultdict
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+key = 0 if len(sys.argv) > 4 and sys.argv[4] == "inst" else 1  # sort by instructions or by stall samples
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda", "-k", "regex:" + kre],
                      capture_output=True, text=True).stdout
 agg = defaultdict(lambda: [0, 0, ""])
@@ -33,5 +34,5 @@ for r in csv.reader(io.StringIO(out)):
 tot_i = sum(v[0] for v in agg.values()) or 1
 tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total inst {tot_i}  samples {tot_s}")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
     print(f"{k[0]}:{k[1]:4d} inst {100*v[0]/tot_i:5.1f}%  stall {100*v[1]/tot_s:5.1f}%  {v[2].strip()}")
