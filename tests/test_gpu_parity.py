@@ -415,6 +415,40 @@ def test_wide_time_sets_take_the_u64_path(flags):
     assert gw.tolist() == [x * 1000 for x in GOLD["two_chains_one_executor"]["R"]]
 
 
+@pytest.mark.parametrize("flags", [0, 1])
+def test_u32_path_overflowing_sums(flags):
+    """Sets that stay on the u32 kernels (every time < 2^31 - 1 ns, A14) but whose Lemma-2 / Lemma-3 / Eq.5
+    sums pass 2^32: times scaled up to just below 2^31 and the CPU and accelerator WCETs of random chains
+    multiplied up to 64x (utilisation far above 1), so the floor-term products reach ~2^51 and the 64-bit
+    sums' latched high words decide saturation (UNSCHED, A4).  Every WCRT, verdict, status and bin equals
+    the oracle's (exact u64 arithmetic), split and fused paths."""
+    rng = random.Random(4242 + flags)
+    lim = (1 << 31) - 1
+    systems = []
+    for i in range(2000):
+        s = random_small_system(rng, max_chains=6, tmax=200)
+        for ch in s.chains:
+            if rng.random() < 0.4:
+                k = rng.choice([2, 8, 64])
+                for c in ch.cbs:
+                    for g in c.segs:
+                        g.wcet *= k
+        top = max([c.T for c in s.chains] + [c.D for c in s.chains] + [g.wcet for c in s.chains for x in c.cbs
+                   for g in x.segs] + [e for a in s.accels for e in a[3:5]] + [1])
+        target = rng.choice([lim - 1, lim - 1, 1 << 30, (1 << 29) + rng.randrange(1 << 20)])
+        s = _scaled(s, max(1, target // top))
+        systems.append(s)
+    for i, s in enumerate(systems):
+        s.bin = i % 5
+    b = flatten(systems, comm_cost=rng.choice([0, 5, 1 << 20]), flags=flags, n_bins=5)
+    times = [b["chain_T"], b["chain_D"], b["seg_wcet"], b["accel_eps"], b["accel_kappa"]]
+    assert max(int(t.max()) for t in times if t.size) < lim  # every set on the u32 kernels
+    assert int(b["chain_T"].max()) > (1 << 30)
+    ow, osch, ost, _ = O.analyze(b, nthreads=NPROC)
+    assert (ow == O.UNSCHED).sum() > 1000 and osch.sum() > 100  # both outcomes well represented
+    assert_same(b, gpu_device_path(b))
+
+
 def test_wide_time_sets_admission_and_des_status():
     """paam_admit decides wide sets on the u64 path too; the DES reports them PAAM_SIM_WIDE (it computes in
     32-bit time distances) and simulates the others."""
