@@ -273,8 +273,9 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
   uint64_t xs = xs2;
   uint32_t xhi = 0;
   #pragma unroll 1
-  for (uint32_t m = depm; m; m &= m - 1) {
-    const uint32_t h = __ffs(m) - 1;
+  for (uint32_t m = depm; m;) {  // order-free sums and minima: walked from the highest bit (one FLO)
+    const uint32_t h = f_hibit(m);
+    m ^= 1u << h;
     const uint32_t X = sadd(s.sE[h], s.Hs[h]);
     const uint4 p = s.pTab[s.sPos[h]];
     const uint32_t q = p.x < R ? (f_shr(__umulhi(h2, p.y), p.z)) : 0u;
@@ -284,8 +285,9 @@ __device__ __forceinline__ void f_eval(const FSmem& s, uint32_t R, uint32_t lmas
   }
   if (R > xTmin) {
     #pragma unroll 1
-    for (uint32_t m = xm & ~depm; m; m &= m - 1) {
-      const uint32_t h = __ffs(m) - 1;
+    for (uint32_t m = xm & ~depm; m;) {
+      const uint32_t h = f_hibit(m);
+      m ^= 1u << h;
       const uint4 p = s.pTab[s.sPos[h]];
       if (p.x < R) {
         const uint32_t q = f_shr(__umulhi(h2, p.y), p.z);
@@ -538,8 +540,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         const uint32_t same_core = __match_any_sync(FULL, xcore) & ~(1u << lane);
         uint32_t pr = 0, m = lane < (int)nex ? same_core : 0u;
         while (m) {
-          const uint32_t y = __ffs(m) - 1;
-          m &= m - 1;
+          const uint32_t y = f_hibit(m);
+          m ^= 1u << y;
           const uint32_t py = s.xPrio[y];
           edup |= (py == xprio);
           pr += (py > xprio);
@@ -759,19 +761,23 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         }
         A2 = base3;
         #pragma unroll 1
-        for (uint32_t um = umask; um; um &= um - 1) A2 = sadd(A2, s.pre2[__ffs(um) - 1][rk]);
+        for (uint32_t um = umask; um;) {
+          const uint32_t u = f_hibit(um);
+          um ^= 1u << u;
+          A2 = sadd(A2, s.pre2[u][rk]);
+        }
         uint32_t m = same_exec & ~(1u << lane);
         while (m) {
-          const uint32_t l = __ffs(m) - 1;
-          m &= m - 1;
+          const uint32_t l = f_hibit(m);
+          m ^= 1u << l;
           if (s.sRank[l] < rk) hpm |= 1u << l;
           else { lpm |= 1u << l; B = max(B, s.sMaxE[l]); }  // B_c
         }
         m = same_core & ~same_exec;
         const uint32_t mypp = s.xPPrank[s_exec];
         while (m) {
-          const uint32_t l = __ffs(m) - 1;
-          m &= m - 1;
+          const uint32_t l = f_hibit(m);
+          m ^= 1u << l;
           if (s.xPPrank[s.sExec[l]] < mypp) hppm |= 1u << l;
         }
         spin = s.xWait[s_exec] == 1;
@@ -825,8 +831,9 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       __syncwarp();
       if (act) {
         #pragma unroll 1
-        for (uint32_t m = xm & ~depm; m; m &= m - 1) {
-          const uint32_t h = __ffs(m) - 1;
+        for (uint32_t m = xm & ~depm; m;) {
+          const uint32_t h = f_hibit(m);
+          m ^= 1u << h;
           xs2 = sadd(xs2, sadd(s.sE[h], s.sEps[h]));
           xTmin = min(xTmin, s.pTab[s.sPos[h]].x);
         }
