@@ -131,8 +131,9 @@ __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uin
   nH = sadd(min(S, C), eps);                     // H*_c(R), Eq.1
   uint64_t xs = xs2;  // CPU interference (hp, hpp): the mu = 2 part of the static interferers
   uint32_t xhi = 0;   // latched, as hi
-  for (uint32_t m = depm; m; m &= m - 1) {  // X_h = E_h + H*_h at h's current iterate (hp, spinning hpp)
-    const uint32_t h = __ffs(m) - 1;
+  for (uint32_t m = depm; m;) {  // X_h = E_h + H*_h at h's current iterate (hp, spinning hpp); order-free
+    const uint32_t h = f_hibit(m);
+    m ^= 1u << h;
     const uint32_t X = sadd(r.sE[h], w.Hs[h]);
     const uint4 p = r.pTab[w.sPos[h]];
     const uint32_t q = p.x < R ? f_shr(__umulhi(h2, p.y), p.z) : 0u;
@@ -141,8 +142,9 @@ __device__ __forceinline__ void eval_eq5(const Record& r, const WarpSmem& w, uin
     xhi |= (uint32_t)(xs >> 32);
   }
   if (R > xTmin) {  // the floor terms of suspending hpp interferers with T_h < R: X_h = E_h + eps_h
-    for (uint32_t m = xm & ~depm; m; m &= m - 1) {
-      const uint32_t h = __ffs(m) - 1;
+    for (uint32_t m = xm & ~depm; m;) {
+      const uint32_t h = f_hibit(m);
+      m ^= 1u << h;
       const uint4 p = r.pTab[w.sPos[h]];
       if (p.x < R) {
         const uint32_t q = f_shr(__umulhi(h2, p.y), p.z);
@@ -375,8 +377,9 @@ __global__ void __launch_bounds__(AW * 32, ANA_MINB) analyze_kernel(const Record
       uint32_t xs2 = 0, xTmin = 0xffffffffu;
       if (act) {
         w.sPos[lane] = w.posOf[rk];
-        for (uint32_t m = xm & ~depm; m; m &= m - 1) {
-          const uint32_t h = __ffs(m) - 1;
+        for (uint32_t m = xm & ~depm; m;) {
+          const uint32_t h = f_hibit(m);
+          m ^= 1u << h;
           xs2 = sadd(xs2, sadd(r.sE[h], r.sEps[h]));
           xTmin = min(xTmin, r.pTab[w.posOf[r.sMisc[h] & 0xffu]].x);
         }

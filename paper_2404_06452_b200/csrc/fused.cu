@@ -115,6 +115,8 @@ struct FSmem {
   };
 };
 
+static_assert(offsetof(FSmem, maxA) % 16 == 0 && sizeof(FSmem::maxA) >= MAXC * sizeof(uint2),
+              "the chain-rank pass reads (priority, period) pairs from maxA's space as 16-byte vectors");
 #ifdef PAAM_EMU_STATS
 unsigned long long emu_stats[8];  // debugging statistics of the host emulation (never on the device)
 #endif
@@ -518,18 +520,25 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
       {  // chain ranks and period positions (ascending T; equal periods by chain index), one pass
         uint32_t rk = 0, below = 0;
         const uint32_t Tme = lane < (int)nch ? T : 0xffffffffu;
+        // (priority, period) of every chain through maxA's space (dead until the per-chain pass of the
+        // derivation; 16-byte aligned after W): one 16-byte broadcast load per two chains instead of four
+        // shuffles
+        uint2* const pt = reinterpret_cast<uint2*>(&s.maxA[0][0]);
+        pt[lane] = uint2{prio, Tme};
+        __syncwarp();
         uint32_t d = 0;
         #pragma unroll 1
-        for (; d + 1 < nch; d += 2) {  // two chains per trip: the four shuffles in flight together
-          const uint32_t p0 = __shfl_sync(FULL, prio, d), p1 = __shfl_sync(FULL, prio, d + 1);
-          const uint32_t t0 = __shfl_sync(FULL, Tme, d), t1 = __shfl_sync(FULL, Tme, d + 1);
-          rk += (uint32_t)(p0 > prio) + (uint32_t)(p1 > prio);
-          below += (uint32_t)(t0 < Tme) + (uint32_t)(t1 < Tme);
+        for (; d + 1 < nch; d += 2) {
+          const uint4 v = reinterpret_cast<const uint4*>(pt)[d >> 1];  // chains d, d + 1
+          rk += (uint32_t)(v.x > prio) + (uint32_t)(v.z > prio);
+          below += (uint32_t)(v.y < Tme) + (uint32_t)(v.w < Tme);
         }
         if (d < nch) {
-          rk += (__shfl_sync(FULL, prio, d) > prio);
-          below += (__shfl_sync(FULL, Tme, d) < Tme);
+          const uint2 v = pt[d];
+          rk += (v.x > prio);
+          below += (v.y < Tme);
         }
+        __syncwarp();  // pt is overwritten by the derivation
         rank = rk;
         ppos = below + __popc(__match_any_sync(FULL, Tme) & lt);
         const uint32_t valid = nch >= 32 ? FULL : (1u << nch) - 1u;
