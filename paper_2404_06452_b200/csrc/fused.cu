@@ -434,13 +434,15 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         s.xWait[lane] = (uint8_t)w;
       }
       __syncwarp();
-      uint32_t units_pack;  // byte a: the units of accelerator a (a < nac <= 4; u <= 255 as loaded)
+      uint32_t units_pack, servers_pack;  // byte a: the units / server core of accelerator a (a < nac <= 4)
       {
         const uint32_t u = lane < (int)nac ? s.aUnits[lane] : 0u;
         const uint32_t ub = f_scan_excl(u, lane);
         if (lane < (int)nac) s.aUbase[lane] = ub;
         n_unit = __reduce_add_sync(FULL, u);
         units_pack = __reduce_or_sync(FULL, lane < 4 ? u << (8 * lane) : 0u);
+        const uint32_t sv = lane < (int)nac ? s.aServer[lane] : 0u;
+        servers_pack = __reduce_or_sync(FULL, lane < 4 ? sv << (8 * lane) : 0u);
       }
       const uint64_t cstart_bit = (lane < (int)nch && cbo < 64) ? (1ull << cbo) : 0ull;
       cstart = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(cstart_bit >> 32)) << 32) |
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         const bool isacc = kind == 1u;
         eaccel |= isacc && a >= nac;
         edang |= isacc && a < nac && u >= ((units_pack >> ((a & 3u) << 3)) & 0xffu);
-        s.gW[i] = (uint32_t)min(w, (uint64_t)SAT);
+        s.gW[i] = (uint32_t)w;  // exact unless the set is ERANGE or wide (its derived values are never used)
         // kind bit: an ACCEL segment (an undefined kind is ESHAPE, counted as no accelerator segment); the
         // accelerator / unit bits are read only for valid sets, where they fit
         s.gMeta[i] = (uint8_t)((kind == 1u ? 1u : 0u) | (a << 1) | (u << 3));
@@ -489,11 +491,13 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
               na++;
             }
           }
-          s.bExec[j] = (uint8_t)min(exec, 255u);
+          // na <= nseg <= MAXSEG < 256, fa < 4, fu < 32; an executor >= 256 is EDANGLING, which precedes
+          // the A13 rule that reads bExec
+          s.bExec[j] = (uint8_t)exec;
           s.bE[j] = E;
-          s.bNa[j] = (uint8_t)min(na, 255u);
-          s.bFa[j] = (uint8_t)min(fa, 255u);
-          s.bFu[j] = (uint8_t)min(fu, 255u);
+          s.bNa[j] = (uint8_t)na;
+          s.bFa[j] = (uint8_t)fa;
+          s.bFu[j] = (uint8_t)fu;
           s.bFw[j] = fw;
         }
         uint32_t pe = __shfl_up_sync(FULL, exec, 1);
@@ -557,8 +561,8 @@ __global__ void __launch_bounds__(FW * 32, FUSED_MINB)
         }
         if (lane < (int)nex) {
           s.xPPrank[lane] = (uint8_t)pr;
-          #pragma unroll 1
-          for (uint32_t a = 0; a < nac; a++) ecore |= (xcore == s.aServer[a]);
+          const uint32_t vmask = nac >= 4 ? FULL : (1u << (8 * nac)) - 1u;  // the bytes of accelerators 0..nac-1
+          ecore |= (__vcmpeq4(servers_pack, xcore * 0x01010101u) & vmask) != 0u;
         }
       }
       erange |= (n_aseg > MAXA) || (n_unit > MAXU);
